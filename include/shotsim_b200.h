@@ -1,0 +1,221 @@
+/*
+ * shotsim_b200 — C ABI of the B200-native multi-shot statevector engine.
+ *
+ * This is the drop-in boundary for the reference's executor plugin API:
+ *
+ *   using ExecutorFn = RunResult (*)(const NoisyCircuit&, const RunOptions&);
+ *   ExecutorFn executor_by_name(std::string_view);
+ *       (reference: proj/include/shotsim/exec.hpp:32-35, registry
+ *        proj/src/exec_naive.cpp:22-27)
+ *
+ * A NoisyCircuit (proj/include/shotsim/program.hpp:18-70) crosses this ABI
+ * either as the reference's own lossless text/JSON inputs
+ * (ssb_program_from_text: circuit_io.cpp:53-146 + noise.cpp:328-365 +
+ * instrument, program.cpp:17-122) or already instrumented and flattened
+ * (ssb_program_from_flat). Runs return one classical-register value per shot
+ * for the contiguous shot-id range [shot_begin, shot_begin + shot_count),
+ * exactly RunResult::shot_values (result.hpp:45-47) restricted to that range,
+ * so shards and sub-samples compose by concatenation.
+ *
+ * Conventions: plain pointers and sizes only; every function returns
+ * SSB_OK (0) or a nonzero ssb_status; ssb_last_error() (thread-local) holds
+ * the message. Status codes mirror the reference's exception types
+ * (common.hpp:18-34; std::invalid_argument for bad arguments).
+ * All device work is sm_100a CUDA; there is no CPU execution path — without a
+ * usable CUDA device every run entry point fails with SSB_ERR_CUDA.
+ */
+#ifndef SHOTSIM_B200_H_
+#define SHOTSIM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SSB_API __attribute__((visibility("default")))
+#else
+#define SSB_API
+#endif
+
+#define SSB_ABI_VERSION 1
+
+typedef enum ssb_status {
+  SSB_OK = 0,
+  SSB_ERR_RUNTIME = 1,          /* std::runtime_error (e.g. norm drift)        */
+  SSB_ERR_INVALID_ARGUMENT = 2, /* std::invalid_argument                       */
+  SSB_ERR_CONFIG = 3,           /* shotsim::ConfigError                        */
+  SSB_ERR_CAPACITY = 4,         /* shotsim::CapacityError                      */
+  SSB_ERR_DEGENERATE = 5,       /* shotsim::DegenerateDistribution             */
+  SSB_ERR_CUDA = 6              /* no device / CUDA failure (no CPU fallback)  */
+} ssb_status;
+
+/* ProgramOp::Kind (program.hpp:19) */
+typedef enum ssb_op_kind {
+  SSB_OP_GATE = 0,
+  SSB_OP_PAULI = 1,
+  SSB_OP_KRAUS = 2,
+  SSB_OP_MEASURE = 3,
+  SSB_OP_RESET = 4,
+  SSB_OP_BARRIER = 5
+} ssb_op_kind;
+
+#define SSB_MAX_OP_QUBITS 4
+
+/* One ProgramOp, flattened. Matrices live in ssb_flat_program.matrices as
+ * row-major 2^k x 2^k complex (re, im) doubles; qubits[0] is the low matrix
+ * axis (statevector.hpp:40). */
+typedef struct ssb_flat_op {
+  uint32_t kind;          /* ssb_op_kind                                   */
+  uint32_t num_qubits;    /* operand count                                 */
+  uint32_t qubits[SSB_MAX_OP_QUBITS];
+  uint32_t clbits[SSB_MAX_OP_QUBITS]; /* MEASURE only                      */
+  uint32_t has_condition;
+  uint32_t gate_kind;     /* GateKind (circuit.hpp:17-19) for GATE         */
+  uint64_t cond_mask;     /* Condition::clbit_mask (circuit.hpp:33-39)     */
+  uint64_t cond_value;
+  uint64_t event;         /* randomness-site index (PAULI/KRAUS/MEAS/RESET)*/
+  uint32_t matrix;        /* GATE: matrix index                            */
+  uint32_t channel;       /* KRAUS: channel index                          */
+  uint32_t term_begin;    /* PAULI: first term in ssb_flat_program.terms   */
+  uint32_t term_count;
+} ssb_flat_op;
+
+/* PauliSite term: ProgramOp::term_cum/term_masks/term_identity
+ * (program.hpp:34-37), PauliMasks (kernels.hpp:15-22). */
+typedef struct ssb_flat_term {
+  double cumulative;
+  uint64_t x_mask;
+  uint64_t z_mask;
+  uint32_t num_y;
+  uint32_t x_max;
+  uint32_t identity;
+  uint32_t reserved;
+} ssb_flat_term;
+
+/* KrausError (noise.hpp:54-57): num_matrices consecutive matrices. */
+typedef struct ssb_flat_channel {
+  uint32_t arity;
+  uint32_t num_matrices;
+  uint32_t matrix_begin;
+  uint32_t reserved;
+} ssb_flat_channel;
+
+typedef struct ssb_flat_program {
+  uint32_t num_qubits;
+  uint32_t num_clbits;
+  uint64_t num_events;
+  uint32_t has_measure;
+  uint32_t sampling_eligible;
+  uint64_t terminal_measure_begin;
+  uint64_t num_ops;
+  const ssb_flat_op* ops;
+  uint64_t num_terms;
+  const ssb_flat_term* terms;
+  uint64_t num_channels;
+  const ssb_flat_channel* channels;
+  uint64_t num_matrices;
+  const double* matrices;           /* num_matrices * 32 doubles (4x4 slot) */
+  uint32_t num_sample_qubits;
+  const uint32_t* sample_qubits;
+  uint32_t num_sample_writes;
+  const uint32_t* sample_write_clbit; /* sample_writes[i].first  */
+  const uint32_t* sample_write_pos;   /* sample_writes[i].second */
+} ssb_flat_program;
+
+#define SSB_MATRIX_STRIDE 32 /* doubles per matrix slot (4x4 complex) */
+
+typedef struct ssb_program ssb_program;
+typedef struct ssb_engine ssb_engine;
+typedef struct ssb_batch ssb_batch;
+
+/* RunOptions (exec.hpp:12-22) minus the CPU-only knobs. */
+typedef struct ssb_run_options {
+  uint64_t max_batch_size;   /* 0: derive from mem_limit_bytes                 */
+  uint64_t branch_budget;    /* gpu-branch: max live states (>= 1)             */
+  uint64_t mem_limit_bytes;  /* 0: SHOTSIM_MEM_LIMIT_BYTES or 90% of free HBM  */
+  uint32_t check_norms;      /* reserved (debug norm checks)                   */
+  uint32_t collect_leaf_stats;
+  uint32_t resident_max_qubits; /* n <= this: whole program SM-resident (0: 13) */
+  uint32_t tile_qubits;      /* streamed mode: local qubits per HBM tile (0: 12) */
+} ssb_run_options;
+
+typedef struct ssb_stats {
+  uint64_t dispatch_count;   /* kernel launches issued by the run             */
+  uint64_t peak_states;      /* concurrently live segments / branch states    */
+  uint64_t passes;           /* branch: passes; batch: shot waves             */
+  uint64_t fused_passes;     /* batch: HBM tile passes per wave               */
+  double device_seconds;     /* CUDA-event time of the device work            */
+  double wall_seconds;
+} ssb_stats;
+
+SSB_API const char* ssb_last_error(void);
+SSB_API int ssb_abi_version(void);
+
+/* ---- program lowering (host) ------------------------------------------ */
+/* circuit_text: reference circuit text (circuit_io.hpp:13-27) or JSON
+ * (leading '{'); noise_json: NoiseModel JSON (noise.cpp:328-365), "" for no
+ * noise, or {"model":"depolarizing","rate":r,"as_kraus":b}
+ * (make_depolarizing_model, noise.cpp:375-392). Runs instrument(). */
+SSB_API int ssb_program_from_text(const char* circuit_text, const char* noise_json,
+                                  ssb_program** out);
+SSB_API int ssb_program_from_flat(const ssb_flat_program* flat, ssb_program** out);
+SSB_API void ssb_program_destroy(ssb_program* program);
+/* Borrowed view, valid while the program lives. */
+SSB_API int ssb_program_flat(const ssb_program* program, ssb_flat_program* out);
+/* Exact text dump (doubles as %a) in the format of oracle/ref_shim.cpp. */
+SSB_API int ssb_program_dump(const ssb_program* program, char* buf, size_t cap, size_t* len);
+/* Writes counts_checksum (result.cpp:23-38) of the histogram of `values`. */
+SSB_API int ssb_counts_checksum(const uint64_t* values, uint64_t count, uint32_t num_clbits,
+                                uint32_t has_measure, uint64_t* checksum_out,
+                                uint64_t* num_keys_out);
+
+/* ---- engine (device) -------------------------------------------------- */
+SSB_API int ssb_engine_create(int device, ssb_engine** out);
+SSB_API void ssb_engine_destroy(ssb_engine* engine);
+/* Opaque cudaStream_t the engine launches on (for CUDA-event timing). */
+SSB_API void* ssb_engine_stream(ssb_engine* engine);
+
+/* gpu-batch (paper SIV.A; exec_batch.cpp:229-287): per-shot values for ids
+ * [shot_begin, shot_begin+shot_count) into HOST memory values_out. */
+SSB_API int ssb_run_batch(ssb_engine* engine, const ssb_program* program, uint64_t shot_begin,
+                          uint64_t shot_count, uint64_t seed, const ssb_run_options* options,
+                          uint64_t* values_out, ssb_stats* stats);
+/* Same, values_out_device is a DEVICE pointer; no host sync at the end. */
+SSB_API int ssb_run_batch_device(ssb_engine* engine, const ssb_program* program,
+                                 uint64_t shot_begin, uint64_t shot_count, uint64_t seed,
+                                 const ssb_run_options* options, uint64_t* values_out_device,
+                                 ssb_stats* stats);
+/* gpu-branch (paper SIV.B; exec_branch.cpp:175-295). */
+SSB_API int ssb_run_branch(ssb_engine* engine, const ssb_program* program, uint64_t shot_begin,
+                           uint64_t shot_count, uint64_t seed, const ssb_run_options* options,
+                           uint64_t* values_out, ssb_stats* stats);
+
+/* Dense histogram of device values (num_clbits <= 24) into a device array of
+ * 2^num_clbits uint64 (accumulating) — the payload of the multi-GPU gather. */
+SSB_API int ssb_histogram_device(ssb_engine* engine, const uint64_t* values_device,
+                                 uint64_t count, uint32_t num_clbits, uint64_t* hist_device);
+
+/* ---- operator-level entry points (BatchState, exec_batch.hpp:22-84) ---- */
+/* A device-resident batch over arbitrary shot ids, initialised to |0...0>. */
+SSB_API int ssb_batch_create(ssb_engine* engine, const ssb_program* program,
+                             const uint64_t* shot_ids, uint64_t count, uint64_t seed,
+                             ssb_batch** out);
+SSB_API void ssb_batch_destroy(ssb_batch* batch);
+/* Apply program op `op_index` to every shot. u: per-shot draws replacing the
+ * keyed stream (the *_with test hooks, exec_batch.hpp:57-62), or NULL. */
+SSB_API int ssb_batch_apply_op(ssb_batch* batch, uint64_t op_index, const double* u);
+/* BatchState::run (exec_batch.cpp:200-227) incl. terminal sampling. */
+SSB_API int ssb_batch_run(ssb_batch* batch);
+/* amps: count * 2^n complex (re,im) doubles; either output may be NULL. */
+SSB_API int ssb_batch_read(ssb_batch* batch, double* amps, uint64_t* cregs);
+SSB_API int ssb_batch_write_segment(ssb_batch* batch, uint64_t s, const double* amps);
+SSB_API uint64_t ssb_batch_dispatches(const ssb_batch* batch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHOTSIM_B200_H_ */

@@ -1,0 +1,276 @@
+"""Python host mirror of the reference's run API over the C ABI.
+
+Mirrors ``RunOptions`` / ``RunResult`` / ``executor_by_name`` (exec.hpp:12-38)
+and ``BatchState`` (exec_batch.hpp:22-84) so parity tests read like the
+reference's own tests. Programs are built from the reference's lossless
+circuit text + noise JSON (``Program.from_text``); every run executes on the
+GPU through ``libshotsim_b200.so`` — there is no CPU execution path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, load
+
+
+class Program:
+    """An instrumented program (NoisyCircuit, program.hpp:42-70)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    @classmethod
+    def from_text(cls, circuit_text: str, noise_json: str = "") -> "Program":
+        h = C.c_void_p()
+        check(load().ssb_program_from_text(circuit_text.encode(), noise_json.encode(), C.byref(h)))
+        return cls(h.value)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            try:
+                load().ssb_program_destroy(self._h)
+            except Exception:
+                pass
+            self._h = C.c_void_p()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def flat(self) -> _lib.FlatProgram:
+        f = _lib.FlatProgram()
+        check(load().ssb_program_flat(self._h, C.byref(f)))
+        return f
+
+    def dump(self) -> str:
+        n = C.c_size_t()
+        check(load().ssb_program_dump(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(load().ssb_program_dump(self._h, buf, n.value + 1, None))
+        return buf.value.decode()
+
+    @property
+    def num_qubits(self) -> int:
+        return self.flat().num_qubits
+
+    @property
+    def num_clbits(self) -> int:
+        return self.flat().num_clbits
+
+    @property
+    def num_events(self) -> int:
+        return self.flat().num_events
+
+    @property
+    def has_measure(self) -> bool:
+        return bool(self.flat().has_measure)
+
+    @property
+    def sampling_eligible(self) -> bool:
+        return bool(self.flat().sampling_eligible)
+
+    def ops(self) -> List[_lib.FlatOp]:
+        f = self.flat()
+        return [f.ops[i] for i in range(f.num_ops)]
+
+
+@dataclass
+class RunOptions:
+    shots: int = 1
+    seed: int = 0
+    workers: int = 1            # GPUs for the executor shim; the Python API runs one engine
+    max_batch_size: int = 0
+    branch_budget: int = 64
+    mem_limit_bytes: int = 0
+    record_shot_values: bool = False
+    check_norms: bool = False
+    collect_leaf_stats: bool = False
+    resident_max_qubits: int = 0  # tuning: 0 = engine default
+    tile_qubits: int = 0
+
+    def to_c(self) -> _lib.RunOptionsC:
+        return _lib.RunOptionsC(self.max_batch_size, self.branch_budget, self.mem_limit_bytes,
+                                int(self.check_norms), int(self.collect_leaf_stats),
+                                self.resident_max_qubits, self.tile_qubits)
+
+
+@dataclass
+class BranchStats:
+    peak_states: int = 0
+    passes: int = 0
+
+
+@dataclass
+class RunResult:
+    counts: Dict[str, int]
+    shot_values: Optional[np.ndarray]
+    dispatch_count: int = 0
+    peak_states: int = 0
+    branch: BranchStats = field(default_factory=BranchStats)
+    strategy: str = ""
+    shots: int = 0
+    seed: int = 0
+    device_seconds: float = 0.0
+    wall_seconds: float = 0.0
+    fused_passes: int = 0
+
+
+def bitstring(value: int, width: int) -> str:
+    """result.cpp:7-13 — MSB first."""
+    return format(value, "b").zfill(width)[-width:] if width else ""
+
+
+def counts_from_values(values: Sequence[int], width: int, has_measure: bool) -> Dict[str, int]:
+    """result.cpp:40-48."""
+    vals = np.asarray(values, dtype=np.uint64)
+    if not has_measure:
+        return {"": int(vals.size)} if vals.size else {}
+    uniq, cnt = np.unique(vals, return_counts=True)
+    return {bitstring(int(u), width): int(c) for u, c in zip(uniq, cnt)}
+
+
+def counts_checksum_of_values(values: np.ndarray, width: int, has_measure: bool):
+    """counts_checksum (result.cpp:23-38) computed by the library; (checksum, keys)."""
+    v = np.ascontiguousarray(values, dtype=np.uint64)
+    cs, nk = C.c_uint64(), C.c_uint64()
+    check(load().ssb_counts_checksum(v.ctypes.data_as(_lib._pu64), v.size, width, int(has_measure),
+                                     C.byref(cs), C.byref(nk)))
+    return cs.value, nk.value
+
+
+class Engine:
+    """One CUDA device (sm_100a)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(load().ssb_engine_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if self._h and self._h.value:
+            load().ssb_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        return load().ssb_engine_stream(self._h) or 0
+
+    def _run(self, fn, program: Program, opts: RunOptions, shot_begin: int, shot_count: int, name: str):
+        if opts.shots < 1 and shot_count is None:
+            raise ValueError("shots must be >= 1")
+        count = opts.shots if shot_count is None else shot_count
+        values = np.empty(count, dtype=np.uint64)
+        st = _lib.StatsC()
+        co = opts.to_c()
+        check(fn(self._h, program.handle, shot_begin, count, opts.seed, C.byref(co),
+                 values.ctypes.data_as(_lib._pu64), C.byref(st)))
+        f = program.flat()
+        r = RunResult(counts=counts_from_values(values, f.num_clbits, bool(f.has_measure)),
+                      shot_values=values if opts.record_shot_values else None,
+                      dispatch_count=st.dispatch_count, peak_states=st.peak_states,
+                      branch=BranchStats(st.peak_states, st.passes), strategy=name, shots=count,
+                      seed=opts.seed, device_seconds=st.device_seconds, wall_seconds=st.wall_seconds,
+                      fused_passes=st.fused_passes)
+        r._values = values
+        return r
+
+    def run_batch(self, program: Program, opts: RunOptions, shot_begin: int = 0,
+                  shot_count: Optional[int] = None) -> RunResult:
+        return self._run(load().ssb_run_batch, program, opts, shot_begin, shot_count, "gpu-batch")
+
+    def run_branch(self, program: Program, opts: RunOptions, shot_begin: int = 0,
+                   shot_count: Optional[int] = None) -> RunResult:
+        if opts.branch_budget < 1:
+            raise ValueError("branch budget must be >= 1")
+        return self._run(load().ssb_run_branch, program, opts, shot_begin, shot_count, "gpu-branch")
+
+    def run_batch_device(self, program: Program, opts: RunOptions, values_ptr: int, shot_begin: int,
+                         shot_count: int) -> _lib.StatsC:
+        st = _lib.StatsC()
+        co = opts.to_c()
+        check(load().ssb_run_batch_device(self._h, program.handle, shot_begin, shot_count, opts.seed,
+                                          C.byref(co), C.c_void_p(values_ptr), C.byref(st)))
+        return st
+
+    def histogram_device(self, values_ptr: int, count: int, num_clbits: int, hist_ptr: int) -> None:
+        check(load().ssb_histogram_device(self._h, C.c_void_p(values_ptr), count, num_clbits,
+                                          C.c_void_p(hist_ptr)))
+
+
+class BatchState:
+    """Operator-level batch over arbitrary shot ids (exec_batch.hpp:22-84)."""
+
+    def __init__(self, engine: Engine, program: Program, shot_ids: Sequence[int], seed: int):
+        ids = np.ascontiguousarray(shot_ids, dtype=np.uint64)
+        h = C.c_void_p()
+        check(load().ssb_batch_create(engine.handle, program.handle, ids.ctypes.data_as(_lib._pu64), ids.size,
+                                      seed, C.byref(h)))
+        self._h = h
+        self.size = int(ids.size)
+        self.n = program.num_qubits
+        self._program = program
+        self._engine = engine
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            try:
+                load().ssb_batch_destroy(self._h)
+            except Exception:
+                pass
+            self._h = C.c_void_p()
+
+    def apply_op(self, op_index: int, u: Optional[Sequence[float]] = None) -> None:
+        if u is None:
+            check(load().ssb_batch_apply_op(self._h, op_index, None))
+        else:
+            arr = np.ascontiguousarray(u, dtype=np.float64)
+            if arr.size != self.size:
+                raise ValueError("need one draw per shot")
+            check(load().ssb_batch_apply_op(self._h, op_index, arr.ctypes.data_as(_lib._pd)))
+
+    def run(self) -> None:
+        check(load().ssb_batch_run(self._h))
+
+    def segments(self) -> np.ndarray:
+        out = np.empty((self.size, 1 << self.n), dtype=np.complex128)
+        check(load().ssb_batch_read(self._h, out.ctypes.data_as(_lib._pd), None))
+        return out
+
+    def cregs(self) -> np.ndarray:
+        out = np.empty(self.size, dtype=np.uint64)
+        check(load().ssb_batch_read(self._h, None, out.ctypes.data_as(_lib._pu64)))
+        return out
+
+    def write_segment(self, s: int, amps: np.ndarray) -> None:
+        a = np.ascontiguousarray(amps, dtype=np.complex128)
+        check(load().ssb_batch_write_segment(self._h, s, a.ctypes.data_as(_lib._pd)))
+
+    @property
+    def dispatches(self) -> int:
+        return int(load().ssb_batch_dispatches(self._h))
+
+
+def executor_by_name(name: str):
+    """``gpu-batch`` | ``gpu-branch`` -> fn(engine, program, options) (exec.hpp:32-35)."""
+    if name == "gpu-batch":
+        return lambda eng, prog, opts: eng.run_batch(prog, opts)
+    if name == "gpu-branch":
+        return lambda eng, prog, opts: eng.run_branch(prog, opts)
+    raise _lib.ConfigError(_lib.SSB_ERR_CONFIG, f"unknown strategy: {name}")

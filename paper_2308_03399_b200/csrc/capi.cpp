@@ -1,0 +1,90 @@
+// C ABI, host half: program lowering, dumps and result folding.
+#include <cstring>
+
+#include "capi_internal.hpp"
+
+namespace ssb {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_uid{1};
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+uint64_t next_program_uid() { return g_uid.fetch_add(1); }
+
+namespace {
+
+ssb_program* make_program(shotsim::NoisyCircuit&& nc) {
+  auto* p = new ssb_program{next_program_uid(), std::move(nc), {}, {}};
+  try {
+    shotsim::flatten(p->nc, p->flat);
+    p->dev = build_device_program(p->nc);
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  return p;
+}
+
+}  // namespace
+}  // namespace ssb
+
+extern "C" {
+
+SSB_API const char* ssb_last_error(void) { return ssb::g_last_error.c_str(); }
+SSB_API int ssb_abi_version(void) { return SSB_ABI_VERSION; }
+
+SSB_API int ssb_program_from_text(const char* circuit_text, const char* noise_json, ssb_program** out) {
+  return ssb::guard([&] {
+    if (!circuit_text || !out) throw std::invalid_argument("null argument");
+    const std::string text(circuit_text);
+    const auto first = text.find_first_not_of(" \t\r\n");
+    const shotsim::Circuit c = (first != std::string::npos && text[first] == '{')
+                                   ? shotsim::circuit_from_json(text)
+                                   : shotsim::circuit_from_text(text);
+    const shotsim::NoiseModel model = shotsim::NoiseModel::from_json(noise_json ? noise_json : "");
+    *out = ssb::make_program(shotsim::instrument(c, model));
+  });
+}
+
+SSB_API int ssb_program_from_flat(const ssb_flat_program* flat, ssb_program** out) {
+  return ssb::guard([&] {
+    if (!flat || !out) throw std::invalid_argument("null argument");
+    *out = ssb::make_program(shotsim::unflatten(*flat));
+  });
+}
+
+SSB_API void ssb_program_destroy(ssb_program* program) { delete program; }
+
+SSB_API int ssb_program_flat(const ssb_program* program, ssb_flat_program* out) {
+  return ssb::guard([&] {
+    if (!program || !out) throw std::invalid_argument("null argument");
+    *out = program->flat.view;
+  });
+}
+
+SSB_API int ssb_program_dump(const ssb_program* program, char* buf, size_t cap, size_t* len) {
+  return ssb::guard([&] {
+    if (!program) throw std::invalid_argument("null program");
+    const std::string s = shotsim::dump_program(program->nc);
+    if (len) *len = s.size();
+    if (buf && cap > 0) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = '\0';
+    }
+  });
+}
+
+SSB_API int ssb_counts_checksum(const uint64_t* values, uint64_t count, uint32_t num_clbits, uint32_t has_measure,
+                                uint64_t* checksum_out, uint64_t* num_keys_out) {
+  return ssb::guard([&] {
+    const shotsim::Counts c =
+        shotsim::counts_from_values(std::span<const uint64_t>(values, count), num_clbits, has_measure != 0);
+    if (checksum_out) *checksum_out = shotsim::counts_checksum(c);
+    if (num_keys_out) *num_keys_out = c.size();
+  });
+}
+
+}  // extern "C"

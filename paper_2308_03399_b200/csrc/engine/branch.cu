@@ -1,0 +1,651 @@
+// gpu-branch: shot-branching executor (paper SIV.B; reference
+// exec_branch.cpp:175-295) with device-resident states and shot lists.
+//
+// Live states sit in a slot pool in HBM; the shots mapped to each live node
+// are a contiguous range of a device shot-id array (node-major). At every
+// randomness site the device computes the node-level quantities (outcome
+// probabilities / Kraus expectation values, exact reference order), then one
+// thread per shot draws its keyed uniform and picks its decision key, counting
+// (node, key) groups. The host only sees the small group-count table: it
+// applies the reference's budget policy (count desc, parent asc, key asc;
+// exec_branch.cpp:217-255), assigns child slots (first child reuses the
+// parent's slot, others are copies taken before any transform), and the device
+// scatters shots, copies states and applies each child's decision.
+// Leaves: per-leaf sequential cumulative (exact pick_outcome order) built once,
+// then one binary search per shot (first index with u < cum, which is what the
+// sequential scan returns because the cumulative is monotone).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <chrono>
+#include <numeric>
+#include <vector>
+
+#include "../capi_internal.hpp"
+#include "kernels.cuh"
+
+namespace ssb {
+
+#define CKB(expr)                                                                          \
+  do {                                                                                     \
+    const cudaError_t e_ = (expr);                                                         \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Node table entry as seen by the device.
+struct DevNode {
+  uint32_t slot;
+  uint32_t cond_ok;  // site condition holds for this node's register
+  uint64_t off, len; // shot range in the node-major shot array
+  uint64_t creg;
+};
+
+__device__ __forceinline__ uint64_t node_of(const DevNode* nodes, uint64_t nn, uint64_t pos) {
+  uint64_t lo = 0, hi = nn;  // last node with off <= pos
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (nodes[mid].off <= pos) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void b_init_slot(double2* pool, uint32_t slot, unsigned n) {
+  const uint64_t A = uint64_t{1} << n;
+  for (uint64_t j = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; j < A; j += uint64_t{gridDim.x} * blockDim.x)
+    pool[(uint64_t{slot} << n) + j] = make_double2(j == 0 ? 1.0 : 0.0, 0.0);
+}
+
+__global__ void b_iota(uint64_t* ids, uint64_t begin, uint64_t count) {
+  const uint64_t i = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (i < count) ids[i] = begin + i;
+}
+
+// Per-shot decision key + (node, key) counts. vals: node-level quantities
+// (probs[node][2^k] for measure/reset, p[node][nmat] for Kraus).
+__global__ void b_decide(ProgView P, DevOp op, const DevNode* nodes, uint64_t nn, const uint64_t* shots,
+                         uint64_t total, uint64_t seed, const double* vals, uint32_t nkeys, uint32_t* keys,
+                         unsigned* counts, int* err) {
+  const uint64_t pos = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (pos >= total) return;
+  const uint64_t node = node_of(nodes, nn, pos);
+  uint32_t key = 0;
+  if (nodes[node].cond_ok) {
+    const double u = keyed_uniform(seed, shots[pos], op.event);
+    if (op.kind == K_PAULI) {
+      key = static_cast<uint32_t>(pick_term(P.terms + op.aux, op.count, u));
+    } else if (op.kind == K_KRAUS) {
+      const double* p = vals + node * nkeys;
+      double cum = 0.0;
+      key = nkeys - 1;  // slack fallback: last matrix with its p (exec_branch.cpp:73-85)
+      for (uint32_t i = 0; i < nkeys; ++i) {
+        cum = __dadd_rn(cum, p[i]);
+        if (u < cum) {
+          key = i;
+          break;
+        }
+      }
+    } else {
+      uint64_t o = 0;
+      if (!pick_outcome(vals + node * nkeys, nkeys, u, &o)) raise(err, DEV_DEGENERATE);
+      key = static_cast<uint32_t>(o);
+    }
+  }
+  keys[pos] = key;
+  atomicAdd(&counts[node * nkeys + key], 1u);
+}
+
+// dst[node*nkeys+key]: base offset in the new shot array (kept) or, with the
+// top bit set, in the waiting array (deferred).
+__global__ void b_scatter(const DevNode* nodes, uint64_t nn, const uint64_t* shots, uint64_t total,
+                          const uint32_t* keys, uint32_t nkeys, const uint64_t* dst, unsigned long long* cursor,
+                          uint64_t* next_shots, uint64_t* waiting) {
+  const uint64_t pos = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (pos >= total) return;
+  const uint64_t g = node_of(nodes, nn, pos) * nkeys + keys[pos];
+  const uint64_t d = dst[g];
+  const uint64_t at = (d & ~(uint64_t{1} << 63)) + atomicAdd(&cursor[g], 1ull);
+  if (d >> 63) waiting[at] = shots[pos];
+  else next_shots[at] = shots[pos];
+}
+
+__global__ void b_copy_slots(double2* pool, const uint2* pairs, uint64_t npairs, unsigned n) {
+  const uint64_t A = uint64_t{1} << n, total = npairs * A;
+  for (uint64_t i = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; i < total; i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint2 pr = pairs[i / A];
+    const uint64_t j = i % A;
+    pool[(uint64_t{pr.y} << n) + j] = pool[(uint64_t{pr.x} << n) + j];
+  }
+}
+
+// One child's decision (apply_decision, exec_branch.cpp:104-136).
+struct ChildOp {
+  uint32_t slot;
+  uint32_t key;
+  double inv;  // Kraus / collapse scale 1/sqrt(param)
+};
+
+__global__ void b_apply(ProgView P, DevOp op, double2* pool, const ChildOp* kids, uint64_t nk, unsigned n) {
+  const uint64_t per = uint64_t{1} << (n - 1), total = nk * per;
+  uint64_t qmask = 0;
+  for (unsigned b = 0; b < op.nq; ++b) qmask |= uint64_t{1} << op.q[b];
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    const ChildOp ch = kids[idx / per];
+    const uint64_t p = idx % per;
+    double2* a = pool + (uint64_t{ch.slot} << n);
+    if (op.kind == K_PAULI) {
+      const DevTerm tm = P.terms[op.aux + ch.key];
+      if (tm.x == 0) {
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t j = 2 * p + h;
+          double2 v = pauli_phase(tm.num_y, a[j]);
+          if (__popcll(j & tm.z) & 1) v = c_neg(v);
+          a[j] = v;
+        }
+      } else {
+        const unsigned xmax = 31 - __clz(tm.x);
+        const uint64_t i0 = insert_zero(p, xmax), i1 = i0 ^ tm.x;
+        double2 t0 = pauli_phase(tm.num_y, a[i1]), t1 = pauli_phase(tm.num_y, a[i0]);
+        if (__popcll(i0 & tm.z) & 1) t0 = c_neg(t0);
+        if (__popcll(i1 & tm.z) & 1) t1 = c_neg(t1);
+        a[i0] = t0;
+        a[i1] = t1;
+      }
+    } else if (op.kind == K_KRAUS) {
+      const DevChannel chn = P.channels[op.aux];
+      const uint32_t slot = chn.mat_begin + ch.key;
+      const uint64_t cls = P.scaled_cls[slot];
+      if (chn.arity == 1) {
+        if (p >= per) continue;
+        double2 m[4];
+        for (int e = 0; e < 4; ++e) m[e] = c_scale(P.mats[16 * slot + e], ch.inv);
+        const uint64_t i0 = insert_zero(p, op.q[0]), i1 = i0 | (uint64_t{1} << op.q[0]);
+        const double2 v[2] = {a[i0], a[i1]};
+        a[i0] = row_apply<2>(m, cls, 0, v);
+        a[i1] = row_apply<2>(m, cls, 1, v);
+      } else {
+        if (p >= per / 2) continue;  // quads: half the pair slots
+        double2 m[16];
+        for (int e = 0; e < 16; ++e) m[e] = c_scale(P.mats[16 * slot + e], ch.inv);
+        const unsigned pl = min(op.q[0], op.q[1]), ph = max(op.q[0], op.q[1]);
+        const uint64_t d0 = uint64_t{1} << op.q[0], d1 = uint64_t{1} << op.q[1];
+        const uint64_t b = insert_zero(insert_zero(p, pl), ph);
+        const double2 v[4] = {a[b], a[b | d0], a[b | d1], a[b | d0 | d1]};
+        a[b] = row_apply<4>(m, cls, 0, v);
+        a[b | d0] = row_apply<4>(m, cls, 1, v);
+        a[b | d1] = row_apply<4>(m, cls, 2, v);
+        a[b | d0 | d1] = row_apply<4>(m, cls, 3, v);
+      }
+    } else {  // measure / reset collapse (+ X-fix)
+      const uint64_t off = scatter_bits(ch.key, op.q, op.nq);
+      const uint64_t xfix = op.kind == K_RESET ? off : 0;
+      const double2 zero = make_double2(0.0, 0.0);
+      if (xfix == 0) {
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t j = 2 * p + h;
+          a[j] = ((j & qmask) == off) ? c_scale(a[j], ch.inv) : zero;
+        }
+      } else {
+        const unsigned xmax = 63 - __clzll(xfix);
+        const uint64_t i0 = insert_zero(p, xmax), i1 = i0 ^ xfix;
+        const double2 a0 = a[i0], a1 = a[i1];
+        a[i0] = ((i1 & qmask) == off) ? c_scale(a1, ch.inv) : zero;
+        a[i1] = ((i0 & qmask) == off) ? c_scale(a0, ch.inv) : zero;
+      }
+    }
+  }
+}
+
+// Leaf cumulative over all sampled outcomes (groups = 1 case) — one thread
+// per leaf, the reference's sequential order; last[] = last nonzero outcome.
+__global__ void b_leaf_cum_full(ProgView P, const double2* pool, const DevNode* leaves, uint64_t nl, double* cum,
+                                uint64_t* last) {
+  const uint64_t l = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (l >= nl) return;
+  const unsigned n = P.n;
+  const double2* a = pool + (uint64_t{leaves[l].slot} << n);
+  const uint64_t count = uint64_t{1} << P.nsample;
+  double c = 0.0;
+  uint64_t lz = count;
+  double* out = cum + l * count;
+  for (uint64_t m = 0; m < count; ++m) {
+    const double p = c_norm(a[P.sample_identity ? m : scatter_bits(m, P.sample_qubits, P.nsample)]);
+    c = __dadd_rn(c, p);
+    out[m] = c;
+    if (p > 0.0) lz = m;
+  }
+  last[l] = lz;
+}
+
+// Same from precomputed probabilities (k < n sampled qubits).
+__global__ void b_leaf_cum_probs(const double* probs, uint64_t nl, uint64_t count, double* cum, uint64_t* last) {
+  const uint64_t l = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (l >= nl) return;
+  double c = 0.0;
+  uint64_t lz = count;
+  for (uint64_t m = 0; m < count; ++m) {
+    const double p = probs[l * count + m];
+    c = __dadd_rn(c, p);
+    cum[l * count + m] = c;
+    if (p > 0.0) lz = m;
+  }
+  last[l] = lz;
+}
+
+__global__ void b_leaf_values(ProgView P, const DevNode* leaves, uint64_t nl, const uint64_t* shots, uint64_t total,
+                              uint64_t seed, const double* cum, const uint64_t* last, uint64_t count,
+                              uint64_t shot_begin, uint64_t* values, int* err) {
+  const uint64_t pos = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (pos >= total) return;
+  const uint64_t l = node_of(leaves, nl, pos);
+  const uint64_t shot = shots[pos];
+  uint64_t v = leaves[l].creg;
+  if (cum) {
+    const double u = keyed_uniform(seed, shot, P.num_events);
+    const double* c = cum + l * count;
+    uint64_t lo = 0, hi = count;  // first m with u < c[m]
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      if (u < c[mid]) hi = mid;
+      else lo = mid + 1;
+    }
+    uint64_t o = lo;
+    if (lo == count) {
+      o = last[l];
+      if (o == count) {
+        raise(err, DEV_DEGENERATE);
+        o = 0;
+      }
+    }
+    v = apply_sample_outcome(P, v, o);
+  }
+  values[shot - shot_begin] = v;
+}
+
+namespace {
+
+unsigned gridn(uint64_t work, unsigned threads = NT) {
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((work + threads - 1) / threads, 1u << 30)));
+}
+
+struct HostNode {
+  uint32_t slot;
+  uint64_t off, len;
+  uint64_t creg;
+};
+
+template <class T>
+struct DBuf {  // grow-only device buffer
+  T* p = nullptr;
+  size_t cap = 0;
+  T* get(size_t n) {
+    if (n > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      CKB(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+      cap = std::max<size_t>(n, 1);
+    }
+    return p;
+  }
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h, uint64_t shot_begin,
+                       uint64_t count, uint64_t seed, const ssb_run_options* opts, uint64_t* values_dev,
+                       ssb_stats* stats, uint64_t mem_limit_bytes) {
+  const uint64_t budget = opts ? opts->branch_budget : 64;
+  if (budget < 1) throw std::invalid_argument("branch budget must be >= 1");
+  if (count < 1) throw std::invalid_argument("shots must be >= 1");
+  cudaStream_t s = E.stream;
+  const unsigned n = h.n;
+  const uint64_t A = uint64_t{1} << n, seg = A * sizeof(double2);
+  const uint64_t launches0 = *E.launches;
+  auto launched = [&] {
+    ++*E.launches;
+    CKB(cudaGetLastError());
+  };
+
+  // Slot pool: live states never exceed min(budget, shots) (+1 transient root).
+  const uint64_t max_slots = std::min<uint64_t>(budget, count) + 1;
+  if (max_slots * seg > mem_limit_bytes)
+    throw shotsim::CapacityError("branch budget of " + std::to_string(budget) + " states at " + std::to_string(n) +
+                                 " qubits needs " + std::to_string(max_slots * seg) + " bytes");
+  DBuf<double2> pool_buf;
+  uint64_t pool_cap = std::min<uint64_t>(max_slots, 64);
+  double2* pool = pool_buf.get(pool_cap * A);
+  std::vector<uint32_t> free_slots;
+  uint32_t next_slot = 0;
+  auto alloc_slot = [&]() -> uint32_t {
+    if (!free_slots.empty()) {
+      const uint32_t sl = free_slots.back();
+      free_slots.pop_back();
+      return sl;
+    }
+    if (next_slot >= pool_cap) {  // grow (rare): copy live slots over
+      const uint64_t ncap = std::min<uint64_t>(max_slots, pool_cap * 2);
+      double2* np = nullptr;
+      CKB(cudaMalloc(&np, ncap * seg));
+      CKB(cudaMemcpyAsync(np, pool_buf.p, pool_cap * seg, cudaMemcpyDeviceToDevice, s));
+      CKB(cudaStreamSynchronize(s));
+      cudaFree(pool_buf.p);
+      pool_buf.p = np;
+      pool_buf.cap = ncap * A;
+      pool = np;
+      pool_cap = ncap;
+    }
+    return next_slot++;
+  };
+
+  DBuf<uint64_t> shots_a, shots_b, waiting_buf;
+  uint64_t* cur_shots = shots_a.get(count);
+  uint64_t* nxt_shots = shots_b.get(count);
+  uint64_t* waiting = waiting_buf.get(count);
+  b_iota<<<gridn(count), NT, 0, s>>>(waiting, shot_begin, count);
+  launched();
+  uint64_t nwaiting = count;
+
+  DBuf<DevNode> dnodes;
+  DBuf<uint32_t> dkeys, dslots;
+  DBuf<unsigned> dcounts;
+  DBuf<uint64_t> ddst, dlast, dcreg;
+  DBuf<unsigned long long> dcursor;
+  DBuf<double> dvals, dpart, dcum;
+  DBuf<uint2> dpairs;
+  DBuf<ChildOp> dkids;
+  DBuf<uint8_t> dactive;
+
+  uint64_t peak = 0, passes = 0;
+  std::vector<HostNode> live;
+  while (nwaiting > 0) {
+    ++passes;
+    std::swap(cur_shots, waiting);  // waiting list becomes this pass's root
+    const uint64_t root_len = nwaiting;
+    nwaiting = 0;
+    free_slots.clear();
+    next_slot = 0;
+    live.assign(1, HostNode{alloc_slot(), 0, root_len, 0});
+    b_init_slot<<<gridn(A), NT, 0, s>>>(pool, live[0].slot, n);
+    launched();
+    peak = std::max<uint64_t>(peak, 1);
+
+    uint32_t i = 0;
+    while (i < h.end) {
+      uint32_t j = i;
+      auto is_site = [&](uint32_t k) {
+        const uint8_t kd = h.ops[k].kind;
+        return kd == K_PAULI || kd == K_KRAUS || kd == K_MEASURE || kd == K_RESET;
+      };
+      while (j < h.end && !is_site(j)) ++j;
+      const uint64_t nn = live.size();
+      // advance_node (exec_branch.cpp:155-162): gates over all live nodes.
+      if (j > i) {
+        std::vector<uint32_t> hs(nn);
+        std::vector<uint64_t> hc(nn);
+        for (uint64_t x = 0; x < nn; ++x) {
+          hs[x] = live[x].slot;
+          hc[x] = live[x].creg;
+        }
+        uint32_t* slots = dslots.get(nn);
+        uint64_t* cregs = dcreg.get(nn);
+        CKB(cudaMemcpyAsync(slots, hs.data(), nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        CKB(cudaMemcpyAsync(cregs, hc.data(), nn * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        for (uint32_t k = i; k < j; ++k) {
+          const DevOp& op = h.ops[k];
+          if (op.kind != K_GATE || op.skip) continue;
+          const uint64_t work = nn << (n - op.nq);
+          if (op.nq == 1) g_gate_kernel<1><<<gridn(work), NT, 0, s>>>(pool, nn, n, op, P.mats, cregs, slots);
+          else g_gate_kernel<2><<<gridn(work), NT, 0, s>>>(pool, nn, n, op, P.mats, cregs, slots);
+          launched();
+        }
+        CKB(cudaStreamSynchronize(s));  // host vectors hs/hc die here
+      }
+      if (j == h.end) break;
+      const DevOp site = h.ops[j];
+
+      // Node table with condition flags.
+      std::vector<DevNode> hn(nn);
+      for (uint64_t x = 0; x < nn; ++x)
+        hn[x] = {live[x].slot, !site.has_cond || (live[x].creg & site.cond_mask) == site.cond_value ? 1u : 0u,
+                 live[x].off, live[x].len, live[x].creg};
+      DevNode* nodes = dnodes.get(nn);
+      CKB(cudaMemcpyAsync(nodes, hn.data(), nn * sizeof(DevNode), cudaMemcpyHostToDevice, s));
+
+      uint32_t nkeys = 1;
+      double* vals = nullptr;
+      if (site.kind == K_PAULI) {
+        nkeys = site.count;
+      } else {
+        // Node-level quantities on the shared states (computed once per node).
+        RedSpec R{};
+        R.n = n;
+        int tree = 0;
+        if (site.kind == K_KRAUS) {
+          const DevChannel ch = h.channels[site.aux];
+          nkeys = ch.nmat;
+          R.k = ch.arity;
+          for (unsigned b = 0; b < ch.arity; ++b) R.q[b] = R.sorted[b] = site.q[b];
+          std::sort(R.sorted, R.sorted + ch.arity);
+          R.nq = ch.nmat;
+          R.mats = P.mats + 16 * ch.mat_begin;
+          if (ch.arity == 1) {
+            R.mode = R_EXPVAL1;
+            const uint64_t pairs = A / 2;
+            R.nb = pairs <= SUM_BLOCK ? 1 : pairs / SUM_BLOCK;
+            R.blk = pairs <= SUM_BLOCK ? pairs : SUM_BLOCK;
+          } else {
+            R.mode = R_EXPVAL2;
+            const uint64_t G = A / 4;
+            R.blk = G <= 8 ? G : 8;
+            R.nb = G / R.blk;
+            tree = 1;
+          }
+        } else {
+          R.mode = R_OUTCOME;
+          R.k = site.nq;
+          for (unsigned b = 0; b < site.nq; ++b) R.q[b] = R.sorted[b] = site.q[b];
+          std::sort(R.sorted, R.sorted + site.nq);
+          const uint64_t G = A >> site.nq;
+          R.nq = 1u << site.nq;
+          R.nb = G <= SUM_BLOCK ? 1 : G / SUM_BLOCK;
+          R.blk = G <= SUM_BLOCK ? G : SUM_BLOCK;
+          nkeys = R.nq;
+        }
+        std::vector<uint32_t> hs(nn);
+        std::vector<uint8_t> ha(nn);
+        for (uint64_t x = 0; x < nn; ++x) {
+          hs[x] = live[x].slot;
+          ha[x] = static_cast<uint8_t>(hn[x].cond_ok);
+        }
+        uint32_t* slots = dslots.get(nn);
+        uint8_t* active = dactive.get(nn);
+        CKB(cudaMemcpyAsync(slots, hs.data(), nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        CKB(cudaMemcpyAsync(active, ha.data(), nn, cudaMemcpyHostToDevice, s));
+        double* part = dpart.get(nn * R.nq * R.nb);
+        vals = dvals.get(nn * R.nq);
+        g_reduce_kernel<<<gridn(nn * R.nq * R.nb), NT, 0, s>>>(pool, nn, R, active, part, slots);
+        launched();
+        g_finish_kernel<<<gridn(nn * R.nq), NT, 0, s>>>(nn, R.nq, R.nb, tree, active, part, vals);
+        launched();
+        CKB(cudaStreamSynchronize(s));
+      }
+
+      // Per-shot decisions and group counts.
+      uint64_t total = 0;
+      for (const HostNode& x : live) total += x.len;
+      uint32_t* keys = dkeys.get(total);
+      unsigned* counts = dcounts.get(nn * nkeys);
+      CKB(cudaMemsetAsync(counts, 0, nn * nkeys * sizeof(unsigned), s));
+      b_decide<<<gridn(total), NT, 0, s>>>(P, site, nodes, nn, cur_shots, total, seed, vals, nkeys, keys, counts,
+                                           E.err);
+      launched();
+      std::vector<unsigned> hcount(nn * nkeys);
+      std::vector<double> hvals;
+      CKB(cudaMemcpyAsync(hcount.data(), counts, hcount.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      if (vals) {
+        hvals.resize(nn * nkeys);
+        CKB(cudaMemcpyAsync(hvals.data(), vals, hvals.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+      }
+      CKB(cudaStreamSynchronize(s));
+
+      // Groups in (parent, key) order; budget policy (exec_branch.cpp:217-255).
+      struct Cand {
+        uint64_t parent;
+        uint32_t key;
+        uint64_t count;
+      };
+      std::vector<Cand> groups;
+      for (uint64_t x = 0; x < nn; ++x)
+        for (uint32_t k = 0; k < nkeys; ++k)
+          if (hcount[x * nkeys + k]) groups.push_back({x, k, hcount[x * nkeys + k]});
+      std::vector<uint8_t> keep(groups.size(), 1);
+      if (groups.size() > budget) {
+        std::vector<size_t> order(groups.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+          if (groups[a].count != groups[b].count) return groups[a].count > groups[b].count;
+          if (groups[a].parent != groups[b].parent) return groups[a].parent < groups[b].parent;
+          return groups[a].key < groups[b].key;
+        });
+        std::fill(keep.begin(), keep.end(), 0);
+        for (uint64_t c = 0; c < budget; ++c) keep[order[c]] = 1;
+      }
+      // Children (materialize, exec_branch.cpp:141-153) and shot destinations.
+      std::vector<HostNode> next;
+      std::vector<uint64_t> hdst(nn * nkeys, 0);
+      std::vector<uint2> pairs;
+      std::vector<ChildOp> kids;
+      uint64_t new_off = 0, wait_off = nwaiting;
+      std::vector<uint8_t> parent_used(nn, 0);
+      for (size_t g = 0; g < groups.size(); ++g) {
+        const Cand& c = groups[g];
+        const uint64_t gi = c.parent * nkeys + c.key;
+        if (!keep[g]) {
+          hdst[gi] = (uint64_t{1} << 63) | wait_off;
+          wait_off += c.count;
+          continue;
+        }
+        const HostNode& par = live[c.parent];
+        uint32_t slot;
+        if (!parent_used[c.parent]) {
+          slot = par.slot;
+          parent_used[c.parent] = 1;
+        } else {
+          slot = alloc_slot();
+          pairs.push_back(make_uint2(par.slot, slot));
+        }
+        uint64_t creg = par.creg;
+        const bool transform = hn[c.parent].cond_ok &&
+                               !(site.kind == K_PAULI && h.terms[site.aux + c.key].identity);
+        if (transform) {
+          double inv = 1.0;
+          if (site.kind != K_PAULI) {
+            const double param = hvals[c.parent * nkeys + c.key];
+            if (!(param > 0.0)) throw shotsim::DegenerateDistribution("branch has zero probability");
+            inv = 1.0 / std::sqrt(param);
+          }
+          kids.push_back({slot, c.key, inv});
+          if (site.kind == K_MEASURE)
+            for (unsigned b = 0; b < site.nq; ++b)
+              creg = (creg & ~(uint64_t{1} << site.c[b])) | (((uint64_t{c.key} >> b) & 1) << site.c[b]);
+        }
+        hdst[gi] = new_off;
+        next.push_back({slot, new_off, c.count, creg});
+        new_off += c.count;
+      }
+      for (uint64_t x = 0; x < nn; ++x)
+        if (!parent_used[x]) free_slots.push_back(live[x].slot);
+      // The free list must not hand out a slot that is a copy source: sources
+      // are parents that have a kept first child, so they are never freed.
+
+      uint64_t* dst = ddst.get(nn * nkeys);
+      unsigned long long* cursor = dcursor.get(nn * nkeys);
+      CKB(cudaMemcpyAsync(dst, hdst.data(), hdst.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+      CKB(cudaMemsetAsync(cursor, 0, nn * nkeys * sizeof(unsigned long long), s));
+      b_scatter<<<gridn(total), NT, 0, s>>>(nodes, nn, cur_shots, total, keys, nkeys, dst, cursor, nxt_shots, waiting);
+      launched();
+      if (!pairs.empty()) {
+        uint2* dp = dpairs.get(pairs.size());
+        CKB(cudaMemcpyAsync(dp, pairs.data(), pairs.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+        b_copy_slots<<<gridn(pairs.size() * A), NT, 0, s>>>(pool, dp, pairs.size(), n);
+        launched();
+      }
+      if (!kids.empty()) {
+        ChildOp* dk = dkids.get(kids.size());
+        CKB(cudaMemcpyAsync(dk, kids.data(), kids.size() * sizeof(ChildOp), cudaMemcpyHostToDevice, s));
+        b_apply<<<gridn(kids.size() * (A / 2)), NT, 0, s>>>(P, site, pool, dk, kids.size(), n);
+        launched();
+      }
+      CKB(cudaStreamSynchronize(s));
+      nwaiting = wait_off;
+      std::swap(cur_shots, nxt_shots);
+      live = std::move(next);
+      peak = std::max<uint64_t>(peak, live.size());
+      i = j + 1;
+    }
+
+    // Leaves (exec_branch.cpp:267-281).
+    const uint64_t nl = live.size();
+    uint64_t total = 0;
+    std::vector<DevNode> hl(nl);
+    for (uint64_t x = 0; x < nl; ++x) {
+      hl[x] = {live[x].slot, 1, live[x].off, live[x].len, live[x].creg};
+      total += live[x].len;
+    }
+    if (nl > 0 && total > 0) {
+      DevNode* leaves = dnodes.get(nl);
+      CKB(cudaMemcpyAsync(leaves, hl.data(), nl * sizeof(DevNode), cudaMemcpyHostToDevice, s));
+      double* cum = nullptr;
+      uint64_t* last = nullptr;
+      const uint64_t cnt = uint64_t{1} << P.nsample;
+      if (h.eligible) {
+        cum = dcum.get(nl * cnt);
+        last = dlast.get(nl);
+        if (P.nsample == n) {
+          b_leaf_cum_full<<<gridn(nl, 64), 64, 0, s>>>(P, pool, leaves, nl, cum, last);
+          launched();
+        } else {
+          RedSpec R{};
+          R.mode = R_OUTCOME;
+          R.n = n;
+          R.k = P.nsample;
+          for (unsigned b = 0; b < P.nsample; ++b) R.q[b] = R.sorted[b] = h.sample_qubits[b];
+          std::sort(R.sorted, R.sorted + P.nsample);
+          const uint64_t G = A >> P.nsample;
+          R.nq = static_cast<uint32_t>(cnt);
+          R.nb = G <= SUM_BLOCK ? 1 : G / SUM_BLOCK;
+          R.blk = G <= SUM_BLOCK ? G : SUM_BLOCK;
+          std::vector<uint32_t> hs(nl);
+          for (uint64_t x = 0; x < nl; ++x) hs[x] = live[x].slot;
+          uint32_t* slots = dslots.get(nl);
+          CKB(cudaMemcpyAsync(slots, hs.data(), nl * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+          double* part = dpart.get(nl * R.nq * R.nb);
+          double* probs = dvals.get(nl * R.nq);
+          g_reduce_kernel<<<gridn(nl * R.nq * R.nb), NT, 0, s>>>(pool, nl, R, nullptr, part, slots);
+          launched();
+          g_finish_kernel<<<gridn(nl * R.nq), NT, 0, s>>>(nl, R.nq, R.nb, 0, nullptr, part, probs);
+          launched();
+          b_leaf_cum_probs<<<gridn(nl, 64), 64, 0, s>>>(probs, nl, cnt, cum, last);
+          launched();
+          CKB(cudaStreamSynchronize(s));
+        }
+      }
+      b_leaf_values<<<gridn(total), NT, 0, s>>>(P, leaves, nl, cur_shots, total, seed, cum, last, cnt, shot_begin,
+                                                values_dev, E.err);
+      launched();
+      CKB(cudaStreamSynchronize(s));
+    }
+  }
+  if (stats) {
+    stats->peak_states = peak;
+    stats->passes = passes;
+    stats->dispatch_count = *E.launches - launches0;
+  }
+}
+
+}  // namespace ssb

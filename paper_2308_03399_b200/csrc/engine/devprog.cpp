@@ -1,0 +1,211 @@
+// Host-side lowering of an instrumented program to the device program and the
+// HBM tile-pass plan (see devprog.hpp).
+#include "devprog.hpp"
+
+#include <bit>
+#include <stdexcept>
+
+#include "exact.cuh"
+
+namespace ssb {
+
+uint64_t classify_matrix(const double* m, unsigned k, bool scaled) {
+  const unsigned entries = 1u << (2 * k);
+  uint64_t cls = 0;
+  for (unsigned i = 0; i < entries; ++i) {
+    const double re = m[2 * i], im = m[2 * i + 1];
+    uint64_t c;
+    if (re == 0.0 && im == 0.0) c = E_ZERO;
+    else if (im == 0.0) c = (!scaled && re == 1.0) ? E_ONE : (!scaled && re == -1.0) ? E_NEG_ONE : E_REAL;
+    else if (re == 0.0) c = E_IMAG;
+    else c = E_GEN;
+    cls |= c << (3 * i);
+  }
+  return cls;
+}
+
+namespace {
+
+bool is_identity_cls(uint64_t cls, unsigned k) {
+  const unsigned d = 1u << k;
+  for (unsigned r = 0; r < d; ++r)
+    for (unsigned c = 0; c < d; ++c)
+      if (entry_class(cls, r * d + c) != (r == c ? E_ONE : E_ZERO)) return false;
+  return true;
+}
+
+}  // namespace
+
+HostDevProgram build_device_program(const shotsim::NoisyCircuit& p) {
+  using shotsim::ProgramOp;
+  if (p.num_qubits < 1 || p.num_qubits > 30) throw std::invalid_argument("qubit count must be in [1, 30]");
+  HostDevProgram d;
+  d.n = p.num_qubits;
+  d.num_clbits = p.num_clbits;
+  d.num_events = p.num_events;
+  d.eligible = p.sampling_eligible;
+  d.has_measure = p.has_measure;
+  d.end = static_cast<uint32_t>(p.sampling_eligible ? p.terminal_measure_begin : p.ops.size());
+
+  auto push_matrix = [&d](const shotsim::GateMatrix& m) {
+    const uint32_t slot = static_cast<uint32_t>(d.mats.size() / 32);
+    d.mats.resize(d.mats.size() + 32, 0.0);
+    for (size_t i = 0; i < m.entries.size(); ++i) {
+      d.mats[slot * 32 + 2 * i] = m.entries[i].real();
+      d.mats[slot * 32 + 2 * i + 1] = m.entries[i].imag();
+    }
+    d.scaled_cls.push_back(classify_matrix(&d.mats[slot * 32], m.num_qubits, true));
+    return slot;
+  };
+
+  for (const shotsim::KrausError& k : p.kraus_channels) {
+    if (k.arity < 1 || k.arity > 2) throw std::invalid_argument("kraus arity must be 1 or 2");
+    DevChannel ch{k.arity, static_cast<uint32_t>(k.matrices.size()), 0, 0};
+    for (size_t i = 0; i < k.matrices.size(); ++i) {
+      const uint32_t s = push_matrix(k.matrices[i]);
+      if (i == 0) ch.mat_begin = s;
+    }
+    if (ch.nmat == 0) throw std::invalid_argument("kraus channel without matrices");
+    d.channels.push_back(ch);
+    d.max_kraus = std::max(d.max_kraus, ch.nmat);
+  }
+
+  for (const ProgramOp& op : p.ops) {
+    DevOp o{};
+    o.kind = static_cast<uint8_t>(op.kind);
+    if (op.qubits.size() > 4) throw std::invalid_argument("op has more than 4 qubits");
+    o.nq = static_cast<uint8_t>(op.qubits.size());
+    for (size_t i = 0; i < op.qubits.size(); ++i) {
+      if (op.qubits[i] >= p.num_qubits) throw std::invalid_argument("target qubit out of range");
+      o.q[i] = static_cast<uint8_t>(op.qubits[i]);
+    }
+    for (size_t i = 0; i < op.clbits.size() && i < 4; ++i) {
+      if (op.clbits[i] >= 64) throw std::invalid_argument("clbit out of range");
+      o.c[i] = static_cast<uint8_t>(op.clbits[i]);
+    }
+    o.has_cond = op.condition.has_value();
+    if (op.condition) {
+      o.cond_mask = op.condition->clbit_mask;
+      o.cond_value = op.condition->value;
+    }
+    o.event = op.event;
+    switch (op.kind) {
+      case ProgramOp::Kind::Gate: {
+        if (op.matrix.num_qubits != op.qubits.size() || op.qubits.size() < 1 || op.qubits.size() > 2)
+          throw std::invalid_argument("matrix dimension does not match target count");
+        if (op.qubits.size() == 2 && op.qubits[0] == op.qubits[1])
+          throw std::invalid_argument("duplicate target qubit");
+        o.aux = push_matrix(op.matrix);
+        o.cls = classify_matrix(&d.mats[o.aux * 32], op.matrix.num_qubits, false);
+        o.skip = is_identity_cls(o.cls, op.matrix.num_qubits);
+        break;
+      }
+      case ProgramOp::Kind::PauliSite: {
+        o.aux = static_cast<uint32_t>(d.terms.size());
+        o.count = static_cast<uint32_t>(op.term_cum.size());
+        o.site = d.num_pauli_sites++;
+        if (o.count == 0 || o.count > 255) throw std::invalid_argument("pauli site term count");
+        for (size_t t = 0; t < op.term_cum.size(); ++t) {
+          const shotsim::PauliMasks& m = op.term_masks[t];
+          if ((m.x_mask >> p.num_qubits) || (m.z_mask >> p.num_qubits))
+            throw std::invalid_argument("pauli mask out of range for state");
+          d.terms.push_back({op.term_cum[t], static_cast<uint32_t>(m.x_mask), static_cast<uint32_t>(m.z_mask),
+                             m.num_y, op.term_identity[t]});
+        }
+        break;
+      }
+      case ProgramOp::Kind::KrausSite: {
+        if (op.channel >= d.channels.size()) throw std::invalid_argument("kraus channel out of range");
+        o.aux = op.channel;
+        o.count = d.channels[op.channel].nmat;
+        if (d.channels[op.channel].arity != op.qubits.size())
+          throw std::invalid_argument("matrix dimension does not match target count");
+        d.has_kraus = true;
+        break;
+      }
+      case ProgramOp::Kind::Measure:
+      case ProgramOp::Kind::Reset:
+        if (op.qubits.empty()) throw std::invalid_argument("measure/reset needs qubits");
+        if (op.kind == ProgramOp::Kind::Measure && op.clbits.size() != op.qubits.size())
+          throw std::invalid_argument("measure needs one clbit per qubit");
+        d.has_measure_ops = true;
+        break;
+      case ProgramOp::Kind::Barrier: break;
+    }
+    d.ops.push_back(o);
+  }
+  for (unsigned q : p.sample_qubits) d.sample_qubits.push_back(static_cast<uint8_t>(q));
+  for (const auto& [c, b] : p.sample_writes) {
+    d.write_clbit.push_back(static_cast<uint8_t>(c));
+    d.write_pos.push_back(static_cast<uint8_t>(b));
+  }
+  d.sample_identity = d.sample_qubits.size() == d.n;
+  for (size_t i = 0; i < d.sample_qubits.size() && d.sample_identity; ++i)
+    d.sample_identity = d.sample_qubits[i] == i;
+  return d;
+}
+
+// Greedy in-order pass formation: consecutive gates / Pauli sites whose union
+// of qubits (plus the always-local low qubits, for 128-byte coalesced tile
+// rows) fits k local qubits share one HBM read+write of the state. Ops are
+// never reordered (gates on disjoint qubits do not commute bitwise in
+// floating point), Kraus / measure / reset sites end a pass.
+void plan_passes(HostDevProgram& d, unsigned tile_k) {
+  d.passes.clear();
+  d.pass_ops.clear();
+  d.steps.clear();
+  const unsigned n = d.n;
+  const unsigned k = std::min(tile_k, n);
+  d.tile_k = k;
+  const uint32_t low = (1u << std::min(3u, k)) - 1;
+  uint32_t cur = low;
+  std::vector<uint32_t> cur_ops;
+  bool need_init = true;
+
+  auto close = [&](bool force) {
+    if (cur_ops.empty() && !(force && need_init)) return;
+    uint32_t mask = cur;
+    for (unsigned q = 0; q < n && static_cast<unsigned>(std::popcount(mask)) < k; ++q) mask |= 1u << q;
+    PassDesc pd{};
+    pd.begin = static_cast<uint32_t>(d.pass_ops.size());
+    pd.lmask = mask;
+    pd.k = static_cast<uint8_t>(k);
+    pd.first = need_init;
+    need_init = false;
+    uint8_t pos[32] = {};
+    for (unsigned q = 0, j = 0; q < n; ++q)
+      if (mask >> q & 1) {
+        pd.lq[j] = static_cast<uint8_t>(q);
+        pos[q] = static_cast<uint8_t>(j++);
+      }
+    for (uint32_t oi : cur_ops) {
+      PassOp po{oi, {}};
+      for (unsigned b = 0; b < d.ops[oi].nq; ++b) po.lq[b] = pos[d.ops[oi].q[b]];
+      d.pass_ops.push_back(po);
+    }
+    pd.end = static_cast<uint32_t>(d.pass_ops.size());
+    d.steps.push_back({S_PASS, static_cast<uint32_t>(d.passes.size())});
+    d.passes.push_back(pd);
+    cur = low;
+    cur_ops.clear();
+  };
+
+  for (uint32_t i = 0; i < d.end; ++i) {
+    const DevOp& o = d.ops[i];
+    if (o.kind == K_BARRIER || (o.kind == K_GATE && o.skip)) continue;
+    if (o.kind == K_GATE || o.kind == K_PAULI) {
+      uint32_t qm = 0;
+      for (unsigned b = 0; b < o.nq; ++b) qm |= 1u << o.q[b];
+      if (static_cast<unsigned>(std::popcount(cur | qm)) > k) close(false);
+      cur |= qm;
+      cur_ops.push_back(i);
+    } else {
+      close(true);
+      d.steps.push_back({S_SPECIAL, i});
+    }
+  }
+  close(true);
+  if (d.eligible) d.steps.push_back({S_SAMPLE, 0});
+}
+
+}  // namespace ssb

@@ -1,0 +1,95 @@
+// Device program: the instrumented NoisyCircuit (program.hpp:18-70) lowered to
+// flat, 64-byte op records plus pooled matrices / Pauli terms / Kraus channels,
+// and the HBM pass plan used by the streamed executor. Built once per program
+// on the host (build_device_program), uploaded once per device.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "shotsim_b200.hpp"
+
+namespace ssb {
+
+enum OpKind : uint8_t { K_GATE = 0, K_PAULI = 1, K_KRAUS = 2, K_MEASURE = 3, K_RESET = 4, K_BARRIER = 5 };
+
+struct alignas(16) DevOp {
+  uint8_t kind;
+  uint8_t nq;
+  uint8_t has_cond;
+  uint8_t skip;        // gate whose matrix is the identity: exact no-op
+  uint8_t q[4];        // qubit operands (qubits[0] = low matrix axis)
+  uint8_t c[4];        // clbits (MEASURE)
+  uint32_t aux;        // GATE: matrix slot; PAULI: first term; KRAUS: channel
+  uint32_t count;      // PAULI: term count; KRAUS: matrix count
+  uint32_t site;       // PAULI: ordinal among Pauli sites (decision table column)
+  uint32_t pad;
+  uint64_t cls;        // GATE: entry classes (exact.cuh EntryClass, 3 bits each)
+  uint64_t cond_mask;
+  uint64_t cond_value;
+  uint64_t event;
+};
+static_assert(sizeof(DevOp) == 64, "DevOp layout");
+
+struct alignas(8) DevTerm {
+  double cum;
+  uint32_t x, z;       // qubit masks (n <= 30)
+  uint32_t num_y;
+  uint32_t identity;
+};
+
+struct DevChannel {
+  uint32_t arity, nmat, mat_begin, pad;
+};
+
+// One fused HBM tile pass: the ops [begin,end) of pass_ops, all acting inside
+// the local qubit set `lmask` (|lmask| = k); `first` synthesises |0...0>
+// instead of loading the tile.
+struct PassDesc {
+  uint32_t begin, end;
+  uint32_t lmask;
+  uint8_t k;
+  uint8_t first;
+  uint8_t pad[2];
+  uint8_t lq[32];      // local position j -> qubit
+};
+
+struct PassOp {
+  uint32_t op;         // index into ops
+  uint8_t lq[4];       // local positions of the op's qubits
+};
+
+enum StepKind : uint8_t { S_PASS = 0, S_SPECIAL = 1, S_SAMPLE = 2 };
+struct Step {
+  StepKind kind;
+  uint32_t index;      // pass index, or op index for S_SPECIAL
+};
+
+struct HostDevProgram {
+  uint32_t n = 0, num_clbits = 0;
+  uint64_t num_events = 0;
+  bool eligible = false, has_measure = false;
+  uint32_t end = 0;                      // ops executed before terminal sampling
+  uint32_t num_pauli_sites = 0;
+  uint32_t max_kraus = 0;                // largest channel size
+  bool has_kraus = false, has_measure_ops = false;
+  std::vector<DevOp> ops;
+  std::vector<DevTerm> terms;
+  std::vector<DevChannel> channels;
+  std::vector<double> mats;              // 32 doubles per slot
+  std::vector<uint64_t> scaled_cls;      // per matrix slot: classes after 1/sqrt(p)
+  std::vector<uint8_t> sample_qubits, write_clbit, write_pos;
+  bool sample_identity = false;          // sample_qubits == [0..n)
+  // Streamed-mode plan (n > resident limit).
+  std::vector<PassDesc> passes;
+  std::vector<PassOp> pass_ops;
+  std::vector<Step> steps;
+  unsigned tile_k = 0;
+};
+
+uint64_t classify_matrix(const double* m, unsigned k, bool scaled);
+HostDevProgram build_device_program(const shotsim::NoisyCircuit& p);
+void plan_passes(HostDevProgram& d, unsigned tile_k);
+
+}  // namespace ssb

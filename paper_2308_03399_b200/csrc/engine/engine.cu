@@ -1,0 +1,634 @@
+// shotsim_b200 engine: device program upload, the batched executors and the
+// device half of the C ABI. Host control only sequences launches on the
+// engine's stream; all state lives in HBM / shared memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../capi_internal.hpp"
+#include "kernels.cuh"
+
+namespace ssb {
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    const cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Device copy of one program (+ its pass plan for one tile size).
+struct DevProgram {
+  HostDevProgram host;  // with passes planned for tile_k
+  std::vector<void*> allocs;
+  ProgView view{};
+  uint32_t* pauli_site_ops = nullptr;
+  uint32_t num_pauli = 0;
+  ~DevProgram() {
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+}  // namespace ssb
+
+struct ssb_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int num_sms = 0;
+  size_t smem_optin = 0;
+  int* err = nullptr;
+  std::map<std::pair<uint64_t, unsigned>, std::unique_ptr<ssb::DevProgram>> programs;
+  std::map<std::string, std::pair<void*, size_t>> scratch;
+  uint64_t launches = 0;
+};
+
+struct ssb_batch {
+  ssb_engine* engine;
+  const ssb_program* program;
+  uint64_t size, seed;
+  uint64_t* ids = nullptr;
+  double2* state = nullptr;
+  uint64_t* cregs = nullptr;
+  uint64_t dispatches = 0;
+};
+
+namespace ssb {
+
+namespace {
+
+constexpr unsigned kResidentMaxDefault = 13;
+constexpr unsigned kTileDefault = 12;
+
+void* scratch(ssb_engine* E, const char* name, size_t bytes) {
+  auto& slot = E->scratch[name];
+  if (slot.second < bytes) {
+    if (slot.first) CK(cudaFree(slot.first));
+    slot.first = nullptr;
+    slot.second = 0;
+    CK(cudaMalloc(&slot.first, bytes));
+    slot.second = bytes;
+  }
+  return slot.first;
+}
+
+template <class T>
+T* upload(DevProgram& d, const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  void* p = nullptr;
+  CK(cudaMalloc(&p, v.size() * sizeof(T)));
+  d.allocs.push_back(p);
+  CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return static_cast<T*>(p);
+}
+
+DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile_k) {
+  const auto key = std::make_pair(prog->uid, tile_k);
+  auto it = E->programs.find(key);
+  if (it != E->programs.end()) return *it->second;
+  auto d = std::make_unique<DevProgram>();
+  d->host = prog->dev;
+  plan_passes(d->host, tile_k);
+  const HostDevProgram& h = d->host;
+  ProgView& v = d->view;
+  v.ops = upload(*d, h.ops);
+  v.terms = upload(*d, h.terms);
+  v.channels = upload(*d, h.channels);
+  v.mats = reinterpret_cast<const double2*>(upload(*d, h.mats));
+  v.scaled_cls = upload(*d, h.scaled_cls);
+  v.sample_qubits = upload(*d, h.sample_qubits);
+  v.write_clbit = upload(*d, h.write_clbit);
+  v.write_pos = upload(*d, h.write_pos);
+  v.passes = upload(*d, h.passes);
+  v.pass_ops = upload(*d, h.pass_ops);
+  v.n = h.n;
+  v.end = h.end;
+  v.nsample = static_cast<uint32_t>(h.sample_qubits.size());
+  v.nwrites = static_cast<uint32_t>(h.write_clbit.size());
+  v.num_events = h.num_events;
+  v.eligible = h.eligible;
+  v.sample_identity = h.sample_identity;
+  std::vector<uint32_t> sites;
+  for (uint32_t i = 0; i < h.ops.size(); ++i)
+    if (h.ops[i].kind == K_PAULI) sites.push_back(i);
+  d->num_pauli = static_cast<uint32_t>(sites.size());
+  d->pauli_site_ops = upload(*d, sites);
+  auto& ref = *d;
+  E->programs.emplace(key, std::move(d));
+  return ref;
+}
+
+unsigned grid_for(uint64_t work, unsigned threads = NT) {
+  const uint64_t g = (work + threads - 1) / threads;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 1u << 30)));
+}
+
+void launched(ssb_engine* E) {
+  ++E->launches;
+  CK(cudaGetLastError());
+}
+
+void check_device_error(ssb_engine* E) {
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, E->err, sizeof(int), cudaMemcpyDeviceToHost, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  if (h == DEV_DEGENERATE) {
+    CK(cudaMemsetAsync(E->err, 0, sizeof(int), E->stream));
+    throw shotsim::DegenerateDistribution("measured distribution sums to zero or branch has zero probability");
+  }
+}
+
+uint64_t mem_limit(const ssb_run_options* o) {
+  if (o && o->mem_limit_bytes) return o->mem_limit_bytes;
+  if (const char* env = std::getenv("SHOTSIM_MEM_LIMIT_BYTES")) {
+    const uint64_t v = std::strtoull(env, nullptr, 10);
+    if (v > 0) return v;
+  }
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  return static_cast<uint64_t>(free_b * 0.8);
+}
+
+// ---- op-at-a-time batched ops (shared by the streamed executor and the
+// operator-level ABI). Shots [0,S) of `state`; ids == nullptr means ids are
+// begin + s. u: optional per-shot draws (device).
+struct SegCtx {
+  double2* state;
+  uint64_t S;
+  uint64_t seed;
+  const uint64_t* ids;
+  uint64_t begin;
+  const double* u;
+  uint64_t* cregs;
+  SegCtx sub(uint64_t off, uint64_t len, unsigned n) const {
+    return {state + (off << n), len, seed, ids ? ids + off : nullptr, begin + off, u ? u + off : nullptr, cregs + off};
+  }
+};
+
+void run_reduction(ssb_engine* E, const SegCtx& c, const RedSpec& R, int leaves_tree, const uint8_t* active,
+                   double* val) {
+  double* part = static_cast<double*>(scratch(E, "part", c.S * R.nq * R.nb * sizeof(double)));
+  g_reduce_kernel<<<grid_for(c.S * R.nq * R.nb), NT, 0, E->stream>>>(c.state, c.S, R, active, part);
+  launched(E);
+  g_finish_kernel<<<grid_for(c.S * R.nq), NT, 0, E->stream>>>(c.S, R.nq, R.nb, leaves_tree, active, part, val);
+  launched(E);
+}
+
+// 512-block outcome reduction spec over qubits q (k of them).
+RedSpec outcome_spec(unsigned n, const uint8_t* q, unsigned k) {
+  RedSpec R{};
+  R.mode = R_OUTCOME;
+  R.n = n;
+  R.k = k;
+  for (unsigned i = 0; i < k; ++i) R.q[i] = R.sorted[i] = q[i];
+  std::sort(R.sorted, R.sorted + k);
+  const uint64_t G = uint64_t{1} << (n - k);
+  R.nq = static_cast<uint32_t>(uint64_t{1} << k);
+  R.nb = G <= SUM_BLOCK ? 1 : G / SUM_BLOCK;
+  R.blk = G <= SUM_BLOCK ? G : SUM_BLOCK;
+  return R;
+}
+
+uint64_t chunk_for(uint64_t S, uint64_t per_shot_bytes) {
+  const uint64_t cap = uint64_t{1} << 30;
+  return std::max<uint64_t>(1, std::min<uint64_t>(S, cap / std::max<uint64_t>(1, per_shot_bytes)));
+}
+
+// Returns the number of logical dispatches in the reference's accounting
+// (README.md:102-107) for the operator-level ABI.
+uint64_t apply_op(ssb_engine* E, DevProgram& dp, uint32_t op_index, const SegCtx& c, bool count_identity_skip) {
+  const DevOp op = dp.host.ops[op_index];
+  const unsigned n = dp.host.n;
+  const ProgView& P = dp.view;
+  switch (op.kind) {
+    case K_BARRIER: return 0;
+    case K_GATE: {
+      if (!op.skip) {
+        const uint64_t work = c.S << (n - op.nq);
+        if (op.nq == 1) g_gate_kernel<1><<<grid_for(work), NT, 0, E->stream>>>(c.state, c.S, n, op, P.mats, c.cregs);
+        else g_gate_kernel<2><<<grid_for(work), NT, 0, E->stream>>>(c.state, c.S, n, op, P.mats, c.cregs);
+        launched(E);
+      }
+      return 1;
+    }
+    case K_PAULI: {
+      int* sel = static_cast<int*>(scratch(E, "sel", c.S * sizeof(int)));
+      g_pauli_decide_kernel<<<grid_for(c.S), NT, 0, E->stream>>>(P, op, c.S, c.seed, c.ids, c.begin, c.u, c.cregs, sel);
+      launched(E);
+      if (count_identity_skip) {  // the reference issues no dispatch when every shot drew identity
+        std::vector<int> h(c.S);
+        CK(cudaMemcpyAsync(h.data(), sel, c.S * sizeof(int), cudaMemcpyDeviceToHost, E->stream));
+        CK(cudaStreamSynchronize(E->stream));
+        if (std::none_of(h.begin(), h.end(), [](int t) { return t >= 0; })) return 0;
+      }
+      g_pauli_apply_kernel<<<grid_for(c.S << (n - 1)), NT, 0, E->stream>>>(c.state, c.S, n, P.terms + op.aux, sel);
+      launched(E);
+      return 1;
+    }
+    case K_KRAUS: {
+      const DevChannel ch = dp.host.channels[op.aux];
+      RedSpec R{};
+      R.n = n;
+      R.k = ch.arity;
+      for (unsigned i = 0; i < ch.arity; ++i) R.q[i] = R.sorted[i] = op.q[i];
+      std::sort(R.sorted, R.sorted + ch.arity);
+      R.nq = ch.nmat;
+      R.mats = P.mats + 16 * ch.mat_begin;
+      int tree = 0;
+      if (ch.arity == 1) {
+        R.mode = R_EXPVAL1;
+        const uint64_t pairs = uint64_t{1} << (n - 1);
+        R.nb = pairs <= SUM_BLOCK ? 1 : pairs / SUM_BLOCK;
+        R.blk = pairs <= SUM_BLOCK ? pairs : SUM_BLOCK;
+      } else {
+        R.mode = R_EXPVAL2;
+        const uint64_t G = uint64_t{1} << (n - 2);
+        R.blk = G <= 8 ? G : 8;
+        R.nb = G / R.blk;
+        tree = 1;
+      }
+      const uint64_t chunk = chunk_for(c.S, (R.nq * R.nb + R.nq) * sizeof(double) + 16 * 16 + 32);
+      for (uint64_t off = 0; off < c.S; off += chunk) {
+        const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
+        uint8_t* active = static_cast<uint8_t*>(scratch(E, "active", cc.S));
+        double* val = static_cast<double*>(scratch(E, "val", cc.S * R.nq * sizeof(double)));
+        double2* scaled = static_cast<double2*>(scratch(E, "kscaled", cc.S * 16 * sizeof(double2)));
+        uint64_t* cls = static_cast<uint64_t*>(scratch(E, "kcls", cc.S * sizeof(uint64_t)));
+        int* chosen = static_cast<int*>(scratch(E, "kchosen", cc.S * sizeof(int)));
+        g_active_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(op, cc.S, cc.cregs, active);
+        launched(E);
+        run_reduction(E, cc, R, tree, active, val);
+        g_kraus_decide_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(P, op, cc.S, cc.seed, cc.ids, cc.begin, cc.u, active,
+                                                                    val, scaled, cls, chosen, E->err);
+        launched(E);
+        const uint64_t work = cc.S << (n - ch.arity);
+        if (ch.arity == 1)
+          g_kraus_apply_kernel<1><<<grid_for(work), NT, 0, E->stream>>>(cc.state, cc.S, n, op, scaled, cls, chosen);
+        else
+          g_kraus_apply_kernel<2><<<grid_for(work), NT, 0, E->stream>>>(cc.state, cc.S, n, op, scaled, cls, chosen);
+        launched(E);
+      }
+      return 2ull * ch.nmat;
+    }
+    case K_MEASURE:
+    case K_RESET: {
+      const RedSpec R = outcome_spec(n, op.q, op.nq);
+      const uint64_t chunk = chunk_for(c.S, (R.nq * R.nb + R.nq) * sizeof(double) + 32);
+      for (uint64_t off = 0; off < c.S; off += chunk) {
+        const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
+        uint8_t* active = static_cast<uint8_t*>(scratch(E, "active", cc.S));
+        double* val = static_cast<double*>(scratch(E, "val", cc.S * R.nq * sizeof(double)));
+        int64_t* outcome = static_cast<int64_t*>(scratch(E, "outcome", cc.S * sizeof(int64_t)));
+        double* inv = static_cast<double*>(scratch(E, "inv", cc.S * sizeof(double)));
+        g_active_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(op, cc.S, cc.cregs, active);
+        launched(E);
+        run_reduction(E, cc, R, 0, active, val);
+        g_measure_decide_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(op, cc.S, cc.seed, cc.ids, cc.begin, cc.u, active,
+                                                                      val, cc.cregs, outcome, inv, E->err);
+        launched(E);
+        g_collapse_kernel<<<grid_for(cc.S << (n - 1)), NT, 0, E->stream>>>(cc.state, cc.S, n, op, outcome, inv);
+        launched(E);
+      }
+      return 2ull * R.nq + 1;
+    }
+  }
+  return 0;
+}
+
+void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c) {
+  const unsigned n = dp.host.n;
+  const ProgView& P = dp.view;
+  if (P.nsample == n) {
+    g_sample_scan_kernel<<<grid_for(c.S, 128), 128, 0, E->stream>>>(P, c.state, c.S, c.seed, c.ids, c.begin, c.cregs,
+                                                                    E->err);
+    launched(E);
+    return;
+  }
+  const RedSpec R = outcome_spec(n, dp.host.sample_qubits.data(), P.nsample);
+  const uint64_t chunk = chunk_for(c.S, (R.nq * R.nb + R.nq) * sizeof(double));
+  for (uint64_t off = 0; off < c.S; off += chunk) {
+    const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
+    double* val = static_cast<double*>(scratch(E, "val", cc.S * R.nq * sizeof(double)));
+    run_reduction(E, cc, R, 0, nullptr, val);
+    g_sample_pick_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(P, val, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs,
+                                                               E->err);
+    launched(E);
+  }
+}
+
+size_t resident_smem(const HostDevProgram& h) {
+  const uint64_t A = uint64_t{1} << h.n;
+  uint64_t probs = 16;
+  if (h.eligible && h.sample_qubits.size() < h.n) probs = std::max<uint64_t>(probs, uint64_t{1} << h.sample_qubits.size());
+  return A * sizeof(double2) + (resident_red_doubles() + probs) * sizeof(double);
+}
+
+struct RunConfig {
+  unsigned resident_max = kResidentMaxDefault;
+  unsigned tile_k = kTileDefault;
+};
+
+RunConfig config_of(const ssb_run_options* o) {
+  RunConfig rc;
+  if (o && o->resident_max_qubits) rc.resident_max = o->resident_max_qubits;
+  if (o && o->tile_qubits) rc.tile_k = std::max(3u, std::min(13u, o->tile_qubits));
+  return rc;
+}
+
+// gpu-batch over shot ids [shot_begin, shot_begin+count) (or explicit ids).
+void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begin, uint64_t count, uint64_t seed,
+                      const ssb_run_options* opts, uint64_t* values_dev, ssb_stats* stats) {
+  if (count < 1) throw std::invalid_argument("shots must be >= 1");
+  const RunConfig rc = config_of(opts);
+  const unsigned n = prog->dev.n;
+  const uint64_t launches0 = E->launches;
+  const size_t rsmem = resident_smem(prog->dev);
+  if (n <= rc.resident_max && rsmem <= E->smem_optin) {
+    DevProgram& dp = device_program(E, prog, rc.tile_k);
+    CK(cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, resident_kernel, NT, rsmem));
+    const uint64_t grid = std::min<uint64_t>(count, static_cast<uint64_t>(std::max(1, per_sm)) * E->num_sms);
+    resident_kernel<<<static_cast<unsigned>(grid), NT, rsmem, E->stream>>>(dp.view, seed, nullptr, shot_begin, count,
+                                                                           values_dev, E->err);
+    launched(E);
+    if (stats) {
+      stats->peak_states = std::min<uint64_t>(count, grid);
+      stats->passes = 1;
+      stats->fused_passes = 1;
+    }
+  } else {
+    DevProgram& dp = device_program(E, prog, rc.tile_k);
+    const HostDevProgram& h = dp.host;
+    const uint64_t seg = (uint64_t{1} << n) * sizeof(double2);
+    const uint64_t limit = mem_limit(opts);
+    uint64_t wave = opts && opts->max_batch_size ? opts->max_batch_size : std::max<uint64_t>(1, limit / seg);
+    const uint64_t largest = std::min(wave, count);
+    if (largest * seg > limit)
+      throw shotsim::CapacityError("batch of " + std::to_string(largest) + " shots at " + std::to_string(n) +
+                                   " qubits needs " + std::to_string(largest * seg) +
+                                   " bytes; lower max_batch_size or raise the memory limit");
+    const uint64_t tiles = uint64_t{1} << (n - h.tile_k);
+    wave = std::min<uint64_t>(largest, (uint64_t{1} << 31) / tiles);
+    double2* state = static_cast<double2*>(scratch(E, "state", wave * seg));
+    uint8_t* psel = dp.num_pauli ? static_cast<uint8_t*>(scratch(E, "psel", wave * dp.num_pauli)) : nullptr;
+    const size_t tsmem = (uint64_t{1} << h.tile_k) * sizeof(double2);
+    CK(cudaFuncSetAttribute(tile_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)));
+    uint64_t waves = 0, fused = 0;
+    for (uint64_t w0 = 0; w0 < count; w0 += wave) {
+      const uint64_t S = std::min(wave, count - w0);
+      ++waves;
+      SegCtx c{state, S, seed, nullptr, shot_begin + w0, nullptr, values_dev + w0};
+      CK(cudaMemsetAsync(c.cregs, 0, S * sizeof(uint64_t), E->stream));
+      if (dp.num_pauli) {
+        pauli_decide_kernel<<<grid_for(S * dp.num_pauli), NT, 0, E->stream>>>(dp.view, dp.pauli_site_ops, dp.num_pauli,
+                                                                             seed, nullptr, c.begin, S, psel);
+        launched(E);
+      }
+      fused = 0;
+      for (const Step& st : h.steps) {
+        if (st.kind == S_PASS) {
+          tile_pass_kernel<<<static_cast<unsigned>(S * tiles), NT, tsmem, E->stream>>>(dp.view, st.index, state, S,
+                                                                                      c.cregs, psel, dp.num_pauli);
+          launched(E);
+          ++fused;
+        } else if (st.kind == S_SPECIAL) {
+          apply_op(E, dp, st.index, c, false);
+        } else {
+          sample_terminal(E, dp, c);
+        }
+      }
+    }
+    if (stats) {
+      stats->peak_states = std::min(wave, count);
+      stats->passes = waves;
+      stats->fused_passes = fused;
+    }
+  }
+  if (stats) stats->dispatch_count = E->launches - launches0;
+}
+
+struct DeviceGuard {
+  explicit DeviceGuard(int dev) { CK(cudaSetDevice(dev)); }
+};
+
+}  // namespace
+
+void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h, uint64_t shot_begin,
+                       uint64_t count, uint64_t seed, const ssb_run_options* opts, uint64_t* values_dev,
+                       ssb_stats* stats, uint64_t mem_limit_bytes);
+}  // namespace ssb
+
+using namespace ssb;
+
+extern "C" {
+
+SSB_API int ssb_engine_create(int device, ssb_engine** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null argument");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw CudaError("no CUDA device available (shotsim_b200 has no CPU execution path)");
+    if (device < 0 || device >= count) throw std::invalid_argument("device index out of range");
+    DeviceGuard g(device);
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw CudaError("shotsim_b200 is built for sm_100a (Blackwell); device is sm_" +
+                                         std::to_string(prop.major) + std::to_string(prop.minor));
+    auto E = std::make_unique<ssb_engine>();
+    E->device = device;
+    E->num_sms = prop.multiProcessorCount;
+    E->smem_optin = prop.sharedMemPerBlockOptin;
+    CK(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&E->ev0));
+    CK(cudaEventCreate(&E->ev1));
+    CK(cudaMalloc(&E->err, sizeof(int)));
+    CK(cudaMemset(E->err, 0, sizeof(int)));
+    *out = E.release();
+  });
+}
+
+SSB_API void ssb_engine_destroy(ssb_engine* E) {
+  if (!E) return;
+  cudaSetDevice(E->device);
+  cudaStreamSynchronize(E->stream);
+  E->programs.clear();
+  for (auto& [name, slot] : E->scratch) cudaFree(slot.first);
+  cudaFree(E->err);
+  cudaEventDestroy(E->ev0);
+  cudaEventDestroy(E->ev1);
+  cudaStreamDestroy(E->stream);
+  delete E;
+}
+
+SSB_API void* ssb_engine_stream(ssb_engine* E) { return E ? static_cast<void*>(E->stream) : nullptr; }
+
+SSB_API int ssb_run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begin, uint64_t shot_count,
+                                 uint64_t seed, const ssb_run_options* options, uint64_t* values_out_device,
+                                 ssb_stats* stats) {
+  return guard([&] {
+    if (!E || !prog || !values_out_device) throw std::invalid_argument("null argument");
+    DeviceGuard g(E->device);
+    run_batch_device(E, prog, shot_begin, shot_count, seed, options, values_out_device, stats);
+  });
+}
+
+SSB_API int ssb_run_batch(ssb_engine* E, const ssb_program* prog, uint64_t shot_begin, uint64_t shot_count,
+                          uint64_t seed, const ssb_run_options* options, uint64_t* values_out, ssb_stats* stats) {
+  return guard([&] {
+    if (!E || !prog || !values_out) throw std::invalid_argument("null argument");
+    if (shot_count < 1) throw std::invalid_argument("shots must be >= 1");
+    DeviceGuard g(E->device);
+    const auto t0 = std::chrono::steady_clock::now();
+    uint64_t* dv = static_cast<uint64_t*>(scratch(E, "values", shot_count * sizeof(uint64_t)));
+    CK(cudaEventRecord(E->ev0, E->stream));
+    run_batch_device(E, prog, shot_begin, shot_count, seed, options, dv, stats);
+    CK(cudaMemcpyAsync(values_out, dv, shot_count * sizeof(uint64_t), cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaEventRecord(E->ev1, E->stream));
+    check_device_error(E);
+    if (stats) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, E->ev0, E->ev1));
+      stats->device_seconds = ms * 1e-3;
+      stats->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+SSB_API int ssb_run_branch(ssb_engine* E, const ssb_program* prog, uint64_t shot_begin, uint64_t shot_count,
+                           uint64_t seed, const ssb_run_options* options, uint64_t* values_out, ssb_stats* stats) {
+  return guard([&] {
+    if (!E || !prog || !values_out) throw std::invalid_argument("null argument");
+    if (shot_count < 1) throw std::invalid_argument("shots must be >= 1");
+    DeviceGuard g(E->device);
+    const auto t0 = std::chrono::steady_clock::now();
+    DevProgram& dp = device_program(E, prog, config_of(options).tile_k);
+    uint64_t* dv = static_cast<uint64_t*>(scratch(E, "values", shot_count * sizeof(uint64_t)));
+    EngineView view{E->stream, E->err, &E->launches};
+    ssb_run_options o = options ? *options : ssb_run_options{};
+    if (!options) o.branch_budget = 64;
+    CK(cudaEventRecord(E->ev0, E->stream));
+    run_branch_device(view, dp.view, dp.host, shot_begin, shot_count, seed, &o, dv, stats, mem_limit(options));
+    CK(cudaMemcpyAsync(values_out, dv, shot_count * sizeof(uint64_t), cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaEventRecord(E->ev1, E->stream));
+    check_device_error(E);
+    if (stats) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, E->ev0, E->ev1));
+      stats->device_seconds = ms * 1e-3;
+      stats->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+SSB_API int ssb_histogram_device(ssb_engine* E, const uint64_t* values_device, uint64_t count, uint32_t num_clbits,
+                                 uint64_t* hist_device) {
+  return guard([&] {
+    if (!E || !values_device || !hist_device) throw std::invalid_argument("null argument");
+    if (num_clbits > 24) throw std::invalid_argument("dense histogram limited to 24 clbits");
+    DeviceGuard g(E->device);
+    g_histogram_kernel<<<grid_for(count), NT, 0, E->stream>>>(values_device, count, num_clbits,
+                                                              reinterpret_cast<unsigned long long*>(hist_device));
+    launched(E);
+  });
+}
+
+// ---- operator-level ABI (BatchState) ---------------------------------------
+SSB_API int ssb_batch_create(ssb_engine* E, const ssb_program* prog, const uint64_t* shot_ids, uint64_t count,
+                             uint64_t seed, ssb_batch** out) {
+  return guard([&] {
+    if (!E || !prog || !shot_ids || !out) throw std::invalid_argument("null argument");
+    if (count == 0) throw std::invalid_argument("batch needs at least one shot");
+    DeviceGuard g(E->device);
+    auto B = std::make_unique<ssb_batch>();
+    B->engine = E;
+    B->program = prog;
+    B->size = count;
+    B->seed = seed;
+    const unsigned n = prog->dev.n;
+    CK(cudaMalloc(&B->ids, count * sizeof(uint64_t)));
+    CK(cudaMalloc(&B->cregs, count * sizeof(uint64_t)));
+    CK(cudaMalloc(&B->state, (count << n) * sizeof(double2)));
+    CK(cudaMemcpy(B->ids, shot_ids, count * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    g_init_kernel<<<grid_for(count << n), NT, 0, E->stream>>>(B->state, count, n, B->cregs);
+    launched(E);
+    CK(cudaStreamSynchronize(E->stream));
+    *out = B.release();
+  });
+}
+
+SSB_API void ssb_batch_destroy(ssb_batch* B) {
+  if (!B) return;
+  cudaSetDevice(B->engine->device);
+  cudaStreamSynchronize(B->engine->stream);
+  cudaFree(B->ids);
+  cudaFree(B->cregs);
+  cudaFree(B->state);
+  delete B;
+}
+
+SSB_API int ssb_batch_apply_op(ssb_batch* B, uint64_t op_index, const double* u) {
+  return guard([&] {
+    if (!B) throw std::invalid_argument("null batch");
+    ssb_engine* E = B->engine;
+    DeviceGuard g(E->device);
+    DevProgram& dp = device_program(E, B->program, kTileDefault);
+    if (op_index >= dp.host.ops.size()) throw std::invalid_argument("op index out of range");
+    double* ud = nullptr;
+    if (u) {
+      ud = static_cast<double*>(scratch(E, "udraw", B->size * sizeof(double)));
+      CK(cudaMemcpyAsync(ud, u, B->size * sizeof(double), cudaMemcpyHostToDevice, E->stream));
+    }
+    const SegCtx c{B->state, B->size, B->seed, B->ids, 0, ud, B->cregs};
+    B->dispatches += apply_op(E, dp, static_cast<uint32_t>(op_index), c, true);
+    check_device_error(E);
+  });
+}
+
+SSB_API int ssb_batch_run(ssb_batch* B) {
+  return guard([&] {
+    if (!B) throw std::invalid_argument("null batch");
+    ssb_engine* E = B->engine;
+    DeviceGuard g(E->device);
+    DevProgram& dp = device_program(E, B->program, kTileDefault);
+    const SegCtx c{B->state, B->size, B->seed, B->ids, 0, nullptr, B->cregs};
+    for (uint32_t i = 0; i < dp.host.end; ++i) B->dispatches += apply_op(E, dp, i, c, true);
+    if (dp.host.eligible) {
+      sample_terminal(E, dp, c);
+      ++B->dispatches;
+    }
+    check_device_error(E);
+  });
+}
+
+SSB_API int ssb_batch_read(ssb_batch* B, double* amps, uint64_t* cregs) {
+  return guard([&] {
+    if (!B) throw std::invalid_argument("null batch");
+    DeviceGuard g(B->engine->device);
+    CK(cudaStreamSynchronize(B->engine->stream));
+    const unsigned n = B->program->dev.n;
+    if (amps) CK(cudaMemcpy(amps, B->state, (B->size << n) * sizeof(double2), cudaMemcpyDeviceToHost));
+    if (cregs) CK(cudaMemcpy(cregs, B->cregs, B->size * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  });
+}
+
+SSB_API int ssb_batch_write_segment(ssb_batch* B, uint64_t s, const double* amps) {
+  return guard([&] {
+    if (!B || !amps) throw std::invalid_argument("null argument");
+    if (s >= B->size) throw std::invalid_argument("segment index out of range");
+    DeviceGuard g(B->engine->device);
+    CK(cudaStreamSynchronize(B->engine->stream));
+    const unsigned n = B->program->dev.n;
+    CK(cudaMemcpy(B->state + (s << n), amps, (uint64_t{1} << n) * sizeof(double2), cudaMemcpyHostToDevice));
+  });
+}
+
+SSB_API uint64_t ssb_batch_dispatches(const ssb_batch* B) { return B ? B->dispatches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,649 @@
+// sm_100a kernels of the shotsim_b200 engine.
+//
+//  resident_kernel   — SM-resident executor (paper SIV.A taken to its limit):
+//                      one CTA owns one shot's whole state in shared memory and
+//                      interprets the entire instrumented program (gates, Pauli
+//                      / Kraus sites, measure, reset, conditionals, terminal
+//                      sampling) in ONE launch. n <= 13 (2^13 x 16 B = 128 KiB).
+//  tile_pass_kernel  — HBM-streamed executor: one CTA per (shot, 2^k tile);
+//                      applies a planned run of gates / Pauli sites whose
+//                      qubits are all tile-local between one HBM read and one
+//                      HBM write of the tile (devprog.cpp plan_passes).
+//  g_*               — op-at-a-time batched kernels over S HBM segments (the
+//                      reference BatchState shape, exec_batch.cpp:54-198): used
+//                      for Kraus / measure / reset / terminal sampling in the
+//                      streamed executor and for the operator-level C ABI.
+#pragma once
+
+#include "cta_ops.cuh"
+
+namespace ssb {
+
+enum DevError : int { DEV_OK = 0, DEV_DEGENERATE = 1 };
+
+// What the executors need from an engine (stream, device error flag, launch
+// counter).
+struct EngineView {
+  cudaStream_t stream;
+  int* err;
+  uint64_t* launches;
+};
+
+struct ProgView {
+  const DevOp* ops;
+  const DevTerm* terms;
+  const DevChannel* channels;
+  const double2* mats;        // 16 double2 per slot
+  const uint64_t* scaled_cls; // per slot
+  const uint8_t* sample_qubits;
+  const uint8_t* write_clbit;
+  const uint8_t* write_pos;
+  const PassDesc* passes;
+  const PassOp* pass_ops;
+  uint32_t n, end, nsample, nwrites;
+  uint64_t num_events;
+  uint32_t eligible, sample_identity;
+};
+
+__device__ __forceinline__ void raise(int* err, int code) { atomicCAS(err, 0, code); }
+
+__device__ __forceinline__ uint64_t shot_of(const uint64_t* ids, uint64_t begin, uint64_t s) {
+  return ids ? ids[s] : begin + s;
+}
+
+__device__ __forceinline__ uint64_t apply_sample_outcome(const ProgView& P, uint64_t creg, uint64_t outcome) {
+  for (uint32_t i = 0; i < P.nwrites; ++i) {
+    const unsigned c = P.write_clbit[i], b = P.write_pos[i];
+    creg = (creg & ~(uint64_t{1} << c)) | (((outcome >> b) & 1) << c);
+  }
+  return creg;
+}
+
+// Sequential inverse-CDF over |a[idx(m)]|^2, m = 0..2^n-1 (terminal sampling
+// with every qubit sampled: groups = 1, statevector.cpp:142-164 + 185-197).
+// One thread. Unrolled x8 so the loads and squares overlap the add chain.
+template <class Amp>
+__device__ __forceinline__ bool scan_full(Amp amp, uint64_t count, bool identity, const uint8_t* sq, unsigned k,
+                                          double u, uint64_t* out) {
+  double cum = 0.0;
+  uint64_t last = count;
+  for (uint64_t m0 = 0; m0 < count; m0 += 8) {
+    double p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t m = m0 + j;
+      p[j] = 0.0;
+      if (m < count) p[j] = c_norm(amp(identity ? m : scatter_bits(m, sq, k)));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (m0 + j >= count) break;
+      cum = __dadd_rn(cum, p[j]);
+      if (u < cum) {
+        *out = m0 + j;
+        return true;
+      }
+      if (p[j] > 0.0) last = m0 + j;
+    }
+  }
+  *out = last == count ? 0 : last;
+  return last != count;
+}
+
+// Shared-memory layout of resident_kernel: state | red (512) | probs (2^k).
+__host__ __device__ constexpr uint64_t resident_red_doubles() { return 513; }
+
+// ---------------------------------------------------------------------------
+static __global__ void __launch_bounds__(NT) resident_kernel(ProgView P, uint64_t seed, const uint64_t* ids,
+                                                      uint64_t shot_begin, uint64_t S, uint64_t* values,
+                                                      int* err) {
+  extern __shared__ double2 smem[];
+  const unsigned n = P.n;
+  const uint64_t A = uint64_t{1} << n;
+  double2* st = smem;
+  double* red = reinterpret_cast<double*>(st + A);
+  double* probs = red + resident_red_doubles();
+  __shared__ uint64_t bc_out;
+  __shared__ double bc_p;
+
+  for (uint64_t s = blockIdx.x; s < S; s += gridDim.x) {
+    const uint64_t shot = shot_of(ids, shot_begin, s);
+    for (uint64_t j = threadIdx.x; j < A; j += NT) st[j] = make_double2(j == 0 ? 1.0 : 0.0, 0.0);
+    uint64_t creg = 0;
+    __syncthreads();
+    for (uint32_t i = 0; i < P.end; ++i) {
+      const DevOp& op = P.ops[i];
+      const uint8_t kind = op.kind;
+      if (kind == K_BARRIER) continue;
+      if (op.has_cond && (creg & op.cond_mask) != op.cond_value) continue;
+      if (kind == K_GATE) {
+        if (op.skip) continue;
+        if (op.nq == 1) {
+          double2 m[4];
+          load_matrix<2>(P.mats + 16 * op.aux, m);
+          cta_apply1(st, n, op.q[0], m, op.cls);
+        } else {
+          double2 m[16];
+          load_matrix<4>(P.mats + 16 * op.aux, m);
+          cta_apply2(st, n, op.q[0], op.q[1], m, op.cls);
+        }
+        __syncthreads();
+      } else if (kind == K_PAULI) {
+        const DevTerm* terms = P.terms + op.aux;
+        const int t = pick_term(terms, op.count, keyed_uniform(seed, shot, op.event));
+        if (!terms[t].identity) {
+          cta_pauli(st, n, terms[t].x, terms[t].z, terms[t].num_y);
+          __syncthreads();
+        }
+      } else if (kind == K_KRAUS) {
+        // apply_kraus_single (exec_naive.cpp:29-42): sequential scan, early exit.
+        const DevChannel ch = P.channels[op.aux];
+        const double u = keyed_uniform(seed, shot, op.event);
+        double cum = 0.0, p = 0.0;
+        uint32_t sel = ch.nmat - 1;
+        for (uint32_t mi = 0; mi < ch.nmat; ++mi) {
+          const double2* mg = P.mats + 16 * (ch.mat_begin + mi);
+          if (ch.arity == 1) {
+            double2 m[4];
+            load_matrix<2>(mg, m);
+            p = cta_expval1(st, n, op.q[0], m, red);
+          } else {
+            double2 m[16];
+            load_matrix<4>(mg, m);
+            p = cta_expval2(st, n, op.q, m, red);
+          }
+          cum = __dadd_rn(cum, p);
+          if (u < cum) {
+            sel = mi;
+            break;
+          }
+        }
+        if (!(p > 0.0)) {
+          if (threadIdx.x == 0) raise(err, DEV_DEGENERATE);
+          p = 1.0;
+        }
+        const double inv = __ddiv_rn(1.0, __dsqrt_rn(p));
+        const uint32_t slot = ch.mat_begin + sel;
+        if (ch.arity == 1) {
+          double2 m[4];
+          load_matrix<2>(P.mats + 16 * slot, m);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) m[e] = c_scale(m[e], inv);
+          cta_apply1(st, n, op.q[0], m, P.scaled_cls[slot]);
+        } else {
+          double2 m[16];
+          load_matrix<4>(P.mats + 16 * slot, m);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) m[e] = c_scale(m[e], inv);
+          cta_apply2(st, n, op.q[0], op.q[1], m, P.scaled_cls[slot]);
+        }
+        __syncthreads();
+      } else {  // K_MEASURE / K_RESET (measure_single / reset_single)
+        const unsigned k = op.nq;
+        cta_outcome_probs(st, n, op.q, k, probs, red);
+        if (threadIdx.x == 0) {
+          uint64_t o = 0;
+          if (!pick_outcome(probs, uint64_t{1} << k, keyed_uniform(seed, shot, op.event), &o)) raise(err, DEV_DEGENERATE);
+          bc_out = o;
+          bc_p = probs[o];
+        }
+        __syncthreads();
+        const uint64_t o = bc_out;
+        double p = bc_p;
+        if (!(p > 0.0)) {
+          if (threadIdx.x == 0) raise(err, DEV_DEGENERATE);
+          p = 1.0;
+        }
+        uint64_t qmask = 0;
+        for (unsigned b = 0; b < k; ++b) qmask |= uint64_t{1} << op.q[b];
+        const uint64_t off = scatter_bits(o, op.q, k);
+        cta_collapse(st, n, qmask, off, __ddiv_rn(1.0, __dsqrt_rn(p)), kind == K_RESET ? off : 0);
+        if (kind == K_MEASURE) creg = write_bits(creg, op.c, k, o);
+        __syncthreads();
+      }
+    }
+    if (P.eligible) {
+      const unsigned k = P.nsample;
+      const double u = keyed_uniform(seed, shot, P.num_events);
+      if (k == n) {
+        if (threadIdx.x == 0) {
+          uint64_t o = 0;
+          if (!scan_full([&](uint64_t idx) { return st[idx]; }, A, P.sample_identity, P.sample_qubits, k, u, &o))
+            raise(err, DEV_DEGENERATE);
+          bc_out = o;
+        }
+      } else {
+        cta_outcome_probs(st, n, P.sample_qubits, k, probs, red);
+        if (threadIdx.x == 0) {
+          uint64_t o = 0;
+          if (!pick_outcome(probs, uint64_t{1} << k, u, &o)) raise(err, DEV_DEGENERATE);
+          bc_out = o;
+        }
+      }
+      __syncthreads();
+      creg = apply_sample_outcome(P, creg, bc_out);
+    }
+    if (threadIdx.x == 0) values[s] = creg;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Streamed executor: fused tile pass. Grid: S * 2^(n-k) CTAs; CTA (s, t) owns
+// tile t of shot s: local index l <-> global index pdep(t, ~lmask) | pdep(l, lmask).
+__device__ __forceinline__ uint64_t pdep_positions(uint64_t v, const uint8_t* pos, unsigned k) {
+  uint64_t out = 0;
+  for (unsigned j = 0; j < k; ++j) out |= ((v >> j) & 1) << pos[j];
+  return out;
+}
+
+static __global__ void __launch_bounds__(NT) tile_pass_kernel(ProgView P, uint32_t pass_index, double2* state,
+                                                       uint64_t S, const uint64_t* cregs,
+                                                       const uint8_t* pauli_sel, uint32_t num_pauli) {
+  extern __shared__ double2 tile[];
+  const PassDesc& pd = P.passes[pass_index];
+  const unsigned n = P.n, k = pd.k;
+  const uint64_t tiles = uint64_t{1} << (n - k), L = uint64_t{1} << k;
+  const uint64_t s = blockIdx.x / tiles, t = blockIdx.x % tiles;
+  if (s >= S) return;
+  __shared__ uint8_t hpos[32];
+  if (threadIdx.x == 0) {
+    for (unsigned q = 0, j = 0; q < n; ++q)
+      if (!((pd.lmask >> q) & 1)) hpos[j++] = static_cast<uint8_t>(q);
+  }
+  __syncthreads();
+  const uint64_t base = pdep_positions(t, hpos, n - k);
+  double2* seg = state + (s << n);
+  // Low local bits: element l = threadIdx.x + NT*i; pdep splits into a
+  // per-thread part and a per-iteration part.
+  const unsigned kt = k < 8 ? k : 8;
+  const uint64_t lo_part = pdep_positions(threadIdx.x, pd.lq, kt);
+  if (pd.first) {
+    for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) {
+      const uint64_t g = base | lo_part | pdep_positions(i, pd.lq + kt, k - kt);
+      tile[l] = make_double2(g == 0 ? 1.0 : 0.0, 0.0);
+    }
+  } else {
+    for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
+      tile[l] = seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)];
+  }
+  __syncthreads();
+  const uint64_t creg = cregs ? cregs[s] : 0;
+  const uint8_t* sel = pauli_sel + s * num_pauli;
+  for (uint32_t i = pd.begin; i < pd.end; ++i) {
+    const PassOp po = P.pass_ops[i];
+    const DevOp& op = P.ops[po.op];
+    if (op.has_cond && (creg & op.cond_mask) != op.cond_value) continue;
+    if (op.kind == K_GATE) {
+      if (op.nq == 1) {
+        double2 m[4];
+        load_matrix<2>(P.mats + 16 * op.aux, m);
+        cta_apply1(tile, k, po.lq[0], m, op.cls);
+      } else {
+        double2 m[16];
+        load_matrix<4>(P.mats + 16 * op.aux, m);
+        cta_apply2(tile, k, po.lq[0], po.lq[1], m, op.cls);
+      }
+      __syncthreads();
+    } else {  // K_PAULI with a precomputed per-shot term
+      const uint8_t term = sel[op.site];
+      const DevTerm& tm = P.terms[op.aux + term];
+      if (tm.identity) continue;
+      uint32_t x = 0, z = 0;
+      for (unsigned b = 0; b < op.nq; ++b) {
+        x |= ((tm.x >> op.q[b]) & 1u) << po.lq[b];
+        z |= ((tm.z >> op.q[b]) & 1u) << po.lq[b];
+      }
+      cta_pauli(tile, k, x, z, tm.num_y);
+      __syncthreads();
+    }
+  }
+  for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
+    seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)] = tile[l];
+}
+
+// Per-(shot, Pauli site) term choice for a wave: sel[s][site] (u8).
+static __global__ void pauli_decide_kernel(ProgView P, const uint32_t* site_ops, uint32_t num_sites, uint64_t seed,
+                                    const uint64_t* ids, uint64_t shot_begin, uint64_t S, uint8_t* sel) {
+  const uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (idx >= S * num_sites) return;
+  const uint64_t s = idx / num_sites, site = idx % num_sites;
+  const DevOp& op = P.ops[site_ops[site]];
+  sel[idx] = static_cast<uint8_t>(pick_term(P.terms + op.aux, op.count, keyed_uniform(seed, shot_of(ids, shot_begin, s), op.event)));
+}
+
+// ---------------------------------------------------------------------------
+// Op-at-a-time batched kernels over S HBM segments (BatchState shape).
+__device__ __forceinline__ bool active_shot(const DevOp& op, const uint64_t* cregs, uint64_t s) {
+  return !op.has_cond || (cregs[s] & op.cond_mask) == op.cond_value;
+}
+
+// slots: optional segment indirection (branch executor's state pool).
+__device__ __forceinline__ uint64_t seg_of(const uint32_t* slots, uint64_t s) { return slots ? slots[s] : s; }
+
+template <int K>
+static __global__ void g_gate_kernel(double2* st, uint64_t S, unsigned n, DevOp op, const double2* mats,
+                              const uint64_t* cregs, const uint32_t* slots = nullptr) {
+  constexpr int D = 1 << K;
+  double2 m[D * D];
+  load_matrix<D>(mats + 16 * op.aux, m);
+  const uint64_t per = uint64_t{1} << (n - K), total = S * per;
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t s = idx >> (n - K), p = idx & (per - 1);  // shot_index (exec_batch.hpp:12-14)
+    if (!active_shot(op, cregs, s)) continue;
+    double2* a = st + (seg_of(slots, s) << n);
+    if constexpr (K == 1) {
+      const uint64_t i0 = insert_zero(p, op.q[0]), i1 = i0 | (uint64_t{1} << op.q[0]);
+      const double2 v[2] = {a[i0], a[i1]};
+      a[i0] = row_apply<2>(m, op.cls, 0, v);
+      a[i1] = row_apply<2>(m, op.cls, 1, v);
+    } else {
+      const unsigned pl = min(op.q[0], op.q[1]), ph = max(op.q[0], op.q[1]);
+      const uint64_t d0 = uint64_t{1} << op.q[0], d1 = uint64_t{1} << op.q[1];
+      const uint64_t b = insert_zero(insert_zero(p, pl), ph);
+      const double2 v[4] = {a[b], a[b | d0], a[b | d1], a[b | d0 | d1]};
+      a[b] = row_apply<4>(m, op.cls, 0, v);
+      a[b | d0] = row_apply<4>(m, op.cls, 1, v);
+      a[b | d1] = row_apply<4>(m, op.cls, 2, v);
+      a[b | d0 | d1] = row_apply<4>(m, op.cls, 3, v);
+    }
+  }
+}
+
+// Per-shot draw: keyed stream, or the explicit u[] of the *_with test hooks.
+__device__ __forceinline__ double draw(const double* u, uint64_t seed, const uint64_t* ids, uint64_t begin,
+                                       uint64_t s, uint64_t event) {
+  return u ? u[s] : keyed_uniform(seed, shot_of(ids, begin, s), event);
+}
+
+// sel[s] = chosen term, or -1 (inactive or identity: no work, exec_batch.cpp:64-82).
+static __global__ void g_pauli_decide_kernel(ProgView P, DevOp op, uint64_t S, uint64_t seed, const uint64_t* ids,
+                                      uint64_t begin, const double* u, const uint64_t* cregs, int* sel) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  int t = -1;
+  if (active_shot(op, cregs, s)) {
+    t = pick_term(P.terms + op.aux, op.count, draw(u, seed, ids, begin, s, op.event));
+    if (P.terms[op.aux + t].identity) t = -1;
+  }
+  sel[s] = t;
+}
+
+static __global__ void g_pauli_apply_kernel(double2* st, uint64_t S, unsigned n, const DevTerm* terms, const int* sel) {
+  const uint64_t per = uint64_t{1} << (n - 1), total = S * per;
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t s = idx >> (n - 1), p = idx & (per - 1);
+    const int t = sel[s];
+    if (t < 0) continue;
+    const DevTerm tm = terms[t];
+    double2* a = st + (s << n);
+    if (tm.x == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t j = 2 * p + h;
+        double2 v = pauli_phase(tm.num_y, a[j]);
+        if (__popcll(j & tm.z) & 1) v = c_neg(v);
+        a[j] = v;
+      }
+    } else {
+      const unsigned xmax = 31 - __clz(tm.x);
+      const uint64_t i0 = insert_zero(p, xmax), i1 = i0 ^ tm.x;
+      double2 t0 = pauli_phase(tm.num_y, a[i1]), t1 = pauli_phase(tm.num_y, a[i0]);
+      if (__popcll(i0 & tm.z) & 1) t0 = c_neg(t0);
+      if (__popcll(i1 & tm.z) & 1) t1 = c_neg(t1);
+      a[i0] = t0;
+      a[i1] = t1;
+    }
+  }
+}
+
+// Exact reductions over HBM segments. Quantities per shot: outcomes (measure,
+// sampling) or Kraus matrices. Partials layout: part[(s*nq + q)*nb + b].
+enum RedMode : int { R_OUTCOME = 0, R_EXPVAL1 = 1, R_EXPVAL2 = 2 };
+struct RedSpec {
+  int mode;
+  unsigned n, k;        // k: measured qubits (R_OUTCOME) / matrix arity
+  uint8_t q[32];
+  uint8_t sorted[32];
+  uint32_t nq;          // quantities per shot
+  uint64_t nb;          // blocks per quantity
+  uint64_t blk;         // elements per block
+  const double2* mats;  // R_EXPVAL*: nq consecutive matrix slots
+};
+
+static __global__ void g_reduce_kernel(const double2* st, uint64_t S, RedSpec R, const uint8_t* active, double* part,
+                                const uint32_t* slots = nullptr) {
+  const uint64_t total = S * R.nq * R.nb;
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t b = idx % R.nb, qs = idx / R.nb, qi = qs % R.nq, s = qs / R.nq;
+    if (active && !active[s]) continue;
+    const double2* a = st + (seg_of(slots, s) << R.n);
+    double acc = 0.0;
+    if (R.mode == R_OUTCOME) {
+      const uint64_t off = scatter_bits(qi, R.q, R.k);
+      for (uint64_t g = b * R.blk; g < (b + 1) * R.blk; ++g)
+        acc = __dadd_rn(acc, c_norm(a[expand_sorted(g, R.sorted, R.k) | off]));
+    } else if (R.mode == R_EXPVAL1) {
+      const double2* m = R.mats + 16 * qi;
+      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
+      const unsigned t = R.q[0];
+      for (uint64_t i = b * R.blk; i < (b + 1) * R.blk; ++i) {
+        const uint64_t i0 = insert_zero(i, t), i1 = i0 | (uint64_t{1} << t);
+        const double2 a0 = a[i0], a1 = a[i1];
+        acc = __dadd_rn(acc, c_norm(c_add(c_mul(m0, a0), c_mul(m1, a1))));
+        acc = __dadd_rn(acc, c_norm(c_add(c_mul(m2, a0), c_mul(m3, a1))));
+      }
+    } else {
+      double2 m[16];
+      load_matrix<4>(R.mats + 16 * qi, m);
+      const uint64_t off[4] = {0, uint64_t{1} << R.q[0], uint64_t{1} << R.q[1],
+                               (uint64_t{1} << R.q[0]) | (uint64_t{1} << R.q[1])};
+      for (uint64_t g = b * R.blk; g < (b + 1) * R.blk; ++g) {
+        const uint64_t base = expand_sorted(g, R.sorted, 2);
+        double2 in[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) in[c] = a[base + off[c]];
+        double row = 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) v = c_add(v, c_mul(m[4 * r + c], in[c]));
+          row = __dadd_rn(row, c_norm(v));
+        }
+        acc = __dadd_rn(acc, row);
+      }
+    }
+    part[idx] = acc;
+  }
+}
+
+// part (nb per quantity) -> val[s*nq + q] (one thread each). 512-block
+// partials finish with pairwise_sum over the partials (common.cpp:12-26);
+// expval_generic leaves (already the 8-element leaves of pairwise_sum over
+// all groups) finish with the balanced tree above them.
+static __global__ void g_finish_kernel(uint64_t S, uint32_t nq, uint64_t nb, int leaves_tree, const uint8_t* active,
+                                double* part, double* val) {
+  const uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (idx >= S * nq) return;
+  if (active && !active[idx / nq]) return;
+  double* v = part + idx * nb;
+  if (nb == 1) {
+    val[idx] = v[0];
+  } else if (!leaves_tree) {
+    val[idx] = pairwise_inplace(v, nb);
+  } else {
+    for (uint64_t w = nb; w > 1; w /= 2)
+      for (uint64_t i = 0; i < w / 2; ++i) v[i] = __dadd_rn(v[2 * i], v[2 * i + 1]);
+    val[idx] = v[0];
+  }
+}
+
+static __global__ void g_active_kernel(DevOp op, uint64_t S, const uint64_t* cregs, uint8_t* active) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s < S) active[s] = active_shot(op, cregs, s) ? 1 : 0;
+}
+
+// Kraus choice per shot (apply_kraus_single semantics on precomputed p_i):
+// writes the scaled matrix (16 double2) and its class word, or marks inactive.
+static __global__ void g_kraus_decide_kernel(ProgView P, DevOp op, uint64_t S, uint64_t seed, const uint64_t* ids,
+                                      uint64_t begin, const double* u, const uint8_t* active, const double* val,
+                                      double2* scaled, uint64_t* cls, int* chosen, int* err) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  if (!active[s]) {
+    chosen[s] = -1;
+    return;
+  }
+  const DevChannel ch = P.channels[op.aux];
+  const double uu = draw(u, seed, ids, begin, s, op.event);
+  double cum = 0.0, p = 0.0;
+  uint32_t sel = ch.nmat - 1;
+  for (uint32_t i = 0; i < ch.nmat; ++i) {
+    p = val[s * ch.nmat + i];
+    cum = __dadd_rn(cum, p);
+    if (uu < cum) {
+      sel = i;
+      break;
+    }
+  }
+  if (!(p > 0.0)) {
+    raise(err, DEV_DEGENERATE);
+    p = 1.0;
+  }
+  const double inv = __ddiv_rn(1.0, __dsqrt_rn(p));
+  const uint32_t slot = ch.mat_begin + sel;
+  for (int e = 0; e < 16; ++e) scaled[s * 16 + e] = c_scale(P.mats[16 * slot + e], inv);
+  cls[s] = P.scaled_cls[slot];
+  chosen[s] = static_cast<int>(sel);
+}
+
+template <int K>
+static __global__ void g_kraus_apply_kernel(double2* st, uint64_t S, unsigned n, DevOp op, const double2* scaled,
+                                     const uint64_t* cls, const int* chosen) {
+  constexpr int D = 1 << K;
+  const uint64_t per = uint64_t{1} << (n - K), total = S * per;
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t s = idx >> (n - K), p = idx & (per - 1);
+    if (chosen[s] < 0) continue;
+    double2 m[D * D];
+    load_matrix<D>(scaled + 16 * s, m);
+    const uint64_t c = cls[s];
+    double2* a = st + (s << n);
+    if constexpr (K == 1) {
+      const uint64_t i0 = insert_zero(p, op.q[0]), i1 = i0 | (uint64_t{1} << op.q[0]);
+      const double2 v[2] = {a[i0], a[i1]};
+      a[i0] = row_apply<2>(m, c, 0, v);
+      a[i1] = row_apply<2>(m, c, 1, v);
+    } else {
+      const unsigned pl = min(op.q[0], op.q[1]), ph = max(op.q[0], op.q[1]);
+      const uint64_t d0 = uint64_t{1} << op.q[0], d1 = uint64_t{1} << op.q[1];
+      const uint64_t b = insert_zero(insert_zero(p, pl), ph);
+      const double2 v[4] = {a[b], a[b | d0], a[b | d1], a[b | d0 | d1]};
+      a[b] = row_apply<4>(m, c, 0, v);
+      a[b | d0] = row_apply<4>(m, c, 1, v);
+      a[b | d1] = row_apply<4>(m, c, 2, v);
+      a[b | d0 | d1] = row_apply<4>(m, c, 3, v);
+    }
+  }
+}
+
+// Measure / reset decision per shot: pick over val[s*2^k..], write creg.
+static __global__ void g_measure_decide_kernel(DevOp op, uint64_t S, uint64_t seed, const uint64_t* ids, uint64_t begin,
+                                        const double* u, const uint8_t* active, const double* val, uint64_t* cregs,
+                                        int64_t* outcome, double* inv, int* err) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  if (!active[s]) {
+    outcome[s] = -1;
+    return;
+  }
+  const uint64_t no = uint64_t{1} << op.nq;
+  uint64_t o = 0;
+  if (!pick_outcome(val + s * no, no, draw(u, seed, ids, begin, s, op.event), &o)) raise(err, DEV_DEGENERATE);
+  double p = val[s * no + o];
+  if (!(p > 0.0)) {
+    raise(err, DEV_DEGENERATE);
+    p = 1.0;
+  }
+  outcome[s] = static_cast<int64_t>(o);
+  inv[s] = __ddiv_rn(1.0, __dsqrt_rn(p));
+  if (op.kind == K_MEASURE) cregs[s] = write_bits(cregs[s], op.c, op.nq, o);
+}
+
+static __global__ void g_collapse_kernel(double2* st, uint64_t S, unsigned n, DevOp op, const int64_t* outcome,
+                                  const double* inv) {
+  const uint64_t per = uint64_t{1} << (n - 1), total = S * per;
+  uint64_t qmask = 0;
+  for (unsigned b = 0; b < op.nq; ++b) qmask |= uint64_t{1} << op.q[b];
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t s = idx >> (n - 1), p = idx & (per - 1);
+    if (outcome[s] < 0) continue;
+    const uint64_t off = scatter_bits(static_cast<uint64_t>(outcome[s]), op.q, op.nq);
+    const uint64_t xfix = op.kind == K_RESET ? off : 0;
+    const double f = inv[s];
+    double2* a = st + (s << n);
+    const double2 zero = make_double2(0.0, 0.0);
+    if (xfix == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t j = 2 * p + h;
+        a[j] = ((j & qmask) == off) ? c_scale(a[j], f) : zero;
+      }
+    } else {
+      const unsigned xmax = 63 - __clzll(xfix);
+      const uint64_t i0 = insert_zero(p, xmax), i1 = i0 ^ xfix;
+      const double2 a0 = a[i0], a1 = a[i1];
+      a[i0] = ((i1 & qmask) == off) ? c_scale(a1, f) : zero;
+      a[i1] = ((i0 & qmask) == off) ? c_scale(a0, f) : zero;
+    }
+  }
+}
+
+// Terminal sampling with every qubit sampled: one thread per shot scans its
+// segment sequentially (exact reference order).
+static __global__ void g_sample_scan_kernel(ProgView P, const double2* st, uint64_t S, uint64_t seed, const uint64_t* ids,
+                                     uint64_t begin, uint64_t* cregs, int* err) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const unsigned n = P.n;
+  const double2* a = st + (s << n);
+  uint64_t o = 0;
+  if (!scan_full([&](uint64_t idx) { return a[idx]; }, uint64_t{1} << n, P.sample_identity, P.sample_qubits, n,
+                 keyed_uniform(seed, shot_of(ids, begin, s), P.num_events), &o))
+    raise(err, DEV_DEGENERATE);
+  cregs[s] = apply_sample_outcome(P, cregs[s], o);
+}
+
+// Terminal sampling over k < n qubits: pick over precomputed probabilities.
+static __global__ void g_sample_pick_kernel(ProgView P, const double* val, uint64_t S, uint64_t seed, const uint64_t* ids,
+                                     uint64_t begin, uint64_t* cregs, int* err) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const uint64_t no = uint64_t{1} << P.nsample;
+  uint64_t o = 0;
+  if (!pick_outcome(val + s * no, no, keyed_uniform(seed, shot_of(ids, begin, s), P.num_events), &o))
+    raise(err, DEV_DEGENERATE);
+  cregs[s] = apply_sample_outcome(P, cregs[s], o);
+}
+
+static __global__ void g_init_kernel(double2* st, uint64_t S, unsigned n, uint64_t* cregs) {
+  const uint64_t total = S << n;
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    st[idx] = make_double2((idx & ((uint64_t{1} << n) - 1)) == 0 ? 1.0 : 0.0, 0.0);
+    if ((idx & ((uint64_t{1} << n) - 1)) == 0 && cregs) cregs[idx >> n] = 0;
+  }
+}
+
+static __global__ void g_histogram_kernel(const uint64_t* values, uint64_t count, uint32_t bits, unsigned long long* hist) {
+  const uint64_t i = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (i < count) atomicAdd(&hist[values[i] & ((uint64_t{1} << bits) - 1)], 1ull);
+}
+
+}  // namespace ssb
