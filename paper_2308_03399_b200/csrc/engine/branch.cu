@@ -329,6 +329,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
     }
     if (next_slot >= pool_cap) {  // grow (rare): copy live slots over
       const uint64_t ncap = std::min<uint64_t>(max_slots, pool_cap * 2);
+      if (ncap <= pool_cap) throw std::logic_error("branch slot pool exhausted");
       double2* np = nullptr;
       CKB(cudaMalloc(&np, ncap * seg));
       CKB(cudaMemcpyAsync(np, pool_buf.p, pool_cap * seg, cudaMemcpyDeviceToDevice, s));
@@ -521,7 +522,13 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       std::vector<uint2> pairs;
       std::vector<ChildOp> kids;
       uint64_t new_off = 0, wait_off = nwaiting;
-      std::vector<uint8_t> parent_used(nn, 0);
+      // Parents without a kept child die first, so the pool never holds more
+      // than `budget` live states (+ the root).
+      std::vector<uint8_t> parent_used(nn, 0), parent_kept(nn, 0);
+      for (size_t g = 0; g < groups.size(); ++g)
+        if (keep[g]) parent_kept[groups[g].parent] = 1;
+      for (uint64_t x = 0; x < nn; ++x)
+        if (!parent_kept[x]) free_slots.push_back(live[x].slot);
       for (size_t g = 0; g < groups.size(); ++g) {
         const Cand& c = groups[g];
         const uint64_t gi = c.parent * nkeys + c.key;
@@ -558,10 +565,6 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
         next.push_back({slot, new_off, c.count, creg});
         new_off += c.count;
       }
-      for (uint64_t x = 0; x < nn; ++x)
-        if (!parent_used[x]) free_slots.push_back(live[x].slot);
-      // The free list must not hand out a slot that is a copy source: sources
-      // are parents that have a kept first child, so they are never freed.
 
       uint64_t* dst = ddst.get(nn * nkeys);
       unsigned long long* cursor = dcursor.get(nn * nkeys);

@@ -157,13 +157,19 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
   const unsigned n = d.n;
   const unsigned k = std::min(tile_k, n);
   d.tile_k = k;
-  const uint32_t low = (1u << std::min(3u, k)) - 1;
+  // Always-local low qubits (coalesced 2^low-amplitude rows), leaving room for
+  // any 2-qubit op so a fresh pass can always take the next op.
+  const unsigned low_bits = k >= 2 ? std::min(3u, k - 2) : 0;
+  const uint32_t low = (1u << low_bits) - 1;
   uint32_t cur = low;
   std::vector<uint32_t> cur_ops;
   bool need_init = true;
 
   auto close = [&](bool force) {
-    if (cur_ops.empty() && !(force && need_init)) return;
+    if (cur_ops.empty() && !(force && need_init)) {
+      cur = low;
+      return;
+    }
     uint32_t mask = cur;
     for (unsigned q = 0; q < n && static_cast<unsigned>(std::popcount(mask)) < k; ++q) mask |= 1u << q;
     PassDesc pd{};
