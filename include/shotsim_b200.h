@@ -140,6 +140,8 @@ typedef struct ssb_run_options {
   uint32_t collect_leaf_stats;
   uint32_t resident_max_qubits; /* n <= this: whole program SM-resident (0: 13) */
   uint32_t tile_qubits;      /* streamed mode: local qubits per HBM tile (0: 12) */
+  uint32_t profile;          /* 1: per-kernel-class CUDA-event times in stats   */
+  uint32_t reserved;
 } ssb_run_options;
 
 typedef struct ssb_stats {
@@ -149,6 +151,11 @@ typedef struct ssb_stats {
   uint64_t fused_passes;     /* batch: HBM tile passes per wave               */
   double device_seconds;     /* CUDA-event time of the device work            */
   double wall_seconds;
+  /* profile=1 only: CUDA-event time per kernel class on the engine stream   */
+  double pass_seconds;       /* fused gate/Pauli passes (tile or resident)    */
+  uint64_t pass_launches;
+  double special_seconds;    /* Kraus / measure / reset op-at-a-time kernels  */
+  double sample_seconds;     /* terminal sampling                             */
 } ssb_stats;
 
 SSB_API const char* ssb_last_error(void);

@@ -66,6 +66,7 @@ class RunOptionsC(C.Structure):
         ("max_batch_size", C.c_uint64), ("branch_budget", C.c_uint64), ("mem_limit_bytes", C.c_uint64),
         ("check_norms", C.c_uint32), ("collect_leaf_stats", C.c_uint32),
         ("resident_max_qubits", C.c_uint32), ("tile_qubits", C.c_uint32),
+        ("profile", C.c_uint32), ("reserved", C.c_uint32),
     ]
 
 
@@ -73,6 +74,8 @@ class StatsC(C.Structure):
     _fields_ = [
         ("dispatch_count", C.c_uint64), ("peak_states", C.c_uint64), ("passes", C.c_uint64),
         ("fused_passes", C.c_uint64), ("device_seconds", C.c_double), ("wall_seconds", C.c_double),
+        ("pass_seconds", C.c_double), ("pass_launches", C.c_uint64), ("special_seconds", C.c_double),
+        ("sample_seconds", C.c_double),
     ]
 
 

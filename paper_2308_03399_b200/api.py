@@ -93,11 +93,12 @@ class RunOptions:
     collect_leaf_stats: bool = False
     resident_max_qubits: int = 0  # tuning: 0 = engine default
     tile_qubits: int = 0
+    profile: bool = False         # per-kernel-class CUDA-event timing in the stats
 
     def to_c(self) -> _lib.RunOptionsC:
         return _lib.RunOptionsC(self.max_batch_size, self.branch_budget, self.mem_limit_bytes,
                                 int(self.check_norms), int(self.collect_leaf_stats),
-                                self.resident_max_qubits, self.tile_qubits)
+                                self.resident_max_qubits, self.tile_qubits, int(self.profile), 0)
 
 
 @dataclass

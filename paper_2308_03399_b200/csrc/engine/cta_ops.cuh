@@ -120,7 +120,7 @@ __device__ __forceinline__ void cta_pauli(double2* st, unsigned nloc, uint32_t x
 // All 2^k outcome probabilities of qubits q (outcome_probability,
 // statevector.cpp:142-164) into probs[] (shared). red: shared scratch of
 // max(2^k * G/512, 1) doubles. Ends with __syncthreads().
-static __device__ void cta_outcome_probs(const double2* st, unsigned n, const uint8_t* q, unsigned k,
+static __device__ __noinline__ void cta_outcome_probs(const double2* st, unsigned n, const uint8_t* q, unsigned k,
                                   double* probs, double* red) {
   uint8_t sorted[32];
   sort_positions(q, k, sorted);
@@ -150,7 +150,7 @@ static __device__ void cta_outcome_probs(const double2* st, unsigned n, const ui
 
 // <psi|M^dag M|psi> for a 2x2 M (expval_matrix1_scalar, kernels_scalar.cpp:103-126).
 // Result valid in all threads. red: >= max(1, 2^(n-1)/512) doubles + 1.
-static __device__ double cta_expval1(const double2* st, unsigned n, unsigned t, const double2* m, double* red) {
+static __device__ __noinline__ double cta_expval1(const double2* st, unsigned n, unsigned t, const double2* m, double* red) {
   const uint64_t pairs = uint64_t{1} << (n - 1), bit = uint64_t{1} << t;
   const uint64_t nb = pairs <= SUM_BLOCK ? 1 : pairs / SUM_BLOCK;
   const uint64_t len = pairs <= SUM_BLOCK ? pairs : SUM_BLOCK;
@@ -176,7 +176,7 @@ static __device__ double cta_expval1(const double2* st, unsigned n, unsigned t, 
 
 // Generic k=2 expval (expval_generic, statevector.cpp:56-80): per-group sums of
 // |row|^2, then pairwise over all 2^(n-2) groups. red: >= max(1, 2^(n-2)/8) + 1.
-static __device__ double cta_expval2(const double2* st, unsigned n, const uint8_t* q, const double2* m,
+static __device__ __noinline__ double cta_expval2(const double2* st, unsigned n, const uint8_t* q, const double2* m,
                               double* red) {
   uint8_t sorted[2];
   sort_positions(q, 2, sorted);

@@ -2,6 +2,7 @@
 // HBM tile-pass plan (see devprog.hpp).
 #include "devprog.hpp"
 
+#include <algorithm>
 #include <bit>
 #include <stdexcept>
 
@@ -32,6 +33,32 @@ bool is_identity_cls(uint64_t cls, unsigned k) {
     for (unsigned c = 0; c < d; ++c)
       if (entry_class(cls, r * d + c) != (r == c ? E_ONE : E_ZERO)) return false;
   return true;
+}
+
+// Picks the arithmetic template for a gate matrix (see MicroKind). Every
+// template performs exactly the reference's nonzero-term products and sums.
+uint8_t micro_kind(uint64_t cls, unsigned k, uint8_t* src) {
+  *src = 0;
+  if (k == 1) {
+    const uint32_t c0 = entry_class(cls, 0), c1 = entry_class(cls, 1), c2 = entry_class(cls, 2),
+                   c3 = entry_class(cls, 3);
+    if (c0 == E_REAL && c1 == E_GEN && c2 == E_GEN && c3 == E_GEN) return MK_1Q_U;
+    if (c0 == E_REAL && c1 == E_REAL && c2 == E_REAL && c3 == E_REAL) return MK_1Q_REAL;
+    return MK_1Q_GEN;
+  }
+  uint8_t s = 0;
+  for (unsigned r = 0; r < 4; ++r) {
+    int col = -1, nz = 0;
+    for (unsigned c = 0; c < 4; ++c)
+      if (entry_class(cls, r * 4 + c) != E_ZERO) {
+        ++nz;
+        col = static_cast<int>(c);
+      }
+    if (nz != 1) return MK_2Q_GEN;
+    s |= static_cast<uint8_t>(col << (2 * r));
+  }
+  *src = s;
+  return MK_2Q_MONO;
 }
 
 }  // namespace
@@ -98,6 +125,7 @@ HostDevProgram build_device_program(const shotsim::NoisyCircuit& p) {
         o.aux = push_matrix(op.matrix);
         o.cls = classify_matrix(&d.mats[o.aux * 32], op.matrix.num_qubits, false);
         o.skip = is_identity_cls(o.cls, op.matrix.num_qubits);
+        o.mk = micro_kind(o.cls, op.matrix.num_qubits, &o.src);
         break;
       }
       case ProgramOp::Kind::PauliSite: {
@@ -145,13 +173,57 @@ HostDevProgram build_device_program(const shotsim::NoisyCircuit& p) {
   return d;
 }
 
+namespace {
+
+// Splits pass ops [first, ops.size()) into register segments: maximal runs of
+// consecutive ops whose qubits stay inside one 2-qubit set. pos: qubit ->
+// local position. A single-qubit segment is paired with another local qubit.
+void segment_ops(HostDevProgram& d, const std::vector<uint32_t>& ops, const uint8_t* pos, unsigned k) {
+  size_t i = 0;
+  while (i < ops.size()) {
+    uint32_t set = 0;  // local positions
+    size_t j = i;
+    for (; j < ops.size(); ++j) {
+      uint32_t m = 0;
+      for (unsigned b = 0; b < d.ops[ops[j]].nq; ++b) m |= 1u << pos[d.ops[ops[j]].q[b]];
+      if (std::popcount(set | m) > 2) break;
+      set |= m;
+    }
+    Item it{};
+    it.kind = IT_SEGMENT;
+    unsigned la = static_cast<unsigned>(std::countr_zero(set));
+    unsigned lb = std::popcount(set) == 2 ? 31u - static_cast<unsigned>(std::countl_zero(set)) : (la == 0 ? 1u : 0u);
+    if (k < 2) lb = la;  // degenerate 1-qubit state: per-op fallback in the kernel
+    if (la > lb) std::swap(la, lb);
+    it.la = static_cast<uint8_t>(la);
+    it.lb = static_cast<uint8_t>(lb);
+    it.begin = static_cast<uint32_t>(d.pass_ops.size());
+    for (size_t t = i; t < j; ++t) {
+      PassOp po{ops[t], {}};
+      for (unsigned b = 0; b < d.ops[ops[t]].nq; ++b) po.qb[b] = pos[d.ops[ops[t]].q[b]] == la ? 0 : 1;
+      if (k < 2)
+        for (unsigned b = 0; b < d.ops[ops[t]].nq; ++b) po.qb[b] = pos[d.ops[ops[t]].q[b]];
+      d.pass_ops.push_back(po);
+    }
+    it.end = static_cast<uint32_t>(d.pass_ops.size());
+    d.items.push_back(it);
+    i = j;
+  }
+}
+
+bool fused_kind(const DevOp& o) { return o.kind == K_GATE || o.kind == K_PAULI; }
+
+}  // namespace
+
 // Greedy in-order pass formation: consecutive gates / Pauli sites whose union
-// of qubits (plus the always-local low qubits, for 128-byte coalesced tile
-// rows) fits k local qubits share one HBM read+write of the state. Ops are
-// never reordered (gates on disjoint qubits do not commute bitwise in
-// floating point), Kraus / measure / reset sites end a pass.
+// of qubits (plus the always-local low qubits, for coalesced tile rows) fits k
+// local qubits share one HBM read+write of the state. Ops are never reordered
+// (gates on disjoint qubits do not commute bitwise in floating point); Kraus /
+// measure / reset sites end a pass. Inside a pass, ops are grouped into
+// register segments (segment_ops).
 void plan_passes(HostDevProgram& d, unsigned tile_k) {
   d.passes.clear();
+  d.items.clear();
   d.pass_ops.clear();
   d.steps.clear();
   const unsigned n = d.n;
@@ -173,7 +245,6 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
     uint32_t mask = cur;
     for (unsigned q = 0; q < n && static_cast<unsigned>(std::popcount(mask)) < k; ++q) mask |= 1u << q;
     PassDesc pd{};
-    pd.begin = static_cast<uint32_t>(d.pass_ops.size());
     pd.lmask = mask;
     pd.k = static_cast<uint8_t>(k);
     pd.first = need_init;
@@ -184,12 +255,9 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
         pd.lq[j] = static_cast<uint8_t>(q);
         pos[q] = static_cast<uint8_t>(j++);
       }
-    for (uint32_t oi : cur_ops) {
-      PassOp po{oi, {}};
-      for (unsigned b = 0; b < d.ops[oi].nq; ++b) po.lq[b] = pos[d.ops[oi].q[b]];
-      d.pass_ops.push_back(po);
-    }
-    pd.end = static_cast<uint32_t>(d.pass_ops.size());
+    pd.item_begin = static_cast<uint32_t>(d.items.size());
+    segment_ops(d, cur_ops, pos, k);
+    pd.item_end = static_cast<uint32_t>(d.items.size());
     d.steps.push_back({S_PASS, static_cast<uint32_t>(d.passes.size())});
     d.passes.push_back(pd);
     cur = low;
@@ -199,7 +267,7 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
   for (uint32_t i = 0; i < d.end; ++i) {
     const DevOp& o = d.ops[i];
     if (o.kind == K_BARRIER || (o.kind == K_GATE && o.skip)) continue;
-    if (o.kind == K_GATE || o.kind == K_PAULI) {
+    if (fused_kind(o)) {
       uint32_t qm = 0;
       for (unsigned b = 0; b < o.nq; ++b) qm |= 1u << o.q[b];
       if (static_cast<unsigned>(std::popcount(cur | qm)) > k) close(false);
@@ -212,6 +280,40 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
   }
   close(true);
   if (d.eligible) d.steps.push_back({S_SAMPLE, 0});
+}
+
+void plan_resident(HostDevProgram& d) {
+  d.passes.clear();
+  d.items.clear();
+  d.pass_ops.clear();
+  d.steps.clear();
+  const unsigned n = d.n;
+  d.tile_k = n;
+  PassDesc pd{};
+  pd.lmask = n >= 32 ? ~0u : (1u << n) - 1;
+  pd.k = static_cast<uint8_t>(n);
+  pd.first = 1;
+  uint8_t pos[32] = {};
+  for (unsigned q = 0; q < n; ++q) pos[q] = pd.lq[q] = static_cast<uint8_t>(q);
+  pd.item_begin = 0;
+  std::vector<uint32_t> run;
+  for (uint32_t i = 0; i < d.end; ++i) {
+    const DevOp& o = d.ops[i];
+    if (o.kind == K_BARRIER || (o.kind == K_GATE && o.skip)) continue;
+    if (fused_kind(o)) {
+      run.push_back(i);
+      continue;
+    }
+    segment_ops(d, run, pos, n);
+    run.clear();
+    Item sp{};
+    sp.kind = IT_SPECIAL;
+    sp.begin = i;
+    d.items.push_back(sp);
+  }
+  segment_ops(d, run, pos, n);
+  pd.item_end = static_cast<uint32_t>(d.items.size());
+  d.passes.push_back(pd);
 }
 
 }  // namespace ssb

@@ -24,7 +24,9 @@ struct alignas(16) DevOp {
   uint32_t aux;        // GATE: matrix slot; PAULI: first term; KRAUS: channel
   uint32_t count;      // PAULI: term count; KRAUS: matrix count
   uint32_t site;       // PAULI: ordinal among Pauli sites (decision table column)
-  uint32_t pad;
+  uint8_t mk;          // GATE: micro-kind (MicroKind), chosen at plan time
+  uint8_t src;         // MK_2Q_MONO: source column of each row (2 bits per row)
+  uint8_t pad[2];
   uint64_t cls;        // GATE: entry classes (exact.cuh EntryClass, 3 bits each)
   uint64_t cond_mask;
   uint64_t cond_value;
@@ -43,11 +45,21 @@ struct DevChannel {
   uint32_t arity, nmat, mat_begin, pad;
 };
 
-// One fused HBM tile pass: the ops [begin,end) of pass_ops, all acting inside
-// the local qubit set `lmask` (|lmask| = k); `first` synthesises |0...0>
-// instead of loading the tile.
+// Gate micro-kinds (exact.cuh): which arithmetic template applies the matrix.
+enum MicroKind : uint8_t {
+  MK_1Q_U = 0,     // classes (REAL, GEN, GEN, GEN): the U gate
+  MK_1Q_REAL = 1,  // all four entries real or zero-free real (H)
+  MK_1Q_GEN = 2,   // anything else: per-entry runtime classes
+  MK_2Q_MONO = 3,  // one nonzero per row (CX, SWAP, CP, CZ...): moves + few products
+  MK_2Q_GEN = 4,   // dense 4x4: per-entry runtime classes
+};
+
+// One fused HBM tile pass over the local qubit set `lmask` (|lmask| = k):
+// items [item_begin, item_end); `first` synthesises |0...0> instead of loading
+// the tile. The resident executor uses one pass with k = n whose items also
+// include special ops (Kraus / measure / reset).
 struct PassDesc {
-  uint32_t begin, end;
+  uint32_t item_begin, item_end;
   uint32_t lmask;
   uint8_t k;
   uint8_t first;
@@ -55,9 +67,20 @@ struct PassDesc {
   uint8_t lq[32];      // local position j -> qubit
 };
 
+// Item: a register segment — consecutive ops [begin,end) of pass_ops acting
+// inside the 2-qubit set {la, lb} (local positions), applied per amplitude
+// quad in registers — or a special op (resident executor only).
+enum ItemKind : uint8_t { IT_SEGMENT = 0, IT_SPECIAL = 1 };
+struct Item {
+  uint8_t kind;
+  uint8_t la, lb;      // local positions, la < lb
+  uint8_t pad;
+  uint32_t begin, end; // segment: pass_ops range; special: begin = op index
+};
+
 struct PassOp {
   uint32_t op;         // index into ops
-  uint8_t lq[4];       // local positions of the op's qubits
+  uint8_t qb[4];       // quad bit (0 -> la, 1 -> lb) of each op qubit
 };
 
 enum StepKind : uint8_t { S_PASS = 0, S_SPECIAL = 1, S_SAMPLE = 2 };
@@ -83,6 +106,7 @@ struct HostDevProgram {
   bool sample_identity = false;          // sample_qubits == [0..n)
   // Streamed-mode plan (n > resident limit).
   std::vector<PassDesc> passes;
+  std::vector<Item> items;
   std::vector<PassOp> pass_ops;
   std::vector<Step> steps;
   unsigned tile_k = 0;
@@ -90,6 +114,9 @@ struct HostDevProgram {
 
 uint64_t classify_matrix(const double* m, unsigned k, bool scaled);
 HostDevProgram build_device_program(const shotsim::NoisyCircuit& p);
+// Streamed plan: HBM tile passes (gates / Pauli sites) + special steps.
 void plan_passes(HostDevProgram& d, unsigned tile_k);
+// Resident plan: one pass (k = n) whose items cover the whole program.
+void plan_resident(HostDevProgram& d);
 
 }  // namespace ssb

@@ -88,13 +88,15 @@ T* upload(DevProgram& d, const std::vector<T>& v) {
   return static_cast<T*>(p);
 }
 
+// tile_k == 0 selects the resident plan (whole program in one pass, k = n).
 DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile_k) {
   const auto key = std::make_pair(prog->uid, tile_k);
   auto it = E->programs.find(key);
   if (it != E->programs.end()) return *it->second;
   auto d = std::make_unique<DevProgram>();
   d->host = prog->dev;
-  plan_passes(d->host, tile_k);
+  if (tile_k == 0) plan_resident(d->host);
+  else plan_passes(d->host, tile_k);
   const HostDevProgram& h = d->host;
   ProgView& v = d->view;
   v.ops = upload(*d, h.ops);
@@ -106,6 +108,7 @@ DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile
   v.write_clbit = upload(*d, h.write_clbit);
   v.write_pos = upload(*d, h.write_pos);
   v.passes = upload(*d, h.passes);
+  v.items = upload(*d, h.items);
   v.pass_ops = upload(*d, h.pass_ops);
   v.n = h.n;
   v.end = h.end;
@@ -119,6 +122,8 @@ DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile
     if (h.ops[i].kind == K_PAULI) sites.push_back(i);
   d->num_pauli = static_cast<uint32_t>(sites.size());
   d->pauli_site_ops = upload(*d, sites);
+  v.pauli_site_ops = d->pauli_site_ops;
+  v.num_pauli = d->num_pauli;
   auto& ref = *d;
   E->programs.emplace(key, std::move(d));
   return ref;
@@ -324,10 +329,50 @@ void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c) {
 
 size_t resident_smem(const HostDevProgram& h) {
   const uint64_t A = uint64_t{1} << h.n;
-  uint64_t probs = 16;
-  if (h.eligible && h.sample_qubits.size() < h.n) probs = std::max<uint64_t>(probs, uint64_t{1} << h.sample_qubits.size());
-  return A * sizeof(double2) + (resident_red_doubles() + probs) * sizeof(double);
+  const uint64_t probs =
+      (h.eligible && h.sample_qubits.size() < h.n) ? (uint64_t{1} << h.sample_qubits.size()) + 16 : 16;
+  uint32_t sites = 0;
+  for (const DevOp& o : h.ops) sites += o.kind == K_PAULI;
+  return A * sizeof(double2) + (resident_red_doubles() + probs) * sizeof(double) + sites;
 }
+
+// Optional per-kernel-class CUDA-event timing (ssb_run_options::profile):
+// 0 = fused passes (tile / resident), 1 = special ops, 2 = terminal sampling.
+struct KernelTimer {
+  bool on = false;
+  cudaStream_t stream = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[3];
+  void begin(int c) {
+    if (!on) return;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, stream));
+    ev[c].emplace_back(a, b);
+  }
+  void end(int c) {
+    if (on) CK(cudaEventRecord(ev[c].back().second, stream));
+  }
+  void collect(ssb_stats* st) {
+    if (!on) return;
+    CK(cudaStreamSynchronize(stream));
+    double secs[3] = {0, 0, 0};
+    for (int c = 0; c < 3; ++c)
+      for (auto& [a, b] : ev[c]) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        secs[c] += ms * 1e-3;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+    if (st) {
+      st->pass_seconds = secs[0];
+      st->pass_launches = ev[0].size();
+      st->special_seconds = secs[1];
+      st->sample_seconds = secs[2];
+    }
+  }
+};
 
 struct RunConfig {
   unsigned resident_max = kResidentMaxDefault;
@@ -349,15 +394,20 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
   const unsigned n = prog->dev.n;
   const uint64_t launches0 = E->launches;
   const size_t rsmem = resident_smem(prog->dev);
+  KernelTimer timer;
+  timer.on = opts && opts->profile;
+  timer.stream = E->stream;
   if (n <= rc.resident_max && rsmem <= E->smem_optin) {
-    DevProgram& dp = device_program(E, prog, rc.tile_k);
+    DevProgram& dp = device_program(E, prog, 0);
     CK(cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, resident_kernel, NT, rsmem));
     const uint64_t grid = std::min<uint64_t>(count, static_cast<uint64_t>(std::max(1, per_sm)) * E->num_sms);
+    timer.begin(0);
     resident_kernel<<<static_cast<unsigned>(grid), NT, rsmem, E->stream>>>(dp.view, seed, nullptr, shot_begin, count,
                                                                            values_dev, E->err);
     launched(E);
+    timer.end(0);
     if (stats) {
       stats->peak_states = std::min<uint64_t>(count, grid);
       stats->passes = 1;
@@ -368,7 +418,11 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
     const HostDevProgram& h = dp.host;
     const uint64_t seg = (uint64_t{1} << n) * sizeof(double2);
     const uint64_t limit = mem_limit(opts);
-    uint64_t wave = opts && opts->max_batch_size ? opts->max_batch_size : std::max<uint64_t>(1, limit / seg);
+    // Default wave: as many shots as the memory limit allows, capped at 16 GiB
+    // of state (>> L2, enough CTAs to fill the GPU many times over).
+    uint64_t wave = opts && opts->max_batch_size
+                        ? opts->max_batch_size
+                        : std::max<uint64_t>(1, std::min<uint64_t>(limit, uint64_t{16} << 30) / seg);
     const uint64_t largest = std::min(wave, count);
     if (largest * seg > limit)
       throw shotsim::CapacityError("batch of " + std::to_string(largest) + " shots at " + std::to_string(n) +
@@ -394,14 +448,20 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       fused = 0;
       for (const Step& st : h.steps) {
         if (st.kind == S_PASS) {
+          timer.begin(0);
           tile_pass_kernel<<<static_cast<unsigned>(S * tiles), NT, tsmem, E->stream>>>(dp.view, st.index, state, S,
                                                                                       c.cregs, psel, dp.num_pauli);
           launched(E);
+          timer.end(0);
           ++fused;
         } else if (st.kind == S_SPECIAL) {
+          timer.begin(1);
           apply_op(E, dp, st.index, c, false);
+          timer.end(1);
         } else {
+          timer.begin(2);
           sample_terminal(E, dp, c);
+          timer.end(2);
         }
       }
     }
@@ -412,6 +472,7 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
     }
   }
   if (stats) stats->dispatch_count = E->launches - launches0;
+  timer.collect(stats);
 }
 
 struct DeviceGuard {

@@ -15,7 +15,7 @@
 //                      streamed executor and for the operator-level C ABI.
 #pragma once
 
-#include "cta_ops.cuh"
+#include "segment.cuh"
 
 namespace ssb {
 
@@ -39,7 +39,10 @@ struct ProgView {
   const uint8_t* write_clbit;
   const uint8_t* write_pos;
   const PassDesc* passes;
+  const Item* items;
   const PassOp* pass_ops;
+  const uint32_t* pauli_site_ops;  // site ordinal -> op index
+  uint32_t num_pauli;
   uint32_t n, end, nsample, nwrites;
   uint64_t num_events;
   uint32_t eligible, sample_identity;
@@ -90,52 +93,47 @@ __device__ __forceinline__ bool scan_full(Amp amp, uint64_t count, bool identity
   return last != count;
 }
 
-// Shared-memory layout of resident_kernel: state | red (512) | probs (2^k).
+// Shared-memory layout of resident_kernel: state | red (513) | probs | Pauli
+// decisions (u8 per site).
 __host__ __device__ constexpr uint64_t resident_red_doubles() { return 513; }
+__host__ __device__ inline uint64_t resident_probs_doubles(const ProgView& P) {
+  return (P.eligible && P.nsample < P.n) ? (uint64_t{1} << P.nsample) + 16 : 16;
+}
 
 // ---------------------------------------------------------------------------
-static __global__ void __launch_bounds__(NT) resident_kernel(ProgView P, uint64_t seed, const uint64_t* ids,
-                                                      uint64_t shot_begin, uint64_t S, uint64_t* values,
-                                                      int* err) {
+static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint64_t seed, const uint64_t* ids,
+                                                         uint64_t shot_begin, uint64_t S, uint64_t* values, int* err) {
   extern __shared__ double2 smem[];
   const unsigned n = P.n;
   const uint64_t A = uint64_t{1} << n;
   double2* st = smem;
   double* red = reinterpret_cast<double*>(st + A);
   double* probs = red + resident_red_doubles();
+  uint8_t* psel = reinterpret_cast<uint8_t*>(probs + resident_probs_doubles(P));
   __shared__ uint64_t bc_out;
   __shared__ double bc_p;
+  const PassDesc& pd = P.passes[0];
 
   for (uint64_t s = blockIdx.x; s < S; s += gridDim.x) {
     const uint64_t shot = shot_of(ids, shot_begin, s);
     for (uint64_t j = threadIdx.x; j < A; j += NT) st[j] = make_double2(j == 0 ? 1.0 : 0.0, 0.0);
+    // This shot's Pauli-site decisions (keyed draws, rng.cpp:36-46), once.
+    for (uint32_t site = threadIdx.x; site < P.num_pauli; site += NT) {
+      const DevOp& op = P.ops[P.pauli_site_ops[site]];
+      psel[site] = static_cast<uint8_t>(pick_term(P.terms + op.aux, op.count, keyed_uniform(seed, shot, op.event)));
+    }
     uint64_t creg = 0;
     __syncthreads();
-    for (uint32_t i = 0; i < P.end; ++i) {
-      const DevOp& op = P.ops[i];
+    for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
+      const Item it = P.items[it_i];
+      if (it.kind == IT_SEGMENT) {
+        run_segment(st, n, it, P.pass_ops, P.ops, P.mats, P.terms, creg, psel);
+        continue;
+      }
+      const DevOp& op = P.ops[it.begin];
       const uint8_t kind = op.kind;
-      if (kind == K_BARRIER) continue;
       if (op.has_cond && (creg & op.cond_mask) != op.cond_value) continue;
-      if (kind == K_GATE) {
-        if (op.skip) continue;
-        if (op.nq == 1) {
-          double2 m[4];
-          load_matrix<2>(P.mats + 16 * op.aux, m);
-          cta_apply1(st, n, op.q[0], m, op.cls);
-        } else {
-          double2 m[16];
-          load_matrix<4>(P.mats + 16 * op.aux, m);
-          cta_apply2(st, n, op.q[0], op.q[1], m, op.cls);
-        }
-        __syncthreads();
-      } else if (kind == K_PAULI) {
-        const DevTerm* terms = P.terms + op.aux;
-        const int t = pick_term(terms, op.count, keyed_uniform(seed, shot, op.event));
-        if (!terms[t].identity) {
-          cta_pauli(st, n, terms[t].x, terms[t].z, terms[t].num_y);
-          __syncthreads();
-        }
-      } else if (kind == K_KRAUS) {
+      if (kind == K_KRAUS) {
         // apply_kraus_single (exec_naive.cpp:29-42): sequential scan, early exit.
         const DevChannel ch = P.channels[op.aux];
         const double u = keyed_uniform(seed, shot, op.event);
@@ -237,7 +235,7 @@ __device__ __forceinline__ uint64_t pdep_positions(uint64_t v, const uint8_t* po
   return out;
 }
 
-static __global__ void __launch_bounds__(NT) tile_pass_kernel(ProgView P, uint32_t pass_index, double2* state,
+static __global__ void __launch_bounds__(NT, 2) tile_pass_kernel(ProgView P, uint32_t pass_index, double2* state,
                                                        uint64_t S, const uint64_t* cregs,
                                                        const uint8_t* pauli_sel, uint32_t num_pauli) {
   extern __shared__ double2 tile[];
@@ -270,34 +268,8 @@ static __global__ void __launch_bounds__(NT) tile_pass_kernel(ProgView P, uint32
   __syncthreads();
   const uint64_t creg = cregs ? cregs[s] : 0;
   const uint8_t* sel = pauli_sel + s * num_pauli;
-  for (uint32_t i = pd.begin; i < pd.end; ++i) {
-    const PassOp po = P.pass_ops[i];
-    const DevOp& op = P.ops[po.op];
-    if (op.has_cond && (creg & op.cond_mask) != op.cond_value) continue;
-    if (op.kind == K_GATE) {
-      if (op.nq == 1) {
-        double2 m[4];
-        load_matrix<2>(P.mats + 16 * op.aux, m);
-        cta_apply1(tile, k, po.lq[0], m, op.cls);
-      } else {
-        double2 m[16];
-        load_matrix<4>(P.mats + 16 * op.aux, m);
-        cta_apply2(tile, k, po.lq[0], po.lq[1], m, op.cls);
-      }
-      __syncthreads();
-    } else {  // K_PAULI with a precomputed per-shot term
-      const uint8_t term = sel[op.site];
-      const DevTerm& tm = P.terms[op.aux + term];
-      if (tm.identity) continue;
-      uint32_t x = 0, z = 0;
-      for (unsigned b = 0; b < op.nq; ++b) {
-        x |= ((tm.x >> op.q[b]) & 1u) << po.lq[b];
-        z |= ((tm.z >> op.q[b]) & 1u) << po.lq[b];
-      }
-      cta_pauli(tile, k, x, z, tm.num_y);
-      __syncthreads();
-    }
-  }
+  for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i)
+    run_segment(tile, k, P.items[it_i], P.pass_ops, P.ops, P.mats, P.terms, creg, sel);
   for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
     seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)] = tile[l];
 }

@@ -1,0 +1,218 @@
+// Register segments: a run of consecutive gates / Pauli sites whose qubits
+// stay inside one 2-qubit set {la, lb} is applied quad by quad in registers —
+// each thread loads the 4 amplitudes (base, +2^la, +2^lb, +both) of a few
+// quads from the shared-memory state, applies every op of the segment, and
+// stores them back: one shared-memory round trip and one barrier per segment
+// instead of per op. Any op on qubits inside {la, lb} maps each quad onto
+// itself, and each op is still applied with the reference's per-amplitude
+// arithmetic in program order, so the result is bit-identical to applying the
+// ops one by one over the whole state (kernels_scalar.cpp:24-81).
+#pragma once
+
+#include "cta_ops.cuh"
+
+namespace ssb {
+
+#ifndef SSB_QPT
+#define SSB_QPT 2
+#endif
+constexpr int QPT = SSB_QPT;  // quads per thread per round
+
+// Quad element e (bit0 <-> la, bit1 <-> lb). 1q gate on quad bit B mixes
+// elements (e, e | 1<<B) for e with bit B clear.
+template <int B, int MK>
+__device__ __forceinline__ void quad_apply1(double2 (&v)[QPT][4], const double2* m, uint64_t cls, int nq) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i0 = B == 0 ? 2 * h : h, i1 = i0 + (1 << B);
+#pragma unroll
+    for (int q = 0; q < QPT; ++q) {
+      if (q >= nq) break;
+      const double2 a0 = v[q][i0], a1 = v[q][i1];
+      if constexpr (MK == MK_1Q_U) {
+        // m0 real: m0*a0 = (m0r*a0r, m0r*a0i); m1..m3 general complex.
+        const double2 t0 = make_double2(__dmul_rn(m[0].x, a0.x), __dmul_rn(m[0].x, a0.y));
+        v[q][i0] = c_add(t0, c_mul(m[1], a1));
+        v[q][i1] = c_add(c_mul(m[2], a0), c_mul(m[3], a1));
+      } else if constexpr (MK == MK_1Q_REAL) {
+        v[q][i0] = c_add(make_double2(__dmul_rn(m[0].x, a0.x), __dmul_rn(m[0].x, a0.y)),
+                         make_double2(__dmul_rn(m[1].x, a1.x), __dmul_rn(m[1].x, a1.y)));
+        v[q][i1] = c_add(make_double2(__dmul_rn(m[2].x, a0.x), __dmul_rn(m[2].x, a0.y)),
+                         make_double2(__dmul_rn(m[3].x, a1.x), __dmul_rn(m[3].x, a1.y)));
+      } else {
+        const double2 in[2] = {a0, a1};
+        v[q][i0] = row_apply<2>(m, cls, 0, in);
+        v[q][i1] = row_apply<2>(m, cls, 1, in);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double2 pick4(const double2 (&a)[4], uint32_t i) {
+  double2 r = a[0];
+  r = i == 1 ? a[1] : r;
+  r = i == 2 ? a[2] : r;
+  r = i == 3 ? a[3] : r;
+  return r;
+}
+
+// 2q gate; `swapped`: op qubits (q0, q1) = (lb, la), i.e. matrix index bit0
+// is quad bit 1. Matrix row r / column c use index order (base, +d0, +d1,
+// +d0+d1). MONO: mr[r] = the single nonzero entry of row r (column src_r);
+// GEN: `m` points at the 16 entries in global memory (rare path, loaded on use
+// to keep the register budget of the common paths).
+template <int MK>
+__device__ __forceinline__ void quad_apply2(double2 (&v)[QPT][4], const double2* mr, const double2* m, uint64_t cls,
+                                            uint8_t src, bool swapped, int nq) {
+  auto el = [swapped](int r) { return swapped ? ((r & 1) << 1) | (r >> 1) : r; };
+#pragma unroll
+  for (int q = 0; q < QPT; ++q) {
+    if (q >= nq) break;
+    double2 in[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) in[r] = v[q][el(r)];
+    double2 out[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if constexpr (MK == MK_2Q_MONO) {
+        const uint32_t c = (src >> (2 * r)) & 3u;
+        const uint32_t k = entry_class(cls, r * 4 + static_cast<int>(c));
+        const double2 x = pick4(in, c);
+        out[r] = k == E_ONE ? x : c_term(mr[r], k, x);
+      } else {
+        out[r] = row_apply<4>(m, cls, r, in);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) v[q][el(r)] = out[r];
+  }
+}
+
+// Pauli on the quad: new[e] = (-i)^num_y * (-1)^popc(e & zq) * old[e ^ xq]
+// (destination-sign form, kernels_scalar.cpp:58-81).
+__device__ __forceinline__ void quad_pauli(double2 (&v)[QPT][4], uint32_t xq, uint32_t zq, uint32_t num_y, int nq) {
+#pragma unroll
+  for (int q = 0; q < QPT; ++q) {
+    if (q >= nq) break;
+    double2 old[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) old[e] = v[q][e];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      double2 t = pauli_phase(num_y, pick4(old, static_cast<uint32_t>(e) ^ xq));
+      if (__popc(static_cast<uint32_t>(e) & zq) & 1) t = c_neg(t);
+      v[q][e] = t;
+    }
+  }
+}
+
+// Per-op fallback for a 1-qubit state (no quads).
+static __device__ void run_ops_per_op(double2* st, unsigned k, uint32_t begin, uint32_t end, const PassOp* pops,
+                               const DevOp* ops, const double2* mats, const DevTerm* terms, uint64_t creg,
+                               const uint8_t* sel) {
+  for (uint32_t i = begin; i < end; ++i) {
+    const PassOp po = pops[i];
+    const DevOp& op = ops[po.op];
+    if (op.has_cond && (creg & op.cond_mask) != op.cond_value) continue;
+    if (op.kind == K_GATE) {
+      double2 m[4];
+      load_matrix<2>(mats + 16 * op.aux, m);
+      cta_apply1(st, k, po.qb[0], m, op.cls);
+    } else {
+      const DevTerm& tm = terms[op.aux + sel[op.site]];
+      if (tm.identity) continue;
+      cta_pauli(st, k, (tm.x >> op.q[0]) & 1u, (tm.z >> op.q[0]) & 1u, tm.num_y);
+    }
+    __syncthreads();
+  }
+}
+
+// Applies item `it` (a register segment) to the shared-memory state `st` of k
+// local qubits. sel: per-site Pauli term choice of this shot. Ends with a
+// barrier.
+static __device__ void run_segment(double2* st, unsigned k, const Item& it, const PassOp* pops, const DevOp* ops,
+                            const double2* mats, const DevTerm* terms, uint64_t creg, const uint8_t* sel) {
+  if (k < 2) {
+    run_ops_per_op(st, k, it.begin, it.end, pops, ops, mats, terms, creg, sel);
+    return;
+  }
+  const unsigned la = it.la, lb = it.lb;
+  const uint64_t dla = uint64_t{1} << la, dlb = uint64_t{1} << lb;
+  const uint64_t nquads = uint64_t{1} << (k - 2);
+  const uint64_t per_round = uint64_t{NT} * QPT;
+  for (uint64_t r0 = 0; r0 < nquads; r0 += per_round) {
+    double2 v[QPT][4];
+    uint64_t base[QPT];
+    int nq = 0;
+#pragma unroll
+    for (int q = 0; q < QPT; ++q) {
+      const uint64_t p = r0 + threadIdx.x + uint64_t{NT} * q;
+      if (p < nquads) {
+        nq = q + 1;
+        base[q] = insert_zero(insert_zero(p, la), lb);
+        v[q][0] = st[base[q]];
+        v[q][1] = st[base[q] | dla];
+        v[q][2] = st[base[q] | dlb];
+        v[q][3] = st[base[q] | dla | dlb];
+      }
+    }
+    for (uint32_t i = it.begin; i < it.end; ++i) {
+      const PassOp po = pops[i];
+      const DevOp& op = ops[po.op];
+      if (op.has_cond && (creg & op.cond_mask) != op.cond_value) continue;
+      if (op.kind == K_GATE) {
+        if (op.nq == 1) {
+          double2 m[4];
+          if (op.mk != MK_1Q_GEN) load_matrix<2>(mats + 16 * op.aux, m);
+          const bool b1 = po.qb[0] != 0;
+          switch (op.mk) {
+            case MK_1Q_U:
+              if (b1) quad_apply1<1, MK_1Q_U>(v, m, op.cls, nq);
+              else quad_apply1<0, MK_1Q_U>(v, m, op.cls, nq);
+              break;
+            case MK_1Q_REAL:
+              if (b1) quad_apply1<1, MK_1Q_REAL>(v, m, op.cls, nq);
+              else quad_apply1<0, MK_1Q_REAL>(v, m, op.cls, nq);
+              break;
+            default:
+              if (b1) quad_apply1<1, MK_1Q_GEN>(v, mats + 16 * op.aux, op.cls, nq);
+              else quad_apply1<0, MK_1Q_GEN>(v, mats + 16 * op.aux, op.cls, nq);
+              break;
+          }
+        } else {
+          const double2* mg = mats + 16 * op.aux;
+          const bool swapped = po.qb[0] != 0;
+          if (op.mk == MK_2Q_MONO) {
+            double2 mr[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) mr[r] = mg[r * 4 + ((op.src >> (2 * r)) & 3u)];
+            quad_apply2<MK_2Q_MONO>(v, mr, mg, op.cls, op.src, swapped, nq);
+          } else {
+            quad_apply2<MK_2Q_GEN>(v, nullptr, mg, op.cls, op.src, swapped, nq);
+          }
+        }
+      } else {  // Pauli site with this shot's term
+        const DevTerm& tm = terms[op.aux + sel[op.site]];
+        if (tm.identity) continue;
+        uint32_t xq = 0, zq = 0;
+        for (unsigned b = 0; b < op.nq; ++b) {
+          xq |= ((tm.x >> op.q[b]) & 1u) << po.qb[b];
+          zq |= ((tm.z >> op.q[b]) & 1u) << po.qb[b];
+        }
+        quad_pauli(v, xq, zq, tm.num_y, nq);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < QPT; ++q) {
+      if (q < nq) {
+        st[base[q]] = v[q][0];
+        st[base[q] | dla] = v[q][1];
+        st[base[q] | dlb] = v[q][2];
+        st[base[q] | dla | dlb] = v[q][3];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace ssb
