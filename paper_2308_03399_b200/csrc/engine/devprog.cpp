@@ -175,6 +175,14 @@ HostDevProgram build_device_program(const shotsim::NoisyCircuit& p) {
 
 namespace {
 
+// Shared-memory budget of one pass's staged micro-op stream: 2 x 16 B per op
+// (uop + compacted copy) + its matrix entries (2q dense: 16 x 16 B, else 4).
+constexpr size_t kMaxPassStageBytes = 28 * 1024;
+size_t stage_bytes(const DevOp& o) {
+  if (o.kind == K_PAULI) return 32;
+  return 32 + 16 * ((o.nq == 2 && o.mk != MK_2Q_MONO) ? 16 : 4);
+}
+
 // Splits pass ops [first, ops.size()) into register segments: maximal runs of
 // consecutive ops whose qubits stay inside one 2-qubit set. pos: qubit ->
 // local position. A single-qubit segment is paired with another local qubit.
@@ -213,6 +221,58 @@ void segment_ops(HostDevProgram& d, const std::vector<uint32_t>& ops, const uint
 
 bool fused_kind(const DevOp& o) { return o.kind == K_GATE || o.kind == K_PAULI; }
 
+// Lowers the pass ops [po_begin, ...) of pass `pd` to micro-ops + a compact
+// matrix table; items are re-based to uop indices relative to the pass.
+void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
+  pd.uop_begin = static_cast<uint32_t>(d.uops.size());
+  pd.mat_begin = static_cast<uint32_t>(d.uop_mats.size() / 2);
+  uint32_t mat = 0;
+  auto push = [&](const double* e) {
+    d.uop_mats.push_back(e[0]);
+    d.uop_mats.push_back(e[1]);
+    ++mat;
+  };
+  for (uint32_t i = po_begin; i < d.pass_ops.size(); ++i) {
+    const PassOp& po = d.pass_ops[i];
+    const DevOp& o = d.ops[po.op];
+    Uop u{};
+    u.ref = po.op;
+    u.flags = o.has_cond ? 1 : 0;
+    u.mat = static_cast<uint16_t>(mat);
+    const double* m = &d.mats[static_cast<size_t>(o.aux) * 32];
+    if (o.kind == K_PAULI) {
+      u.code = UC_PAULI;
+      u.qb = static_cast<uint8_t>((po.qb[0] & 1) | (o.nq > 1 ? (po.qb[1] & 1) << 1 : 0));
+    } else if (o.nq == 1) {
+      u.code = o.mk == MK_1Q_U ? UC_U : o.mk == MK_1Q_REAL ? UC_REAL : UC_GEN1;
+      u.qb = po.qb[0];
+      for (int e = 0; e < 4; ++e) push(m + 2 * e);
+    } else {
+      u.qb = po.qb[0];  // 1: op qubit0 is lb, i.e. swapped
+      if (o.mk == MK_2Q_MONO) {
+        u.code = UC_MONO;
+        u.src = o.src;
+        for (int r = 0; r < 4; ++r) {
+          const int c = (o.src >> (2 * r)) & 3;
+          push(m + 2 * (r * 4 + c));
+          u.mcls |= static_cast<uint16_t>(entry_class(o.cls, r * 4 + c) << (3 * r));
+        }
+      } else {
+        u.code = UC_GEN2;
+        for (int e = 0; e < 16; ++e) push(m + 2 * e);
+      }
+    }
+    if (mat > 0xFFFF) throw std::length_error("pass matrix table too large");
+    d.uops.push_back(u);
+  }
+  pd.uop_end = static_cast<uint32_t>(d.uops.size());
+  pd.mat_count = mat;
+  for (uint32_t it = pd.item_begin; it < pd.item_end; ++it) {
+    d.items[it].begin -= po_begin;
+    d.items[it].end -= po_begin;
+  }
+}
+
 }  // namespace
 
 // Greedy in-order pass formation: consecutive gates / Pauli sites whose union
@@ -225,6 +285,8 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
   d.passes.clear();
   d.items.clear();
   d.pass_ops.clear();
+  d.uops.clear();
+  d.uop_mats.clear();
   d.steps.clear();
   const unsigned n = d.n;
   const unsigned k = std::min(tile_k, n);
@@ -236,8 +298,10 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
   uint32_t cur = low;
   std::vector<uint32_t> cur_ops;
   bool need_init = true;
+  size_t staged = 0;
 
   auto close = [&](bool force) {
+    staged = 0;
     if (cur_ops.empty() && !(force && need_init)) {
       cur = low;
       return;
@@ -256,8 +320,10 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
         pos[q] = static_cast<uint8_t>(j++);
       }
     pd.item_begin = static_cast<uint32_t>(d.items.size());
+    const uint32_t po_begin = static_cast<uint32_t>(d.pass_ops.size());
     segment_ops(d, cur_ops, pos, k);
     pd.item_end = static_cast<uint32_t>(d.items.size());
+    build_uops(d, pd, po_begin);
     d.steps.push_back({S_PASS, static_cast<uint32_t>(d.passes.size())});
     d.passes.push_back(pd);
     cur = low;
@@ -270,9 +336,13 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
     if (fused_kind(o)) {
       uint32_t qm = 0;
       for (unsigned b = 0; b < o.nq; ++b) qm |= 1u << o.q[b];
-      if (static_cast<unsigned>(std::popcount(cur | qm)) > k) close(false);
+      if (static_cast<unsigned>(std::popcount(cur | qm)) > k || staged + stage_bytes(o) > kMaxPassStageBytes) {
+        close(false);
+        staged = 0;
+      }
       cur |= qm;
       cur_ops.push_back(i);
+      staged += stage_bytes(o);
     } else {
       close(true);
       d.steps.push_back({S_SPECIAL, i});

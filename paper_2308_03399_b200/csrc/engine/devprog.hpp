@@ -65,7 +65,37 @@ struct PassDesc {
   uint8_t first;
   uint8_t pad[2];
   uint8_t lq[32];      // local position j -> qubit
+  // Streamed passes: micro-op stream [uop_begin, uop_end) (items index it
+  // relative to uop_begin) and its matrix table [mat_begin, mat_begin+mat_count)
+  // (double2 units), staged into shared memory by the tile kernel.
+  uint32_t uop_begin, uop_end;
+  uint32_t mat_begin, mat_count;
 };
+
+// Micro-op codes of a streamed pass (one per gate / Pauli site).
+enum UopCode : uint8_t {
+  UC_U = 0,        // 1q U pattern          (qb: quad bit)
+  UC_REAL = 1,     // 1q all-real           (qb: quad bit)
+  UC_GEN1 = 2,     // 1q runtime classes    (qb: quad bit; cls via ref)
+  UC_MONO = 3,     // 2q monomial           (qb: swapped; src; mcls)
+  UC_GEN2 = 4,     // 2q runtime classes    (qb: swapped; cls via ref)
+  UC_PAULI = 5,    // Pauli site            (qb: quad bits of op qubits, bit b)
+};
+
+// 16-byte micro-op. After per-shot compaction (identity Pauli draws and
+// failed conditions removed) `pauli` holds xq | zq << 2 | (num_y & 3) << 4.
+struct Uop {
+  uint8_t code;
+  uint8_t qb;
+  uint8_t src;
+  uint8_t flags;       // bit0: conditional
+  uint16_t mat;        // offset into the pass matrix table (double2 units)
+  uint16_t mcls;       // UC_MONO: class of row r's nonzero entry, 3 bits per row
+  uint32_t ref;        // program op index
+  uint8_t pauli;
+  uint8_t pad[3];
+};
+static_assert(sizeof(Uop) == 16, "Uop layout");
 
 // Item: a register segment — consecutive ops [begin,end) of pass_ops acting
 // inside the 2-qubit set {la, lb} (local positions), applied per amplitude
@@ -108,6 +138,8 @@ struct HostDevProgram {
   std::vector<PassDesc> passes;
   std::vector<Item> items;
   std::vector<PassOp> pass_ops;
+  std::vector<Uop> uops;
+  std::vector<double> uop_mats;          // 2 doubles per double2
   std::vector<Step> steps;
   unsigned tile_k = 0;
 };

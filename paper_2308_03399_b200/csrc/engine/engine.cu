@@ -110,6 +110,8 @@ DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile
   v.passes = upload(*d, h.passes);
   v.items = upload(*d, h.items);
   v.pass_ops = upload(*d, h.pass_ops);
+  v.uops = upload(*d, h.uops);
+  v.uop_mats = reinterpret_cast<const double2*>(upload(*d, h.uop_mats));
   v.n = h.n;
   v.end = h.end;
   v.nsample = static_cast<uint32_t>(h.sample_qubits.size());
@@ -432,8 +434,12 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
     wave = std::min<uint64_t>(largest, (uint64_t{1} << 31) / tiles);
     double2* state = static_cast<double2*>(scratch(E, "state", wave * seg));
     uint8_t* psel = dp.num_pauli ? static_cast<uint8_t*>(scratch(E, "psel", wave * dp.num_pauli)) : nullptr;
-    const size_t tsmem = (uint64_t{1} << h.tile_k) * sizeof(double2);
+    size_t tsmem = 0;
+    for (const PassDesc& pd : h.passes)
+      tsmem = std::max(tsmem, tile_smem_bytes(pd.k, pd.uop_end - pd.uop_begin, pd.mat_count));
     CK(cudaFuncSetAttribute(tile_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_pass_kernel, NT, tsmem));
     uint64_t waves = 0, fused = 0;
     for (uint64_t w0 = 0; w0 < count; w0 += wave) {
       const uint64_t S = std::min(wave, count - w0);
@@ -449,8 +455,9 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       for (const Step& st : h.steps) {
         if (st.kind == S_PASS) {
           timer.begin(0);
-          tile_pass_kernel<<<static_cast<unsigned>(S * tiles), NT, tsmem, E->stream>>>(dp.view, st.index, state, S,
-                                                                                      c.cregs, psel, dp.num_pauli);
+          const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(S, uint64_t(std::max(per_sm, 1)) * E->num_sms));
+          tile_pass_kernel<<<grid, NT, tsmem, E->stream>>>(dp.view, st.index, state, S, c.cregs, psel,
+                                                           dp.num_pauli);
           launched(E);
           timer.end(0);
           ++fused;

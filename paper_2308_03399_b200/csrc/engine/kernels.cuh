@@ -41,6 +41,8 @@ struct ProgView {
   const PassDesc* passes;
   const Item* items;
   const PassOp* pass_ops;
+  const Uop* uops;
+  const double2* uop_mats;
   const uint32_t* pauli_site_ops;  // site ordinal -> op index
   uint32_t num_pauli;
   uint32_t n, end, nsample, nwrites;
@@ -235,43 +237,108 @@ __device__ __forceinline__ uint64_t pdep_positions(uint64_t v, const uint8_t* po
   return out;
 }
 
+// Shared-memory layout of tile_pass_kernel: tile | matrix table | uops |
+// compacted uops | prefix (u16, one per uop + 1).
+__host__ __device__ inline size_t tile_smem_bytes(unsigned k, uint32_t nuops, uint32_t nmats) {
+  return (size_t{1} << k) * 16 + size_t{nmats} * 16 + size_t{nuops} * 32 + (size_t{nuops} + 1) * 2 + 16;
+}
+
+// Persistent: each CTA owns a contiguous range of shots and sweeps all tiles
+// of each shot, so the pass's micro-op stream is staged once per CTA and
+// compacted once per shot.
 static __global__ void __launch_bounds__(NT, 2) tile_pass_kernel(ProgView P, uint32_t pass_index, double2* state,
-                                                       uint64_t S, const uint64_t* cregs,
-                                                       const uint8_t* pauli_sel, uint32_t num_pauli) {
+                                                                 uint64_t S, const uint64_t* cregs,
+                                                                 const uint8_t* pauli_sel, uint32_t num_pauli) {
   extern __shared__ double2 tile[];
   const PassDesc& pd = P.passes[pass_index];
   const unsigned n = P.n, k = pd.k;
   const uint64_t tiles = uint64_t{1} << (n - k), L = uint64_t{1} << k;
-  const uint64_t s = blockIdx.x / tiles, t = blockIdx.x % tiles;
-  if (s >= S) return;
+  const uint32_t nu = pd.uop_end - pd.uop_begin;
+  double2* smats = tile + L;
+  Uop* uops = reinterpret_cast<Uop*>(smats + pd.mat_count);
+  Uop* eops = uops + nu;
+  uint16_t* pre = reinterpret_cast<uint16_t*>(eops + nu);
   __shared__ uint8_t hpos[32];
-  if (threadIdx.x == 0) {
+
+  for (uint32_t i = threadIdx.x; i < pd.mat_count; i += NT) smats[i] = P.uop_mats[pd.mat_begin + i];
+  for (uint32_t i = threadIdx.x; i < nu; i += NT) uops[i] = P.uops[pd.uop_begin + i];
+  if (threadIdx.x == 0)
     for (unsigned q = 0, j = 0; q < n; ++q)
       if (!((pd.lmask >> q) & 1)) hpos[j++] = static_cast<uint8_t>(q);
-  }
   __syncthreads();
-  const uint64_t base = pdep_positions(t, hpos, n - k);
-  double2* seg = state + (s << n);
-  // Low local bits: element l = threadIdx.x + NT*i; pdep splits into a
-  // per-thread part and a per-iteration part.
+
   const unsigned kt = k < 8 ? k : 8;
   const uint64_t lo_part = pdep_positions(threadIdx.x, pd.lq, kt);
-  if (pd.first) {
-    for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) {
-      const uint64_t g = base | lo_part | pdep_positions(i, pd.lq + kt, k - kt);
-      tile[l] = make_double2(g == 0 ? 1.0 : 0.0, 0.0);
+  const uint64_t s_begin = S * blockIdx.x / gridDim.x, s_end = S * (blockIdx.x + 1) / gridDim.x;
+  for (uint64_t s = s_begin; s < s_end; ++s) {
+    // Per-shot compaction (warp 0, in order): drop failed conditions and
+    // identity Pauli draws; resolve each Pauli to quad masks.
+    if (threadIdx.x < 32) {
+      const uint64_t creg = cregs ? cregs[s] : 0;
+      const uint8_t* sel = pauli_sel + s * num_pauli;
+      uint32_t count = 0;
+      for (uint32_t c0 = 0; c0 < nu; c0 += 32) {
+        const uint32_t i = c0 + threadIdx.x;
+        bool keep = false;
+        Uop u{};
+        if (i < nu) {
+          u = uops[i];
+          keep = true;
+          const DevOp& op = P.ops[u.ref];
+          if ((u.flags & 1) && (creg & op.cond_mask) != op.cond_value) keep = false;
+          if (keep && u.code == UC_PAULI) {
+            const DevTerm tm = P.terms[op.aux + sel[op.site]];
+            if (tm.identity) {
+              keep = false;
+            } else {
+              uint32_t xq = 0, zq = 0;
+              for (unsigned b = 0; b < op.nq; ++b) {
+                const uint32_t qb = (u.qb >> b) & 1u;
+                xq |= ((tm.x >> op.q[b]) & 1u) << qb;
+                zq |= ((tm.z >> op.q[b]) & 1u) << qb;
+              }
+              u.pauli = static_cast<uint8_t>(xq | (zq << 2) | ((tm.num_y & 3u) << 4));
+            }
+          }
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+        const uint32_t at = count + __popc(ballot & ((1u << threadIdx.x) - 1));
+        if (i < nu) pre[i] = static_cast<uint16_t>(at);
+        if (keep) eops[at] = u;
+        count += __popc(ballot);
+      }
+      if (threadIdx.x == 0) pre[nu] = static_cast<uint16_t>(count);
     }
-  } else {
-    for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
-      tile[l] = seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)];
+    __syncthreads();
+    double2* seg = state + (s << n);
+    for (uint64_t t = 0; t < tiles; ++t) {
+      const uint64_t base = pdep_positions(t, hpos, n - k);
+      if (pd.first) {
+        for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) {
+          const uint64_t g = base | lo_part | pdep_positions(i, pd.lq + kt, k - kt);
+          tile[l] = make_double2(g == 0 ? 1.0 : 0.0, 0.0);
+        }
+      } else {
+        for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
+          tile[l] = seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)];
+      }
+      __syncthreads();
+      for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
+        const Item it = P.items[it_i];
+        const uint32_t b = pre[it.begin], e = pre[it.end];
+        if (b == e) continue;
+        if (k < 2) {
+          run_ops_per_op(tile, k, it.begin, it.end, P.pass_ops + pd.uop_begin, P.ops, P.mats, P.terms, cregs ? cregs[s] : 0,
+                         pauli_sel + s * num_pauli);
+        } else {
+          run_segment_staged(tile, k, it.la, it.lb, eops, b, e, smats, P.ops, P.mats);
+        }
+      }
+      for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
+        seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)] = tile[l];
+    }
+    __syncthreads();  // compaction of the next shot rewrites eops/pre
   }
-  __syncthreads();
-  const uint64_t creg = cregs ? cregs[s] : 0;
-  const uint8_t* sel = pauli_sel + s * num_pauli;
-  for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i)
-    run_segment(tile, k, P.items[it_i], P.pass_ops, P.ops, P.mats, P.terms, creg, sel);
-  for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
-    seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)] = tile[l];
 }
 
 // Per-(shot, Pauli site) term choice for a wave: sel[s][site] (u8).

@@ -215,4 +215,84 @@ static __device__ void run_segment(double2* st, unsigned k, const Item& it, cons
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// Staged variant for the streamed tile passes: the pass's micro-ops, already
+// compacted for this shot (identity Pauli draws and failed conditions
+// removed), and its matrix table live in shared memory.
+static __device__ __forceinline__ void run_segment_staged(double2* st, unsigned k, unsigned la, unsigned lb,
+                                                          const Uop* eops, uint32_t begin, uint32_t end,
+                                                          const double2* smats, const DevOp* ops,
+                                                          const double2* gmats) {
+  const uint64_t dla = uint64_t{1} << la, dlb = uint64_t{1} << lb;
+  const uint64_t nquads = uint64_t{1} << (k - 2);
+  const uint64_t per_round = uint64_t{NT} * QPT;
+  for (uint64_t r0 = 0; r0 < nquads; r0 += per_round) {
+    double2 v[QPT][4];
+    uint64_t base[QPT];
+    int nq = 0;
+#pragma unroll
+    for (int q = 0; q < QPT; ++q) {
+      const uint64_t p = r0 + threadIdx.x + uint64_t{NT} * q;
+      if (p < nquads) {
+        nq = q + 1;
+        base[q] = insert_zero(insert_zero(p, la), lb);
+        v[q][0] = st[base[q]];
+        v[q][1] = st[base[q] | dla];
+        v[q][2] = st[base[q] | dlb];
+        v[q][3] = st[base[q] | dla | dlb];
+      }
+    }
+    for (uint32_t i = begin; i < end; ++i) {
+      const Uop u = eops[i];
+      const double2* m = smats + u.mat;
+      switch (u.code) {
+        case UC_U: {
+          const double2 mm[4] = {m[0], m[1], m[2], m[3]};
+          if (u.qb) quad_apply1<1, MK_1Q_U>(v, mm, 0, nq);
+          else quad_apply1<0, MK_1Q_U>(v, mm, 0, nq);
+          break;
+        }
+        case UC_REAL: {
+          const double2 mm[4] = {m[0], m[1], m[2], m[3]};
+          if (u.qb) quad_apply1<1, MK_1Q_REAL>(v, mm, 0, nq);
+          else quad_apply1<0, MK_1Q_REAL>(v, mm, 0, nq);
+          break;
+        }
+        case UC_GEN1: {
+          const uint64_t cls = ops[u.ref].cls;
+          if (u.qb) quad_apply1<1, MK_1Q_GEN>(v, m, cls, nq);
+          else quad_apply1<0, MK_1Q_GEN>(v, m, cls, nq);
+          break;
+        }
+        case UC_MONO: {
+          // classes of the row nonzeros, re-packed at their matrix positions
+          uint64_t cls = 0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            cls |= uint64_t{(u.mcls >> (3 * r)) & 7u} << (3 * (r * 4 + ((u.src >> (2 * r)) & 3)));
+          const double2 mr[4] = {m[0], m[1], m[2], m[3]};
+          quad_apply2<MK_2Q_MONO>(v, mr, nullptr, cls, u.src, u.qb != 0, nq);
+          break;
+        }
+        case UC_GEN2:
+          quad_apply2<MK_2Q_GEN>(v, nullptr, m, ops[u.ref].cls, 0, u.qb != 0, nq);
+          break;
+        default:  // UC_PAULI, pre-resolved for this shot
+          quad_pauli(v, u.pauli & 3u, (u.pauli >> 2) & 3u, (u.pauli >> 4) & 3u, nq);
+          break;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < QPT; ++q) {
+      if (q < nq) {
+        st[base[q]] = v[q][0];
+        st[base[q] | dla] = v[q][1];
+        st[base[q] | dlb] = v[q][2];
+        st[base[q] | dla | dlb] = v[q][3];
+      }
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace ssb
