@@ -249,7 +249,33 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
       for (int e = 0; e < 4; ++e) push(m + 2 * e);
     } else {
       u.qb = po.qb[0];  // 1: op qubit0 is lb, i.e. swapped
+      // Quad element of matrix index r (index bits: q0, q1).
+      auto el = [swapped = po.qb[0] != 0](int r) { return swapped ? ((r & 1) << 1) | (r >> 1) : r; };
+      int perm[4], cls_r[4], n_nonone = 0, moved = 0;
       if (o.mk == MK_2Q_MONO) {
+        for (int r = 0; r < 4; ++r) {
+          const int c = (o.src >> (2 * r)) & 3;
+          perm[el(r)] = el(c);
+          cls_r[r] = static_cast<int>(entry_class(o.cls, r * 4 + c));
+          n_nonone += cls_r[r] != E_ONE;
+          moved += perm[el(r)] != el(r);
+        }
+      }
+      if (o.mk == MK_2Q_MONO && n_nonone == 0 && moved == 2) {
+        u.code = UC_SWAP;
+        int a = -1, b = -1;
+        for (int e = 0; e < 4; ++e)
+          if (perm[e] != e) (a < 0 ? a : b) = e;
+        u.qb = static_cast<uint8_t>(a | (b << 2));
+      } else if (o.mk == MK_2Q_MONO && n_nonone == 1 && moved == 0) {
+        u.code = UC_PHASE;
+        for (int r = 0; r < 4; ++r)
+          if (cls_r[r] != E_ONE) {
+            u.qb = static_cast<uint8_t>(el(r));
+            u.mcls = static_cast<uint16_t>(cls_r[r]);
+            push(m + 2 * (r * 4 + r));
+          }
+      } else if (o.mk == MK_2Q_MONO) {
         u.code = UC_MONO;
         u.src = o.src;
         for (int r = 0; r < 4; ++r) {

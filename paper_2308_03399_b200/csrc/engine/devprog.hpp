@@ -80,6 +80,10 @@ enum UopCode : uint8_t {
   UC_MONO = 3,     // 2q monomial           (qb: swapped; src; mcls)
   UC_GEN2 = 4,     // 2q runtime classes    (qb: swapped; cls via ref)
   UC_PAULI = 5,    // Pauli site            (qb: quad bits of op qubits, bit b)
+  UC_SWAP = 6,     // 2q permutation that is one transposition of quad elements
+                   // (qb: e0 | e1 << 2) — CX, SWAP: pure data movement
+  UC_PHASE = 7,    // 2q diagonal with one non-unit entry (qb: element; mcls:
+                   // its class) — CP
 };
 
 // 16-byte micro-op. After per-shot compaction (identity Pauli draws and

@@ -88,6 +88,26 @@ __device__ __forceinline__ void quad_apply2(double2 (&v)[QPT][4], const double2*
   }
 }
 
+template <int A, int B>
+__device__ __forceinline__ void quad_swap(double2 (&v)[QPT][4], int nq) {
+#pragma unroll
+  for (int q = 0; q < QPT; ++q) {
+    if (q >= nq) break;
+    const double2 t = v[q][A];
+    v[q][A] = v[q][B];
+    v[q][B] = t;
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void quad_phase(double2 (&v)[QPT][4], double2 ph, uint32_t cls, int nq) {
+#pragma unroll
+  for (int q = 0; q < QPT; ++q) {
+    if (q >= nq) break;
+    v[q][E] = c_term(ph, cls, v[q][E]);
+  }
+}
+
 // Pauli on the quad: new[e] = (-i)^num_y * (-1)^popc(e & zq) * old[e ^ xq]
 // (destination-sign form, kernels_scalar.cpp:58-81).
 __device__ __forceinline__ void quad_pauli(double2 (&v)[QPT][4], uint32_t xq, uint32_t zq, uint32_t num_y, int nq) {
@@ -277,6 +297,26 @@ static __device__ __forceinline__ void run_segment_staged(double2* st, unsigned 
         case UC_GEN2:
           quad_apply2<MK_2Q_GEN>(v, nullptr, m, ops[u.ref].cls, 0, u.qb != 0, nq);
           break;
+        case UC_SWAP:  // exact: every moved entry of the matrix is 1 (signed zeros aside)
+          switch (u.qb) {
+            case 0 | (1 << 2): quad_swap<0, 1>(v, nq); break;
+            case 0 | (2 << 2): quad_swap<0, 2>(v, nq); break;
+            case 0 | (3 << 2): quad_swap<0, 3>(v, nq); break;
+            case 1 | (2 << 2): quad_swap<1, 2>(v, nq); break;
+            case 1 | (3 << 2): quad_swap<1, 3>(v, nq); break;
+            default: quad_swap<2, 3>(v, nq); break;
+          }
+          break;
+        case UC_PHASE: {
+          const double2 ph = m[0];
+          switch (u.qb) {
+            case 0: quad_phase<0>(v, ph, u.mcls, nq); break;
+            case 1: quad_phase<1>(v, ph, u.mcls, nq); break;
+            case 2: quad_phase<2>(v, ph, u.mcls, nq); break;
+            default: quad_phase<3>(v, ph, u.mcls, nq); break;
+          }
+          break;
+        }
         default:  // UC_PAULI, pre-resolved for this shot
           quad_pauli(v, u.pauli & 3u, (u.pauli >> 2) & 3u, (u.pauli >> 4) & 3u, nq);
           break;
