@@ -8,7 +8,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libshotsim_b200.so"
+LIB_PATH = Path(os.environ.get("SHOTSIM_B200_LIB", "")) if os.environ.get("SHOTSIM_B200_LIB") else \
+    Path(__file__).resolve().parent / "lib" / "libshotsim_b200.so"
 
 SSB_OK = 0
 SSB_ERR_RUNTIME = 1

@@ -222,9 +222,12 @@ void segment_ops(HostDevProgram& d, const std::vector<uint32_t>& ops, const uint
 bool fused_kind(const DevOp& o) { return o.kind == K_GATE || o.kind == K_PAULI; }
 
 // Lowers the pass ops [po_begin, ...) of pass `pd` to micro-ops + a compact
-// matrix table; items are re-based to uop indices relative to the pass.
+// matrix table, segment by segment, folding unconditional 2q permutations
+// into the register relabeling sigma; items are re-based to uop indices
+// relative to the pass.
 void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
   pd.uop_begin = static_cast<uint32_t>(d.uops.size());
+  pd.po_begin = po_begin;
   pd.mat_begin = static_cast<uint32_t>(d.uop_mats.size() / 2);
   uint32_t mat = 0;
   auto push = [&](const double* e) {
@@ -232,71 +235,90 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
     d.uop_mats.push_back(e[1]);
     ++mat;
   };
-  for (uint32_t i = po_begin; i < d.pass_ops.size(); ++i) {
-    const PassOp& po = d.pass_ops[i];
-    const DevOp& o = d.ops[po.op];
-    Uop u{};
-    u.ref = po.op;
-    u.flags = o.has_cond ? 1 : 0;
-    u.mat = static_cast<uint16_t>(mat);
-    const double* m = &d.mats[static_cast<size_t>(o.aux) * 32];
-    if (o.kind == K_PAULI) {
-      u.code = UC_PAULI;
-      u.qb = static_cast<uint8_t>((po.qb[0] & 1) | (o.nq > 1 ? (po.qb[1] & 1) << 1 : 0));
-    } else if (o.nq == 1) {
-      u.code = o.mk == MK_1Q_U ? UC_U : o.mk == MK_1Q_REAL ? UC_REAL : UC_GEN1;
-      u.qb = po.qb[0];
-      for (int e = 0; e < 4; ++e) push(m + 2 * e);
-    } else {
-      u.qb = po.qb[0];  // 1: op qubit0 is lb, i.e. swapped
-      // Quad element of matrix index r (index bits: q0, q1).
-      auto el = [swapped = po.qb[0] != 0](int r) { return swapped ? ((r & 1) << 1) | (r >> 1) : r; };
-      int perm[4], cls_r[4], n_nonone = 0, moved = 0;
-      if (o.mk == MK_2Q_MONO) {
-        for (int r = 0; r < 4; ++r) {
-          const int c = (o.src >> (2 * r)) & 3;
-          perm[el(r)] = el(c);
-          cls_r[r] = static_cast<int>(entry_class(o.cls, r * 4 + c));
-          n_nonone += cls_r[r] != E_ONE;
-          moved += perm[el(r)] != el(r);
-        }
-      }
-      if (o.mk == MK_2Q_MONO && n_nonone == 0 && moved == 2) {
-        u.code = UC_SWAP;
-        int a = -1, b = -1;
-        for (int e = 0; e < 4; ++e)
-          if (perm[e] != e) (a < 0 ? a : b) = e;
-        u.qb = static_cast<uint8_t>(a | (b << 2));
-      } else if (o.mk == MK_2Q_MONO && n_nonone == 1 && moved == 0) {
-        u.code = UC_PHASE;
-        for (int r = 0; r < 4; ++r)
-          if (cls_r[r] != E_ONE) {
-            u.qb = static_cast<uint8_t>(el(r));
-            u.mcls = static_cast<uint16_t>(cls_r[r]);
-            push(m + 2 * (r * 4 + r));
-          }
-      } else if (o.mk == MK_2Q_MONO) {
-        u.code = UC_MONO;
-        u.src = o.src;
-        for (int r = 0; r < 4; ++r) {
-          const int c = (o.src >> (2 * r)) & 3;
-          push(m + 2 * (r * 4 + c));
-          u.mcls |= static_cast<uint16_t>(entry_class(o.cls, r * 4 + c) << (3 * r));
-        }
+  auto pack = [](const int* sg) {
+    return static_cast<uint8_t>(sg[0] | (sg[1] << 2) | (sg[2] << 4) | (sg[3] << 6));
+  };
+  for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
+    Item& it = d.items[it_i];
+    int sg[4] = {0, 1, 2, 3};  // logical element -> register
+    const uint32_t ubegin = static_cast<uint32_t>(d.uops.size()) - pd.uop_begin;
+    for (uint32_t i = it.begin; i < it.end; ++i) {
+      const PassOp& po = d.pass_ops[i];
+      const DevOp& o = d.ops[po.op];
+      Uop u{};
+      u.ref = po.op;
+      u.flags = o.has_cond ? 1 : 0;
+      u.mat = static_cast<uint16_t>(mat);
+      u.sigma = pack(sg);
+      const double* m = &d.mats[static_cast<size_t>(o.aux) * 32];
+      if (o.kind == K_PAULI) {
+        u.code = UC_PAULI;
+        u.qb = static_cast<uint8_t>((po.qb[0] & 1) | (o.nq > 1 ? (po.qb[1] & 1) << 1 : 0));
+      } else if (o.nq == 1) {
+        u.code = o.mk == MK_1Q_U ? UC_U : o.mk == MK_1Q_REAL ? UC_REAL : UC_GEN1;
+        const int bit = 1 << po.qb[0];
+        const int l0 = 0, l1 = bit, l2 = bit == 1 ? 2 : 1, l3 = l2 | bit;  // logical pairs (l0,l1), (l2,l3)
+        u.qb = static_cast<uint8_t>(sg[l0] | (sg[l1] << 2) | (sg[l2] << 4) | (sg[l3] << 6));
+        u.src = po.qb[0];  // logical quad bit (generic path)
+        for (int e = 0; e < 4; ++e) push(m + 2 * e);
       } else {
-        u.code = UC_GEN2;
-        for (int e = 0; e < 16; ++e) push(m + 2 * e);
+        // Quad element of matrix index r (index bits: q0, q1).
+        auto el = [swapped = po.qb[0] != 0](int r) { return swapped ? ((r & 1) << 1) | (r >> 1) : r; };
+        int perm[4] = {0, 1, 2, 3}, cls_r[4] = {0, 0, 0, 0}, n_nonone = 0, moved = 0;
+        if (o.mk == MK_2Q_MONO) {
+          for (int r = 0; r < 4; ++r) {
+            const int c = (o.src >> (2 * r)) & 3;
+            perm[el(r)] = el(c);  // new logical element el(r) takes old element el(c)
+            cls_r[r] = static_cast<int>(entry_class(o.cls, r * 4 + c));
+            n_nonone += cls_r[r] != E_ONE;
+            moved += el(c) != el(r);
+          }
+        }
+        if (o.mk == MK_2Q_MONO && n_nonone == 0 && !o.has_cond) {
+          // Exact pure permutation (every moved entry is 1): relabel registers.
+          int ns[4];
+          for (int e = 0; e < 4; ++e) ns[e] = sg[perm[e]];
+          for (int e = 0; e < 4; ++e) sg[e] = ns[e];
+          continue;  // no micro-op
+        }
+        if (o.mk == MK_2Q_MONO && n_nonone == 0 && moved == 2) {
+          u.code = UC_SWAP;  // conditional transposition: physical registers
+          int a = -1, b = -1;
+          for (int e = 0; e < 4; ++e)
+            if (perm[e] != e) (a < 0 ? a : b) = e;
+          u.qb = static_cast<uint8_t>(sg[a] | (sg[b] << 2));
+        } else if (o.mk == MK_2Q_MONO && n_nonone == 1 && moved == 0) {
+          u.code = UC_PHASE;
+          for (int r = 0; r < 4; ++r)
+            if (cls_r[r] != E_ONE) {
+              u.qb = static_cast<uint8_t>(sg[el(r)]);
+              u.mcls = static_cast<uint16_t>(cls_r[r]);
+              push(m + 2 * (r * 4 + r));
+            }
+        } else if (o.mk == MK_2Q_MONO) {
+          u.code = UC_MONO;
+          u.qb = po.qb[0];
+          u.src = o.src;
+          for (int r = 0; r < 4; ++r) {
+            const int c = (o.src >> (2 * r)) & 3;
+            push(m + 2 * (r * 4 + c));
+            u.mcls |= static_cast<uint16_t>(entry_class(o.cls, r * 4 + c) << (3 * r));
+          }
+        } else {
+          u.code = UC_GEN2;
+          u.qb = po.qb[0];
+          for (int e = 0; e < 16; ++e) push(m + 2 * e);
+        }
       }
+      if (mat > 0xFFFF) throw std::length_error("pass matrix table too large");
+      d.uops.push_back(u);
     }
-    if (mat > 0xFFFF) throw std::length_error("pass matrix table too large");
-    d.uops.push_back(u);
+    it.begin = ubegin;
+    it.end = static_cast<uint32_t>(d.uops.size()) - pd.uop_begin;
+    it.sigma = pack(sg);
   }
   pd.uop_end = static_cast<uint32_t>(d.uops.size());
   pd.mat_count = mat;
-  for (uint32_t it = pd.item_begin; it < pd.item_end; ++it) {
-    d.items[it].begin -= po_begin;
-    d.items[it].end -= po_begin;
-  }
 }
 
 }  // namespace

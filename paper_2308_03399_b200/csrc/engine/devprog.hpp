@@ -70,18 +70,23 @@ struct PassDesc {
   // (double2 units), staged into shared memory by the tile kernel.
   uint32_t uop_begin, uop_end;
   uint32_t mat_begin, mat_count;
+  uint32_t po_begin;   // first pass_op of this pass (per-op fallback, k < 2)
 };
 
 // Micro-op codes of a streamed pass (one per gate / Pauli site).
+// Within a segment, unconditional 2q permutations (CX, SWAP) are folded into a
+// plan-time relabeling sigma of the quad's 4 registers (logical element e
+// lives in register sigma(e)); later micro-ops address physical registers and
+// the segment store writes register sigma(e) to element e's address. sigma
+// is packed 2 bits per element; 0xE4 is the identity.
 enum UopCode : uint8_t {
-  UC_U = 0,        // 1q U pattern          (qb: quad bit)
-  UC_REAL = 1,     // 1q all-real           (qb: quad bit)
-  UC_GEN1 = 2,     // 1q runtime classes    (qb: quad bit; cls via ref)
+  UC_U = 0,        // 1q U pattern          (qb: physical pairs a0|a1<<2|b0<<4|b1<<6)
+  UC_REAL = 1,     // 1q all-real           (qb: physical pairs)
+  UC_GEN1 = 2,     // 1q runtime classes    (qb: physical pairs; cls via ref)
   UC_MONO = 3,     // 2q monomial           (qb: swapped; src; mcls)
   UC_GEN2 = 4,     // 2q runtime classes    (qb: swapped; cls via ref)
   UC_PAULI = 5,    // Pauli site            (qb: quad bits of op qubits, bit b)
-  UC_SWAP = 6,     // 2q permutation that is one transposition of quad elements
-                   // (qb: e0 | e1 << 2) — CX, SWAP: pure data movement
+  UC_SWAP = 6,     // conditional 2q transposition (qb: physical e0 | e1 << 2)
   UC_PHASE = 7,    // 2q diagonal with one non-unit entry (qb: element; mcls:
                    // its class) — CP
 };
@@ -97,7 +102,8 @@ struct Uop {
   uint16_t mcls;       // UC_MONO: class of row r's nonzero entry, 3 bits per row
   uint32_t ref;        // program op index
   uint8_t pauli;
-  uint8_t pad[3];
+  uint8_t sigma;       // UC_PAULI / UC_MONO / UC_GEN2: logical->physical quad map
+  uint8_t pad[2];
 };
 static_assert(sizeof(Uop) == 16, "Uop layout");
 
@@ -108,7 +114,7 @@ enum ItemKind : uint8_t { IT_SEGMENT = 0, IT_SPECIAL = 1 };
 struct Item {
   uint8_t kind;
   uint8_t la, lb;      // local positions, la < lb
-  uint8_t pad;
+  uint8_t sigma;       // streamed passes: register map at the segment end
   uint32_t begin, end; // segment: pass_ops range; special: begin = op index
 };
 

@@ -246,7 +246,7 @@ __host__ __device__ inline size_t tile_smem_bytes(unsigned k, uint32_t nuops, ui
 // Persistent: each CTA owns a contiguous range of shots and sweeps all tiles
 // of each shot, so the pass's micro-op stream is staged once per CTA and
 // compacted once per shot.
-static __global__ void __launch_bounds__(NT, 2) tile_pass_kernel(ProgView P, uint32_t pass_index, double2* state,
+static __global__ void __launch_bounds__(NT, SSB_TILE_MINB) tile_pass_kernel(ProgView P, uint32_t pass_index, double2* state,
                                                                  uint64_t S, const uint64_t* cregs,
                                                                  const uint8_t* pauli_sel, uint32_t num_pauli) {
   extern __shared__ double2 tile[];
@@ -326,12 +326,12 @@ static __global__ void __launch_bounds__(NT, 2) tile_pass_kernel(ProgView P, uin
       for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
         const Item it = P.items[it_i];
         const uint32_t b = pre[it.begin], e = pre[it.end];
-        if (b == e) continue;
+        if (b == e && it.sigma == 0xE4) continue;  // nothing to apply and no relabeling to store
         if (k < 2) {
-          run_ops_per_op(tile, k, it.begin, it.end, P.pass_ops + pd.uop_begin, P.ops, P.mats, P.terms, cregs ? cregs[s] : 0,
-                         pauli_sel + s * num_pauli);
+          run_ops_per_op(tile, k, it.begin, it.end, P.pass_ops + pd.po_begin, P.ops, P.mats, P.terms,
+                         cregs ? cregs[s] : 0, pauli_sel + s * num_pauli);
         } else {
-          run_segment_staged(tile, k, it.la, it.lb, eops, b, e, smats, P.ops, P.mats);
+          run_segment_staged(tile, k, it, eops, b, e, smats, P.ops);
         }
       }
       for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)

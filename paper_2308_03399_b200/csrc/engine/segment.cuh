@@ -16,6 +16,9 @@ namespace ssb {
 #ifndef SSB_QPT
 #define SSB_QPT 2
 #endif
+#ifndef SSB_TILE_MINB
+#define SSB_TILE_MINB 2
+#endif
 constexpr int QPT = SSB_QPT;  // quads per thread per round
 
 // Quad element e (bit0 <-> la, bit1 <-> lb). 1q gate on quad bit B mixes
@@ -123,6 +126,36 @@ __device__ __forceinline__ void quad_pauli(double2 (&v)[QPT][4], uint32_t xq, ui
       if (__popc(static_cast<uint32_t>(e) & zq) & 1) t = c_neg(t);
       v[q][e] = t;
     }
+  }
+}
+
+// Single-quad forms of the generic 2q apply and the Pauli (logical order).
+template <int MK>
+__device__ __forceinline__ void quad_apply2_one(double2 (&v)[4], const double2* mr, const double2* m, uint64_t cls,
+                                                uint8_t src, bool swapped) {
+  auto el = [swapped](int r) { return swapped ? ((r & 1) << 1) | (r >> 1) : r; };
+  double2 in[4], out[4];
+  for (int r = 0; r < 4; ++r) in[r] = v[el(r)];
+  for (int r = 0; r < 4; ++r) {
+    if constexpr (MK == MK_2Q_MONO) {
+      const uint32_t c = (src >> (2 * r)) & 3u;
+      const uint32_t k = entry_class(cls, r * 4 + static_cast<int>(c));
+      const double2 x = pick4(in, c);
+      out[r] = k == E_ONE ? x : c_term(mr[r], k, x);
+    } else {
+      out[r] = row_apply<4>(m, cls, r, in);
+    }
+  }
+  for (int r = 0; r < 4; ++r) v[el(r)] = out[r];
+}
+
+__device__ __forceinline__ void quad_pauli1(double2 (&v)[4], uint32_t xq, uint32_t zq, uint32_t num_y) {
+  double2 old[4];
+  for (int e = 0; e < 4; ++e) old[e] = v[e];
+  for (int e = 0; e < 4; ++e) {
+    double2 t = pauli_phase(num_y, pick4(old, static_cast<uint32_t>(e) ^ xq));
+    if (__popc(static_cast<uint32_t>(e) & zq) & 1) t = c_neg(t);
+    v[e] = t;
   }
 }
 
@@ -238,23 +271,122 @@ static __device__ void run_segment(double2* st, unsigned k, const Item& it, cons
 // ---------------------------------------------------------------------------
 // Staged variant for the streamed tile passes: the pass's micro-ops, already
 // compacted for this shot (identity Pauli draws and failed conditions
-// removed), and its matrix table live in shared memory.
-static __device__ __forceinline__ void run_segment_staged(double2* st, unsigned k, unsigned la, unsigned lb,
-                                                          const Uop* eops, uint32_t begin, uint32_t end,
-                                                          const double2* smats, const DevOp* ops,
-                                                          const double2* gmats) {
+// removed), and its matrix table live in shared memory. Registers are
+// addressed physically; sigma (2 bits per logical element) maps logical quad
+// elements to registers (devprog.hpp UopCode).
+
+// 1q gate on physical register pairs (A0, A1) and (B0, B1) (low, high).
+template <int A0, int A1, int B0, int B1, int MK, bool FULL, int NQ = QPT>
+__device__ __forceinline__ void quad_apply1p(double2 (&v)[NQ][4], const double2* m, uint64_t cls, int nq) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    if (!FULL && q >= nq) break;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i0 = h ? B0 : A0, i1 = h ? B1 : A1;
+      const double2 a0 = v[q][i0], a1 = v[q][i1];
+      if constexpr (MK == MK_1Q_U) {
+        const double2 t0 = make_double2(__dmul_rn(m[0].x, a0.x), __dmul_rn(m[0].x, a0.y));
+        v[q][i0] = c_add(t0, c_mul(m[1], a1));
+        v[q][i1] = c_add(c_mul(m[2], a0), c_mul(m[3], a1));
+      } else if constexpr (MK == MK_1Q_REAL) {
+        const double2 t0 = make_double2(__dmul_rn(m[0].x, a0.x), __dmul_rn(m[0].x, a0.y));
+        const double2 t1 = make_double2(__dmul_rn(m[1].x, a1.x), __dmul_rn(m[1].x, a1.y));
+        const double2 t2 = make_double2(__dmul_rn(m[2].x, a0.x), __dmul_rn(m[2].x, a0.y));
+        const double2 t3 = make_double2(__dmul_rn(m[3].x, a1.x), __dmul_rn(m[3].x, a1.y));
+        v[q][i0] = c_add(t0, t1);
+        v[q][i1] = c_add(t2, t3);
+      } else {
+        const double2 in[2] = {a0, a1};
+        const double2 o0 = row_apply<2>(m, cls, 0, in), o1 = row_apply<2>(m, cls, 1, in);
+        v[q][i0] = o0;
+        v[q][i1] = o1;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t sig(uint8_t sigma, uint32_t e) { return (sigma >> (2 * e)) & 3u; }
+
+// Logical view of one quad: L[e] = v[sigma(e)] and back.
+__device__ __forceinline__ void gather_logical(const double2 (&v)[4], uint8_t sigma, double2 (&L)[4]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) L[e] = pick4(v, sig(sigma, e));
+}
+__device__ __forceinline__ void scatter_logical(double2 (&v)[4], uint8_t sigma, const double2 (&L)[4]) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    double2 x = L[0];
+#pragma unroll
+    for (int e = 1; e < 4; ++e) x = sig(sigma, e) == static_cast<uint32_t>(p) ? L[e] : x;
+    v[p] = x;
+  }
+}
+
+struct Quad4 {
+  double2 e[4];
+};
+
+// Rare micro-ops on one quad through its logical view (kept out of line so
+// the hot path's register allocation is unaffected).
+static __device__ __noinline__ Quad4 generic_quad_op(Quad4 x, Uop u, const double2* m, const DevOp* ops) {
+  double2 L[4];
+  double2 v[4] = {x.e[0], x.e[1], x.e[2], x.e[3]};
+  gather_logical(v, u.sigma, L);
+  double2 one[1][4] = {{L[0], L[1], L[2], L[3]}};
+  const uint64_t gcls = (u.code == UC_GEN1 || u.code == UC_GEN2) ? ops[u.ref].cls : 0;
+  switch (u.code) {
+    case UC_U:
+    case UC_REAL:
+    case UC_GEN1:
+      if (u.src) {
+        if (u.code == UC_U) quad_apply1p<0, 2, 1, 3, MK_1Q_U, true, 1>(one, m, 0, 1);
+        else if (u.code == UC_REAL) quad_apply1p<0, 2, 1, 3, MK_1Q_REAL, true, 1>(one, m, 0, 1);
+        else quad_apply1p<0, 2, 1, 3, MK_1Q_GEN, true, 1>(one, m, gcls, 1);
+      } else {
+        if (u.code == UC_U) quad_apply1p<0, 1, 2, 3, MK_1Q_U, true, 1>(one, m, 0, 1);
+        else if (u.code == UC_REAL) quad_apply1p<0, 1, 2, 3, MK_1Q_REAL, true, 1>(one, m, 0, 1);
+        else quad_apply1p<0, 1, 2, 3, MK_1Q_GEN, true, 1>(one, m, gcls, 1);
+      }
+      break;
+    case UC_PAULI:
+      quad_pauli1(one[0], u.pauli & 3u, (u.pauli >> 2) & 3u, (u.pauli >> 4) & 3u);
+      break;
+    case UC_MONO: {
+      uint64_t cls = 0;
+      for (int r = 0; r < 4; ++r)
+        cls |= uint64_t{(u.mcls >> (3 * r)) & 7u} << (3 * (r * 4 + ((u.src >> (2 * r)) & 3)));
+      const double2 mr[4] = {m[0], m[1], m[2], m[3]};
+      quad_apply2_one<MK_2Q_MONO>(one[0], mr, nullptr, cls, u.src, u.qb != 0);
+      break;
+    }
+    default:
+      quad_apply2_one<MK_2Q_GEN>(one[0], nullptr, m, gcls, 0, u.qb != 0);
+      break;
+  }
+  const double2 R[4] = {one[0][0], one[0][1], one[0][2], one[0][3]};
+  scatter_logical(v, u.sigma, R);
+  return Quad4{{v[0], v[1], v[2], v[3]}};
+}
+
+template <bool FULL>
+static __device__ __forceinline__ void run_segment_staged_t(double2* st, unsigned k, const Item& it, const Uop* eops,
+                                                            uint32_t begin, uint32_t end, const double2* smats,
+                                                            const DevOp* ops) {
+  const unsigned la = it.la, lb = it.lb;
   const uint64_t dla = uint64_t{1} << la, dlb = uint64_t{1} << lb;
   const uint64_t nquads = uint64_t{1} << (k - 2);
   const uint64_t per_round = uint64_t{NT} * QPT;
   for (uint64_t r0 = 0; r0 < nquads; r0 += per_round) {
     double2 v[QPT][4];
     uint64_t base[QPT];
-    int nq = 0;
+    int nq = QPT;
+    if (!FULL) nq = 0;
 #pragma unroll
     for (int q = 0; q < QPT; ++q) {
       const uint64_t p = r0 + threadIdx.x + uint64_t{NT} * q;
-      if (p < nquads) {
-        nq = q + 1;
+      if (FULL || p < nquads) {
+        if (!FULL) nq = q + 1;
         base[q] = insert_zero(insert_zero(p, la), lb);
         v[q][0] = st[base[q]];
         v[q][1] = st[base[q] | dla];
@@ -265,39 +397,23 @@ static __device__ __forceinline__ void run_segment_staged(double2* st, unsigned 
     for (uint32_t i = begin; i < end; ++i) {
       const Uop u = eops[i];
       const double2* m = smats + u.mat;
+      if (FULL && u.code == UC_U) {
+        // Hot path (QV: 8 of 11 block ops): compile-time register pairs for
+        // the relabelings a CX / SWAP run produces; anything else below.
+        const double2 mm[4] = {m[0], m[1], m[2], m[3]};
+        bool done = true;
+#define SSB_P1(a0, a1, b0, b1) \
+  case (a0 | (a1 << 2) | (b0 << 4) | (b1 << 6)): quad_apply1p<a0, a1, b0, b1, MK_1Q_U, true>(v, mm, 0, nq); break;
+        switch (u.qb) {
+          SSB_P1(0, 1, 2, 3) SSB_P1(0, 2, 1, 3) SSB_P1(0, 3, 2, 1) SSB_P1(0, 2, 3, 1) SSB_P1(0, 1, 3, 2)
+          SSB_P1(0, 3, 1, 2)
+          default: done = false; break;
+        }
+#undef SSB_P1
+        if (done) continue;
+      }
       switch (u.code) {
-        case UC_U: {
-          const double2 mm[4] = {m[0], m[1], m[2], m[3]};
-          if (u.qb) quad_apply1<1, MK_1Q_U>(v, mm, 0, nq);
-          else quad_apply1<0, MK_1Q_U>(v, mm, 0, nq);
-          break;
-        }
-        case UC_REAL: {
-          const double2 mm[4] = {m[0], m[1], m[2], m[3]};
-          if (u.qb) quad_apply1<1, MK_1Q_REAL>(v, mm, 0, nq);
-          else quad_apply1<0, MK_1Q_REAL>(v, mm, 0, nq);
-          break;
-        }
-        case UC_GEN1: {
-          const uint64_t cls = ops[u.ref].cls;
-          if (u.qb) quad_apply1<1, MK_1Q_GEN>(v, m, cls, nq);
-          else quad_apply1<0, MK_1Q_GEN>(v, m, cls, nq);
-          break;
-        }
-        case UC_MONO: {
-          // classes of the row nonzeros, re-packed at their matrix positions
-          uint64_t cls = 0;
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            cls |= uint64_t{(u.mcls >> (3 * r)) & 7u} << (3 * (r * 4 + ((u.src >> (2 * r)) & 3)));
-          const double2 mr[4] = {m[0], m[1], m[2], m[3]};
-          quad_apply2<MK_2Q_MONO>(v, mr, nullptr, cls, u.src, u.qb != 0, nq);
-          break;
-        }
-        case UC_GEN2:
-          quad_apply2<MK_2Q_GEN>(v, nullptr, m, ops[u.ref].cls, 0, u.qb != 0, nq);
-          break;
-        case UC_SWAP:  // exact: every moved entry of the matrix is 1 (signed zeros aside)
+        case UC_SWAP:
           switch (u.qb) {
             case 0 | (1 << 2): quad_swap<0, 1>(v, nq); break;
             case 0 | (2 << 2): quad_swap<0, 2>(v, nq); break;
@@ -317,22 +433,46 @@ static __device__ __forceinline__ void run_segment_staged(double2* st, unsigned 
           }
           break;
         }
-        default:  // UC_PAULI, pre-resolved for this shot
-          quad_pauli(v, u.pauli & 3u, (u.pauli >> 2) & 3u, (u.pauli >> 4) & 3u, nq);
+        default: {  // everything else through the logical view of each quad (rare)
+#pragma unroll
+          for (int q = 0; q < QPT; ++q) {
+            if (!FULL && q >= nq) break;
+            Quad4 x{{v[q][0], v[q][1], v[q][2], v[q][3]}};
+            x = generic_quad_op(x, u, m, ops);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[q][e] = x.e[e];
+          }
           break;
+        }
       }
     }
+    const uint8_t sg = it.sigma;
 #pragma unroll
     for (int q = 0; q < QPT; ++q) {
-      if (q < nq) {
-        st[base[q]] = v[q][0];
-        st[base[q] | dla] = v[q][1];
-        st[base[q] | dlb] = v[q][2];
-        st[base[q] | dla | dlb] = v[q][3];
+      if (FULL || q < nq) {
+        double2 L[4];
+        if (sg == 0xE4) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) L[e] = v[q][e];
+        } else {
+          gather_logical(v[q], sg, L);
+        }
+        st[base[q]] = L[0];
+        st[base[q] | dla] = L[1];
+        st[base[q] | dlb] = L[2];
+        st[base[q] | dla | dlb] = L[3];
       }
     }
   }
   __syncthreads();
+}
+
+static __device__ void run_segment_staged(double2* st, unsigned k, const Item& it, const Uop* eops, uint32_t begin,
+                                          uint32_t end, const double2* smats, const DevOp* ops) {
+  if ((uint64_t{1} << (k - 2)) % (uint64_t{NT} * QPT) == 0)
+    run_segment_staged_t<true>(st, k, it, eops, begin, end, smats, ops);
+  else
+    run_segment_staged_t<false>(st, k, it, eops, begin, end, smats, ops);
 }
 
 }  // namespace ssb
