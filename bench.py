@@ -109,13 +109,16 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(key):
-    """Per-launch DRAM bytes of the dominant kernel from a committed ncu capture."""
+def ncu_traffic(key, shot_passes_per_launch):
+    """Per-launch DRAM bytes of the dominant kernel: the committed ncu capture's
+    measured bytes per (shot, pass) scaled to this run's shots per launch."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text()).get(key)
-    return None if not d else d.get("dram_bytes_per_launch")
+    if not d or d.get("dram_bytes_per_shot") is None:
+        return None
+    return d["dram_bytes_per_shot"] * shot_passes_per_launch
 
 
 # ---- clocks ---------------------------------------------------------------------------
@@ -306,13 +309,14 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     pass_s = other_s = 0.0
-    pass_launches = launches = 0
+    pass_launches = launches = passes_per_wave = 0
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
             st, nl = step(prof)
             pass_s += st.pass_seconds
             pass_launches += st.pass_launches
+            passes_per_wave = st.fused_passes
             other_s += st.special_seconds + st.sample_seconds
             launches += nl
         ev1.record(stream)
@@ -361,7 +365,9 @@ def main():
         achieved = pass_b * n_timed_shots / pass_s / 1e9
         roof = {"bound": "hbm", "kernel": "tile_pass_kernel" if prog.num_qubits > 13 else "resident_kernel",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config), "peak_source": peak_src,
+                "traffic": ncu_traffic(args.config, n_timed_shots * passes_per_wave / max(pass_launches, 1)),
+                "traffic_source": "profiles/ncu_summary.json (ncu --set full dram__bytes_read+write per shot-pass)",
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_shot": pass_b, "alg_bytes_per_launch": pass_b * n_timed_shots / max(
                     pass_launches, 1),
                 "kernel_share_of_step": pass_s / max(elapsed, 1e-12), "launches": pass_launches,
