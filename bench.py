@@ -102,6 +102,52 @@ def algorithmic_bytes(program):
     return pass_b, pass_b + other
 
 
+def _entry_cost(re, im):
+    """Rounded FP64 ops of one complex product m*v in the engine's exact
+    arithmetic (exact.cuh c_term): 0 for 0 / +-1, 2 for real or imaginary m,
+    6 (4 DMUL + 2 DADD) for general m. Returns (ops, is_term)."""
+    if re == 0.0 and im == 0.0:
+        return 0, False
+    if im == 0.0 and re in (1.0, -1.0):
+        return 0, True
+    if im == 0.0 or re == 0.0:
+        return 2, True
+    return 6, True
+
+
+def dp_ops_per_shot(program):
+    """FP64 ops (DMUL + DADD, no FMA) the fused tile passes execute per shot:
+    per row, every nonzero term's product plus 2 DADD per complex add
+    (row_apply / quad_apply*, exact.cuh). Pure permutations (CX, SWAP) and
+    identity gates cost nothing; Pauli sites are sign / register moves."""
+    f = program.flat()
+    A = 1 << f.num_qubits
+    end = f.terminal_measure_begin if f.sampling_eligible else f.num_ops
+    total = 0
+    for i in range(end):
+        op = f.ops[i]
+        if op.kind != 0:
+            continue
+        k = op.num_qubits
+        d = 1 << k
+        base = op.matrix * 32
+        ops = 0
+        identity = True
+        for r in range(d):
+            terms = 0
+            for c in range(d):
+                re, im = f.matrices[base + 2 * (r * d + c)], f.matrices[base + 2 * (r * d + c) + 1]
+                cost, term = _entry_cost(re, im)
+                ops += cost
+                terms += term
+                if (r == c) != (re == 1.0 and im == 0.0) or (r != c and term):
+                    identity = False
+            ops += 2 * max(terms - 1, 0)
+        if not identity:
+            total += ops * (A >> k)
+    return total
+
+
 def measured_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -360,6 +406,17 @@ def main():
 
     pass_b, total_b = algorithmic_bytes(prog)
     peak, peak_src = measured_peak()
+    from paper_2308_03399_b200.api import _fp64_peak
+    dp_peak = _fp64_peak(eng)
+    dp_shot = dp_ops_per_shot(prog)
+    fp64 = None
+    if pass_s > 0:
+        dp_achieved = dp_shot * shots * args.steps / pass_s
+        fp64 = {"bound": "fp64-pipe", "achieved": dp_achieved / 1e12, "peak": dp_peak / 1e12, "unit": "T DP-op/s",
+                "frac": dp_achieved / dp_peak, "dp_ops_per_shot": dp_shot,
+                "peak_source": "measured live: ssb_fp64_peak (independent DMUL/DADD chains, CUDA events)",
+                "note": "the tile passes are FP64-issue bound: bit-exact parity forbids FMA, so every complex "
+                        "product is 4 DMUL + 2 DADD; this is the kernel's true roofline fraction"}
     n_timed_shots = shots * args.steps
     if pass_s > 0:
         achieved = pass_b * n_timed_shots / pass_s / 1e9
@@ -372,6 +429,7 @@ def main():
                     pass_launches, 1),
                 "kernel_share_of_step": pass_s / max(elapsed, 1e-12), "launches": pass_launches,
                 "whole_step_alg_frac": value / world * total_b / 1e9 / peak,
+                "fp64": fp64,
                 "note": "algorithmic bytes = the reference's unfused op stream (SURVEY 8(d)); fused HBM tile "
                         "passes move far fewer real bytes, so frac > 1 is expected — see traffic"}
     else:

@@ -141,7 +141,7 @@ typedef struct ssb_run_options {
   uint32_t resident_max_qubits; /* n <= this: whole program SM-resident (0: 13) */
   uint32_t tile_qubits;      /* streamed mode: local qubits per HBM tile (0: 12) */
   uint32_t profile;          /* 1: per-kernel-class CUDA-event times in stats   */
-  uint32_t reserved;
+  uint32_t interpret_only;   /* 1: never use the shape-specialised tile kernel  */
 } ssb_run_options;
 
 typedef struct ssb_stats {
@@ -156,6 +156,10 @@ typedef struct ssb_stats {
   uint64_t pass_launches;
   double special_seconds;    /* Kraus / measure / reset op-at-a-time kernels  */
   double sample_seconds;     /* terminal sampling                             */
+  uint64_t specialised_shapes; /* streamed: segment shapes run straight-line
+                                  (run-time specialised kernel); 0: interpreter */
+  uint64_t sampling_guard_hits; /* terminal samples re-decided by the exact
+                                   sequential scan (guard band) */
 } ssb_stats;
 
 SSB_API const char* ssb_last_error(void);
@@ -204,6 +208,11 @@ SSB_API int ssb_run_branch(ssb_engine* engine, const ssb_program* program, uint6
  * 2^num_clbits uint64 (accumulating) — the payload of the multi-GPU gather. */
 SSB_API int ssb_histogram_device(ssb_engine* engine, const uint64_t* values_device,
                                  uint64_t count, uint32_t num_clbits, uint64_t* hist_device);
+
+/* FP64-pipe roofline probe: the sustained rate of rounded DMUL/DADD (no FMA,
+ * the engine's arithmetic) over the whole device, in FP64 ops per second,
+ * measured with CUDA events (the denominator of bench.py's fp64 roofline). */
+SSB_API int ssb_fp64_peak(ssb_engine* engine, double* ops_per_second);
 
 /* ---- operator-level entry points (BatchState, exec_batch.hpp:22-84) ---- */
 /* A device-resident batch over arbitrary shot ids, initialised to |0...0>. */

@@ -67,7 +67,7 @@ class RunOptionsC(C.Structure):
         ("max_batch_size", C.c_uint64), ("branch_budget", C.c_uint64), ("mem_limit_bytes", C.c_uint64),
         ("check_norms", C.c_uint32), ("collect_leaf_stats", C.c_uint32),
         ("resident_max_qubits", C.c_uint32), ("tile_qubits", C.c_uint32),
-        ("profile", C.c_uint32), ("reserved", C.c_uint32),
+        ("profile", C.c_uint32), ("interpret_only", C.c_uint32),
     ]
 
 
@@ -76,7 +76,8 @@ class StatsC(C.Structure):
         ("dispatch_count", C.c_uint64), ("peak_states", C.c_uint64), ("passes", C.c_uint64),
         ("fused_passes", C.c_uint64), ("device_seconds", C.c_double), ("wall_seconds", C.c_double),
         ("pass_seconds", C.c_double), ("pass_launches", C.c_uint64), ("special_seconds", C.c_double),
-        ("sample_seconds", C.c_double),
+        ("sample_seconds", C.c_double), ("specialised_shapes", C.c_uint64),
+        ("sampling_guard_hits", C.c_uint64),
     ]
 
 
@@ -103,6 +104,7 @@ SIGNATURES = {
                                        C.POINTER(StatsC)]),
     "ssb_run_branch": (C.c_int, [_vp, _vp, _u64, _u64, _u64, C.POINTER(RunOptionsC), _pu64, C.POINTER(StatsC)]),
     "ssb_histogram_device": (C.c_int, [_vp, _vp, _u64, C.c_uint32, _vp]),
+    "ssb_fp64_peak": (C.c_int, [_vp, _pd]),
     "ssb_batch_create": (C.c_int, [_vp, _vp, _pu64, _u64, _u64, C.POINTER(_vp)]),
     "ssb_batch_destroy": (None, [_vp]),
     "ssb_batch_apply_op": (C.c_int, [_vp, _u64, _pd]),

@@ -94,11 +94,13 @@ class RunOptions:
     resident_max_qubits: int = 0  # tuning: 0 = engine default
     tile_qubits: int = 0
     profile: bool = False         # per-kernel-class CUDA-event timing in the stats
+    interpret_only: bool = False  # never use the run-time shape-specialised tile kernel
 
     def to_c(self) -> _lib.RunOptionsC:
         return _lib.RunOptionsC(self.max_batch_size, self.branch_budget, self.mem_limit_bytes,
                                 int(self.check_norms), int(self.collect_leaf_stats),
-                                self.resident_max_qubits, self.tile_qubits, int(self.profile), 0)
+                                self.resident_max_qubits, self.tile_qubits, int(self.profile),
+                                int(self.interpret_only))
 
 
 @dataclass
@@ -120,6 +122,8 @@ class RunResult:
     device_seconds: float = 0.0
     wall_seconds: float = 0.0
     fused_passes: int = 0
+    specialised_shapes: int = 0
+    sampling_guard_hits: int = 0
 
 
 def bitstring(value: int, width: int) -> str:
@@ -188,7 +192,8 @@ class Engine:
                       dispatch_count=st.dispatch_count, peak_states=st.peak_states,
                       branch=BranchStats(st.peak_states, st.passes), strategy=name, shots=count,
                       seed=opts.seed, device_seconds=st.device_seconds, wall_seconds=st.wall_seconds,
-                      fused_passes=st.fused_passes)
+                      fused_passes=st.fused_passes, specialised_shapes=st.specialised_shapes,
+                      sampling_guard_hits=st.sampling_guard_hits)
         r._values = values
         return r
 
@@ -213,6 +218,12 @@ class Engine:
     def histogram_device(self, values_ptr: int, count: int, num_clbits: int, hist_ptr: int) -> None:
         check(load().ssb_histogram_device(self._h, C.c_void_p(values_ptr), count, num_clbits,
                                           C.c_void_p(hist_ptr)))
+
+
+def _fp64_peak(engine) -> float:
+    out = C.c_double(0.0)
+    check(load().ssb_fp64_peak(engine._h, C.byref(out)))
+    return out.value
 
 
 class BatchState:

@@ -252,6 +252,40 @@ def random_mixed(rng: SplitMix64, max_qubits: int = 4) -> str:
     return c.text()
 
 
+def random_bursts(rng: SplitMix64, n: int = 12, bursts: int = 24, clbits: int = 4) -> str:
+    """Streamed-path stress circuits: bursts of every gate kind on random
+    qubit pairs (so segments of many kinds form inside each tile pass), a few
+    conditionals on pre-measured clbits, then measure_all."""
+    c = CircuitText(n, max(n, clbits))
+    for b in range(clbits):
+        c.op("h", [b])
+        c.op("measure", [b], clbits=[b])
+    one = ["id", "x", "y", "z", "h", "s", "sdg", "t", "tdg"]
+    for _ in range(bursts):
+        a = rng.below(n)
+        b = (a + 1 + rng.below(n - 1)) % n
+        for _ in range(2 + rng.below(10)):
+            q = a if rng.below(2) else b
+            kind = rng.below(16)
+            cond = None
+            if rng.below(10) == 0:
+                m = 1 << rng.below(clbits)
+                cond = (m, m if rng.below(2) else 0)
+            if kind < 5:
+                c.op("u", [q], [_angle(rng), _angle(rng), _angle(rng)], cond=cond)
+            elif kind < 8:
+                c.op(one[rng.below(len(one))], [q], cond=cond)
+            elif kind == 8:
+                c.op("p", [q], [_angle(rng)], cond=cond)
+            elif kind < 12:
+                c.op("cx", [q, b if q == a else a], cond=cond)
+            elif kind < 14:
+                c.op("cp", [a, b] if rng.below(2) else [b, a], [_angle(rng)], cond=cond)
+            else:
+                c.op("swap", [a, b], cond=cond)
+    return c.measure_all().text()
+
+
 CONFIGS = {
     "C1": dict(name="ghz10", circuit=lambda: ghz(10), noise=lambda: depolarizing_model(0.01), shots=1000, seed=1),
     "C2": dict(name="qv16", circuit=lambda: quantum_volume(16), noise=lambda: qv_noise(0.01, 0.01), shots=100_000,

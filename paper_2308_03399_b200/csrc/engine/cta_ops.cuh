@@ -8,7 +8,7 @@
 // Callers own the __syncthreads() between ops.
 #pragma once
 
-#include "devprog.hpp"
+#include "devtypes.h"
 #include "exact.cuh"
 
 namespace ssb {

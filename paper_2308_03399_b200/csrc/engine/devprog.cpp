@@ -4,7 +4,9 @@
 
 #include <algorithm>
 #include <bit>
+#include <cstdio>
 #include <stdexcept>
+#include <string>
 
 #include "exact.cuh"
 
@@ -199,6 +201,7 @@ void segment_ops(HostDevProgram& d, const std::vector<uint32_t>& ops, const uint
     }
     Item it{};
     it.kind = IT_SEGMENT;
+    it.shape = kNoShape;
     unsigned la = static_cast<unsigned>(std::countr_zero(set));
     unsigned lb = std::popcount(set) == 2 ? 31u - static_cast<unsigned>(std::countl_zero(set)) : (la == 0 ? 1u : 0u);
     if (k < 2) lb = la;  // degenerate 1-qubit state: per-op fallback in the kernel
@@ -220,6 +223,39 @@ void segment_ops(HostDevProgram& d, const std::vector<uint32_t>& ops, const uint
 }
 
 bool fused_kind(const DevOp& o) { return o.kind == K_GATE || o.kind == K_PAULI; }
+
+// Shape key of a lowered segment: every field of its non-Pauli micro-ops that
+// the straight-line executor bakes in (code, register operands, classes,
+// matrix offsets relative to the segment's first matrix), plus the final
+// register map. Items with equal keys share one generated executor.
+void assign_shape(HostDevProgram& d, Item& it, uint32_t uop_base) {
+  std::string key;
+  uint32_t nfast = 0, mat0 = it.end > it.begin ? d.uops[uop_base + it.begin].mat : 0;
+  char buf[96];
+  for (uint32_t i = it.begin; i < it.end; ++i) {
+    const Uop& u = d.uops[uop_base + i];
+    if (u.code == UC_PAULI) continue;
+    const uint64_t cls = (u.code == UC_GEN1 || u.code == UC_GEN2) ? d.ops[u.ref].cls : 0;
+    std::snprintf(buf, sizeof buf, "%u.%u.%u.%u.%u.%llx.%u;", u.code, u.qb, u.src, u.mcls, u.sigma,
+                  static_cast<unsigned long long>(cls), static_cast<unsigned>(u.mat - mat0));
+    key += buf;
+    ++nfast;
+  }
+  std::snprintf(buf, sizeof buf, "|%u", it.sigma);
+  key += buf;
+  if (nfast > 0xFFFF) throw std::length_error("segment too long");
+  it.nfast = static_cast<uint16_t>(nfast);
+  auto pos = std::find(d.shapes.begin(), d.shapes.end(), key);
+  if (pos == d.shapes.end()) {
+    if (d.shapes.size() >= kNoShape) {
+      it.shape = kNoShape;
+      return;
+    }
+    d.shapes.push_back(key);
+    pos = d.shapes.end() - 1;
+  }
+  it.shape = static_cast<uint16_t>(pos - d.shapes.begin());
+}
 
 // Lowers the pass ops [po_begin, ...) of pass `pd` to micro-ops + a compact
 // matrix table, segment by segment, folding unconditional 2q permutations
@@ -286,7 +322,7 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
           int a = -1, b = -1;
           for (int e = 0; e < 4; ++e)
             if (perm[e] != e) (a < 0 ? a : b) = e;
-          u.qb = static_cast<uint8_t>(sg[a] | (sg[b] << 2));
+          u.qb = static_cast<uint8_t>(std::min(sg[a], sg[b]) | (std::max(sg[a], sg[b]) << 2));  // physical, ascending
         } else if (o.mk == MK_2Q_MONO && n_nonone == 1 && moved == 0) {
           u.code = UC_PHASE;
           for (int r = 0; r < 4; ++r)
@@ -316,6 +352,7 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
     it.begin = ubegin;
     it.end = static_cast<uint32_t>(d.uops.size()) - pd.uop_begin;
     it.sigma = pack(sg);
+    assign_shape(d, it, pd.uop_begin);
   }
   pd.uop_end = static_cast<uint32_t>(d.uops.size());
   pd.mat_count = mat;
@@ -330,6 +367,7 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
 // measure / reset sites end a pass. Inside a pass, ops are grouped into
 // register segments (segment_ops).
 void plan_passes(HostDevProgram& d, unsigned tile_k) {
+  d.shapes.clear();
   d.passes.clear();
   d.items.clear();
   d.pass_ops.clear();
@@ -426,12 +464,94 @@ void plan_resident(HostDevProgram& d) {
     run.clear();
     Item sp{};
     sp.kind = IT_SPECIAL;
+    sp.shape = kNoShape;
     sp.begin = i;
     d.items.push_back(sp);
   }
   segment_ops(d, run, pos, n);
   pd.item_end = static_cast<uint32_t>(d.items.size());
   d.passes.push_back(pd);
+}
+
+namespace {
+
+// Parses one micro-op of a shape key back (see assign_shape).
+struct ShapeOp {
+  unsigned code, qb, src, mcls, sigma, off;
+  unsigned long long cls;
+};
+
+std::vector<ShapeOp> parse_shape(const std::string& key, unsigned* final_sigma) {
+  std::vector<ShapeOp> ops;
+  size_t i = 0;
+  while (i < key.size() && key[i] != '|') {
+    ShapeOp o{};
+    if (std::sscanf(key.c_str() + i, "%u.%u.%u.%u.%u.%llx.%u;", &o.code, &o.qb, &o.src, &o.mcls, &o.sigma, &o.cls,
+                    &o.off) != 7)
+      throw std::logic_error("bad shape key");
+    ops.push_back(o);
+    i = key.find(';', i) + 1;
+  }
+  *final_sigma = static_cast<unsigned>(std::stoul(key.substr(i + 1)));
+  return ops;
+}
+
+}  // namespace
+
+// One straight-line executor per shape: the segment's micro-ops with every
+// operand a compile-time constant (register pairs, relabelings, entry classes,
+// matrix offsets), so the quads stay in registers with no per-op dispatch.
+// Each executor performs exactly the interpreter's arithmetic
+// (run_segment_staged), op for op.
+std::string shape_source(const HostDevProgram& d) {
+  std::string src = "namespace ssb {\n";
+  char buf[512];
+  for (size_t id = 0; id < d.shapes.size(); ++id) {
+    unsigned fs = 0;
+    const std::vector<ShapeOp> ops = parse_shape(d.shapes[id], &fs);
+    std::snprintf(buf, sizeof buf,
+                  "static __device__ __forceinline__ void ssb_shape_%zu(double2* st, unsigned k, unsigned la, "
+                  "unsigned lb, const double2* m) {\n  SSB_SHAPE_BEGIN\n",
+                  id);
+    src += buf;
+    for (const ShapeOp& o : ops) {
+      const unsigned a0 = o.qb & 3, a1 = (o.qb >> 2) & 3, b0 = (o.qb >> 4) & 3, b1 = (o.qb >> 6) & 3;
+      switch (o.code) {
+        case UC_U:
+        case UC_REAL:
+        case UC_GEN1:
+          std::snprintf(buf, sizeof buf,
+                        "  { const double2 mm[4] = {m[%u], m[%u], m[%u], m[%u]}; "
+                        "quad_apply1p<%u, %u, %u, %u, %s, true>(v, mm, 0x%llxull, QPT); }\n",
+                        o.off, o.off + 1, o.off + 2, o.off + 3, a0, a1, b0, b1,
+                        o.code == UC_U ? "MK_1Q_U" : o.code == UC_REAL ? "MK_1Q_REAL" : "MK_1Q_GEN", o.cls);
+          break;
+        case UC_SWAP:
+          std::snprintf(buf, sizeof buf, "  quad_swap<%u, %u>(v, QPT);\n", std::min(a0, a1), std::max(a0, a1));
+          break;
+        case UC_PHASE:
+          std::snprintf(buf, sizeof buf, "  quad_phase<%u>(v, m[%u], %uu, QPT);\n", o.qb & 3, o.off, o.mcls);
+          break;
+        default:  // UC_MONO / UC_GEN2 through the logical view (constant relabeling)
+          std::snprintf(buf, sizeof buf,
+                        "  { Uop u{}; u.code = %u; u.qb = %u; u.src = %u; u.mcls = %u; u.sigma = %u;\n"
+                        "    SSB_SHAPE_LOGICAL(u, m + %u, 0x%llxull) }\n",
+                        o.code, o.qb, o.src, o.mcls, o.sigma, o.off, o.cls);
+          break;
+      }
+      src += buf;
+    }
+    std::snprintf(buf, sizeof buf, "  SSB_SHAPE_END(%u)\n}\n", fs);
+    src += buf;
+  }
+  src += "static __device__ __forceinline__ bool ssb_run_shape(unsigned id, double2* st, unsigned k, unsigned la, "
+         "unsigned lb, const double2* m) {\n  switch (id) {\n";
+  for (size_t id = 0; id < d.shapes.size(); ++id) {
+    std::snprintf(buf, sizeof buf, "    case %zu: ssb_shape_%zu(st, k, la, lb, m); return true;\n", id, id);
+    src += buf;
+  }
+  src += "    default: return false;\n  }\n}\n}  // namespace ssb\n";
+  return src;
 }
 
 }  // namespace ssb

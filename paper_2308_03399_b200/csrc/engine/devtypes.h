@@ -1,0 +1,141 @@
+// Device-side program types (shared by the static kernels and the run-time
+// specialised kernels, so this header has no host-library dependencies).
+#pragma once
+
+#ifdef __CUDACC_RTC__
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+#else
+#include <cstdint>
+#endif
+
+namespace ssb {
+
+enum OpKind : uint8_t { K_GATE = 0, K_PAULI = 1, K_KRAUS = 2, K_MEASURE = 3, K_RESET = 4, K_BARRIER = 5 };
+
+struct alignas(16) DevOp {
+  uint8_t kind;
+  uint8_t nq;
+  uint8_t has_cond;
+  uint8_t skip;        // gate whose matrix is the identity: exact no-op
+  uint8_t q[4];        // qubit operands (qubits[0] = low matrix axis)
+  uint8_t c[4];        // clbits (MEASURE)
+  uint32_t aux;        // GATE: matrix slot; PAULI: first term; KRAUS: channel
+  uint32_t count;      // PAULI: term count; KRAUS: matrix count
+  uint32_t site;       // PAULI: ordinal among Pauli sites (decision table column)
+  uint8_t mk;          // GATE: micro-kind (MicroKind), chosen at plan time
+  uint8_t src;         // MK_2Q_MONO: source column of each row (2 bits per row)
+  uint8_t pad[2];
+  uint64_t cls;        // GATE: entry classes (exact.cuh EntryClass, 3 bits each)
+  uint64_t cond_mask;
+  uint64_t cond_value;
+  uint64_t event;
+};
+static_assert(sizeof(DevOp) == 64, "DevOp layout");
+
+struct alignas(8) DevTerm {
+  double cum;
+  uint32_t x, z;       // qubit masks (n <= 30)
+  uint32_t num_y;
+  uint32_t identity;
+};
+
+struct DevChannel {
+  uint32_t arity, nmat, mat_begin, pad;
+};
+
+// Gate micro-kinds (exact.cuh): which arithmetic template applies the matrix.
+enum MicroKind : uint8_t {
+  MK_1Q_U = 0,     // classes (REAL, GEN, GEN, GEN): the U gate
+  MK_1Q_REAL = 1,  // all four entries real or zero-free real (H)
+  MK_1Q_GEN = 2,   // anything else: per-entry runtime classes
+  MK_2Q_MONO = 3,  // one nonzero per row (CX, SWAP, CP, CZ...): moves + few products
+  MK_2Q_GEN = 4,   // dense 4x4: per-entry runtime classes
+};
+
+// One fused HBM tile pass over the local qubit set `lmask` (|lmask| = k):
+// items [item_begin, item_end); `first` synthesises |0...0> instead of loading
+// the tile. The resident executor uses one pass with k = n whose items also
+// include special ops (Kraus / measure / reset).
+struct PassDesc {
+  uint32_t item_begin, item_end;
+  uint32_t lmask;
+  uint8_t k;
+  uint8_t first;
+  uint8_t pad[2];
+  uint8_t lq[32];      // local position j -> qubit
+  // Streamed passes: micro-op stream [uop_begin, uop_end) (items index it
+  // relative to uop_begin) and its matrix table [mat_begin, mat_begin+mat_count)
+  // (double2 units), staged into shared memory by the tile kernel.
+  uint32_t uop_begin, uop_end;
+  uint32_t mat_begin, mat_count;
+  uint32_t po_begin;   // first pass_op of this pass (per-op fallback, k < 2)
+};
+
+// Micro-op codes of a streamed pass (one per gate / Pauli site).
+// Within a segment, unconditional 2q permutations (CX, SWAP) are folded into a
+// plan-time relabeling sigma of the quad's 4 registers (logical element e
+// lives in register sigma(e)); later micro-ops address physical registers and
+// the segment store writes register sigma(e) to element e's address. sigma
+// is packed 2 bits per element; 0xE4 is the identity.
+enum UopCode : uint8_t {
+  UC_U = 0,        // 1q U pattern          (qb: physical pairs a0|a1<<2|b0<<4|b1<<6)
+  UC_REAL = 1,     // 1q all-real           (qb: physical pairs)
+  UC_GEN1 = 2,     // 1q runtime classes    (qb: physical pairs; cls via ref)
+  UC_MONO = 3,     // 2q monomial           (qb: swapped; src; mcls)
+  UC_GEN2 = 4,     // 2q runtime classes    (qb: swapped; cls via ref)
+  UC_PAULI = 5,    // Pauli site            (qb: quad bits of op qubits, bit b)
+  UC_SWAP = 6,     // conditional 2q transposition (qb: physical e0 | e1 << 2)
+  UC_PHASE = 7,    // 2q diagonal with one non-unit entry (qb: element; mcls:
+                   // its class) — CP
+};
+
+// 16-byte micro-op. After per-shot compaction (identity Pauli draws and
+// failed conditions removed) `pauli` holds xq | zq << 2 | (num_y & 3) << 4.
+struct Uop {
+  uint8_t code;
+  uint8_t qb;
+  uint8_t src;
+  uint8_t flags;       // bit0: conditional
+  uint16_t mat;        // offset into the pass matrix table (double2 units)
+  uint16_t mcls;       // UC_MONO: class of row r's nonzero entry, 3 bits per row
+  uint32_t ref;        // program op index
+  uint8_t pauli;
+  uint8_t sigma;       // UC_PAULI / UC_MONO / UC_GEN2: logical->physical quad map
+  uint8_t pad[2];
+};
+static_assert(sizeof(Uop) == 16, "Uop layout");
+
+// Item: a register segment — consecutive ops [begin,end) of pass_ops acting
+// inside the 2-qubit set {la, lb} (local positions), applied per amplitude
+// quad in registers — or a special op (resident executor only).
+enum ItemKind : uint8_t { IT_SEGMENT = 0, IT_SPECIAL = 1 };
+struct Item {
+  uint8_t kind;
+  uint8_t la, lb;      // local positions, la < lb
+  uint8_t sigma;       // streamed passes: register map at the segment end
+  uint32_t begin, end; // segment: pass_ops range; special: begin = op index
+  // Streamed passes: the segment's "shape" — its micro-op sequence with every
+  // Pauli draw identity and every condition true (the common case per shot) —
+  // as an index into HostDevProgram::shapes (kNoShape: none), and the number
+  // of non-Pauli micro-ops that case executes.
+  uint16_t shape;
+  uint16_t nfast;
+};
+constexpr uint16_t kNoShape = 0xFFFF;
+
+struct PassOp {
+  uint32_t op;         // index into ops
+  uint8_t qb[4];       // quad bit (0 -> la, 1 -> lb) of each op qubit
+};
+
+enum StepKind : uint8_t { S_PASS = 0, S_SPECIAL = 1, S_SAMPLE = 2 };
+struct Step {
+  StepKind kind;
+  uint32_t index;      // pass index, or op index for S_SPECIAL
+};
+
+}  // namespace ssb

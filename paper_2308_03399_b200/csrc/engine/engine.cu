@@ -23,6 +23,9 @@ namespace ssb {
     if (e_ != cudaSuccess) throw CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// specialise.cpp: the shape-specialised tile-pass kernel for a plan, or null.
+const void* specialised_tile_kernel(const HostDevProgram& h);
+
 // Device copy of one program (+ its pass plan for one tile size).
 struct DevProgram {
   HostDevProgram host;  // with passes planned for tile_k
@@ -44,6 +47,7 @@ struct ssb_engine {
   int num_sms = 0;
   size_t smem_optin = 0;
   int* err = nullptr;
+  unsigned long long* guard_hits = nullptr;  // guarded-sampling exact re-decisions
   std::map<std::pair<uint64_t, unsigned>, std::unique_ptr<ssb::DevProgram>> programs;
   std::map<std::string, std::pair<void*, size_t>> scratch;
   uint64_t launches = 0;
@@ -308,9 +312,34 @@ uint64_t apply_op(ssb_engine* E, DevProgram& dp, uint32_t op_index, const SegCtx
   return 0;
 }
 
+// Test hook: SHOTSIM_B200_GUARD_SCALE widens the sampling guard band (e.g.
+// 1e12 sends every shot through the exact sequential re-decision).
+double guard_scale() {
+  const char* v = std::getenv("SHOTSIM_B200_GUARD_SCALE");
+  const double s = v ? std::strtod(v, nullptr) : 1.0;
+  return s >= 1.0 ? s : 1.0;
+}
+
 void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c) {
   const unsigned n = dp.host.n;
   const ProgView& P = dp.view;
+  if (P.nsample == n && n >= 12) {
+    // Parallel guarded sampling (sample_block_kernel / sample_guard_kernel).
+    const uint64_t nb = ((uint64_t{1} << n) + SAMPLE_BLOCK - 1) / SAMPLE_BLOCK;
+    const uint64_t chunk = chunk_for(c.S, nb * (sizeof(double) + sizeof(int32_t)));
+    for (uint64_t off = 0; off < c.S; off += chunk) {
+      const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
+      double* bsum = static_cast<double*>(scratch(E, "bsum", cc.S * nb * sizeof(double)));
+      int32_t* blast = static_cast<int32_t*>(scratch(E, "blast", cc.S * nb * sizeof(int32_t)));
+      sample_block_kernel<<<grid_for(cc.S * nb * 32), NT, 0, E->stream>>>(P, cc.state, cc.S, bsum, blast);
+      launched(E);
+      sample_guard_kernel<<<grid_for(cc.S, 64), 64, 0, E->stream>>>(P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, bsum,
+                                                                    blast, cc.cregs, E->guard_hits, E->err,
+                                                                    guard_scale());
+      launched(E);
+    }
+    return;
+  }
   if (P.nsample == n) {
     g_sample_scan_kernel<<<grid_for(c.S, 128), 128, 0, E->stream>>>(P, c.state, c.S, c.seed, c.ids, c.begin, c.cregs,
                                                                     E->err);
@@ -395,6 +424,7 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
   const RunConfig rc = config_of(opts);
   const unsigned n = prog->dev.n;
   const uint64_t launches0 = E->launches;
+  CK(cudaMemsetAsync(E->guard_hits, 0, sizeof(unsigned long long), E->stream));
   const size_t rsmem = resident_smem(prog->dev);
   KernelTimer timer;
   timer.on = opts && opts->profile;
@@ -436,10 +466,15 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
     uint8_t* psel = dp.num_pauli ? static_cast<uint8_t*>(scratch(E, "psel", wave * dp.num_pauli)) : nullptr;
     size_t tsmem = 0;
     for (const PassDesc& pd : h.passes)
-      tsmem = std::max(tsmem, tile_smem_bytes(pd.k, pd.uop_end - pd.uop_begin, pd.mat_count));
-    CK(cudaFuncSetAttribute(tile_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)));
+      tsmem = std::max<size_t>(tsmem, tile_smem_bytes(pd.k, pd.uop_end - pd.uop_begin, pd.mat_count));
+    // The shape-specialised build of the same kernel (specialise.cpp) when
+    // available, else the static interpreter build.
+    const void* kfn = (opts && opts->interpret_only) ? nullptr : specialised_tile_kernel(h);
+    const bool specialised = kfn != nullptr;
+    if (!kfn) kfn = reinterpret_cast<const void*>(tile_pass_kernel);
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_pass_kernel, NT, tsmem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, tsmem));
     uint64_t waves = 0, fused = 0;
     for (uint64_t w0 = 0; w0 < count; w0 += wave) {
       const uint64_t S = std::min(wave, count - w0);
@@ -455,9 +490,12 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       for (const Step& st : h.steps) {
         if (st.kind == S_PASS) {
           timer.begin(0);
-          const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(S, uint64_t(std::max(per_sm, 1)) * E->num_sms));
-          tile_pass_kernel<<<grid, NT, tsmem, E->stream>>>(dp.view, st.index, state, S, c.cregs, psel,
-                                                           dp.num_pauli);
+          const unsigned grid =
+              static_cast<unsigned>(std::min<uint64_t>(S * tiles, uint64_t(std::max(per_sm, 1)) * E->num_sms));
+          uint32_t pass_index = st.index, num_pauli = dp.num_pauli;
+          uint64_t* cregs = c.cregs;
+          void* args[] = {&dp.view, &pass_index, &state, const_cast<uint64_t*>(&S), &cregs, &psel, &num_pauli};
+          CK(cudaLaunchKernel(kfn, dim3(grid), dim3(NT), args, tsmem, E->stream));
           launched(E);
           timer.end(0);
           ++fused;
@@ -476,9 +514,16 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       stats->peak_states = std::min(wave, count);
       stats->passes = waves;
       stats->fused_passes = fused;
+      stats->specialised_shapes = specialised ? h.shapes.size() : 0;
     }
   }
-  if (stats) stats->dispatch_count = E->launches - launches0;
+  if (stats) {
+    stats->dispatch_count = E->launches - launches0;
+    unsigned long long hits = 0;
+    CK(cudaMemcpyAsync(&hits, E->guard_hits, sizeof hits, cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    stats->sampling_guard_hits = hits;
+  }
   timer.collect(stats);
 }
 
@@ -518,6 +563,8 @@ SSB_API int ssb_engine_create(int device, ssb_engine** out) {
     CK(cudaEventCreate(&E->ev1));
     CK(cudaMalloc(&E->err, sizeof(int)));
     CK(cudaMemset(E->err, 0, sizeof(int)));
+    CK(cudaMalloc(&E->guard_hits, sizeof(unsigned long long)));
+    CK(cudaMemset(E->guard_hits, 0, sizeof(unsigned long long)));
     *out = E.release();
   });
 }
@@ -529,6 +576,7 @@ SSB_API void ssb_engine_destroy(ssb_engine* E) {
   E->programs.clear();
   for (auto& [name, slot] : E->scratch) cudaFree(slot.first);
   cudaFree(E->err);
+  cudaFree(E->guard_hits);
   cudaEventDestroy(E->ev0);
   cudaEventDestroy(E->ev1);
   cudaStreamDestroy(E->stream);
@@ -604,6 +652,32 @@ SSB_API int ssb_histogram_device(ssb_engine* E, const uint64_t* values_device, u
     g_histogram_kernel<<<grid_for(count), NT, 0, E->stream>>>(values_device, count, num_clbits,
                                                               reinterpret_cast<unsigned long long*>(hist_device));
     launched(E);
+  });
+}
+
+SSB_API int ssb_fp64_peak(ssb_engine* E, double* ops_per_second) {
+  return guard([&] {
+    if (!E || !ops_per_second) throw std::invalid_argument("null argument");
+    DeviceGuard g(E->device);
+    constexpr int kThreads = 256, kIters = 4096;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fp64_probe_kernel<kIters>, kThreads, 0));
+    const unsigned grid = static_cast<unsigned>(std::max(per_sm, 1) * E->num_sms * 4);
+    double* sink = static_cast<double*>(scratch(E, "fp64_sink", sizeof(double)));
+    fp64_probe_kernel<kIters><<<grid, kThreads, 0, E->stream>>>(sink, 1.0000001, 1e-9);  // warm-up
+    launched(E);
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+      CK(cudaEventRecord(E->ev0, E->stream));
+      fp64_probe_kernel<kIters><<<grid, kThreads, 0, E->stream>>>(sink, 1.0000001, 1e-9);
+      launched(E);
+      CK(cudaEventRecord(E->ev1, E->stream));
+      CK(cudaEventSynchronize(E->ev1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, E->ev0, E->ev1));
+      best = std::min(best, ms);
+    }
+    *ops_per_second = double(grid) * kThreads * kIters * fp64_probe_ops_per_iter() / (best * 1e-3);
   });
 }
 

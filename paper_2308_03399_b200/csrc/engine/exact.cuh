@@ -14,7 +14,9 @@
 // probability or decision (signed zeros square to +0).
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 #ifdef __CUDACC__
 #define SSB_HD __host__ __device__

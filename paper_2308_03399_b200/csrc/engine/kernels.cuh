@@ -15,46 +15,9 @@
 //                      streamed executor and for the operator-level C ABI.
 #pragma once
 
-#include "segment.cuh"
+#include "tile_pass.cuh"
 
 namespace ssb {
-
-enum DevError : int { DEV_OK = 0, DEV_DEGENERATE = 1 };
-
-// What the executors need from an engine (stream, device error flag, launch
-// counter).
-struct EngineView {
-  cudaStream_t stream;
-  int* err;
-  uint64_t* launches;
-};
-
-struct ProgView {
-  const DevOp* ops;
-  const DevTerm* terms;
-  const DevChannel* channels;
-  const double2* mats;        // 16 double2 per slot
-  const uint64_t* scaled_cls; // per slot
-  const uint8_t* sample_qubits;
-  const uint8_t* write_clbit;
-  const uint8_t* write_pos;
-  const PassDesc* passes;
-  const Item* items;
-  const PassOp* pass_ops;
-  const Uop* uops;
-  const double2* uop_mats;
-  const uint32_t* pauli_site_ops;  // site ordinal -> op index
-  uint32_t num_pauli;
-  uint32_t n, end, nsample, nwrites;
-  uint64_t num_events;
-  uint32_t eligible, sample_identity;
-};
-
-__device__ __forceinline__ void raise(int* err, int code) { atomicCAS(err, 0, code); }
-
-__device__ __forceinline__ uint64_t shot_of(const uint64_t* ids, uint64_t begin, uint64_t s) {
-  return ids ? ids[s] : begin + s;
-}
 
 __device__ __forceinline__ uint64_t apply_sample_outcome(const ProgView& P, uint64_t creg, uint64_t outcome) {
   for (uint32_t i = 0; i < P.nwrites; ++i) {
@@ -228,117 +191,8 @@ static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint
   }
 }
 
-// ---------------------------------------------------------------------------
-// Streamed executor: fused tile pass. Grid: S * 2^(n-k) CTAs; CTA (s, t) owns
-// tile t of shot s: local index l <-> global index pdep(t, ~lmask) | pdep(l, lmask).
-__device__ __forceinline__ uint64_t pdep_positions(uint64_t v, const uint8_t* pos, unsigned k) {
-  uint64_t out = 0;
-  for (unsigned j = 0; j < k; ++j) out |= ((v >> j) & 1) << pos[j];
-  return out;
-}
-
-// Shared-memory layout of tile_pass_kernel: tile | matrix table | uops |
-// compacted uops | prefix (u16, one per uop + 1).
-__host__ __device__ inline size_t tile_smem_bytes(unsigned k, uint32_t nuops, uint32_t nmats) {
-  return (size_t{1} << k) * 16 + size_t{nmats} * 16 + size_t{nuops} * 32 + (size_t{nuops} + 1) * 2 + 16;
-}
-
-// Persistent: each CTA owns a contiguous range of shots and sweeps all tiles
-// of each shot, so the pass's micro-op stream is staged once per CTA and
-// compacted once per shot.
-static __global__ void __launch_bounds__(NT, SSB_TILE_MINB) tile_pass_kernel(ProgView P, uint32_t pass_index, double2* state,
-                                                                 uint64_t S, const uint64_t* cregs,
-                                                                 const uint8_t* pauli_sel, uint32_t num_pauli) {
-  extern __shared__ double2 tile[];
-  const PassDesc& pd = P.passes[pass_index];
-  const unsigned n = P.n, k = pd.k;
-  const uint64_t tiles = uint64_t{1} << (n - k), L = uint64_t{1} << k;
-  const uint32_t nu = pd.uop_end - pd.uop_begin;
-  double2* smats = tile + L;
-  Uop* uops = reinterpret_cast<Uop*>(smats + pd.mat_count);
-  Uop* eops = uops + nu;
-  uint16_t* pre = reinterpret_cast<uint16_t*>(eops + nu);
-  __shared__ uint8_t hpos[32];
-
-  for (uint32_t i = threadIdx.x; i < pd.mat_count; i += NT) smats[i] = P.uop_mats[pd.mat_begin + i];
-  for (uint32_t i = threadIdx.x; i < nu; i += NT) uops[i] = P.uops[pd.uop_begin + i];
-  if (threadIdx.x == 0)
-    for (unsigned q = 0, j = 0; q < n; ++q)
-      if (!((pd.lmask >> q) & 1)) hpos[j++] = static_cast<uint8_t>(q);
-  __syncthreads();
-
-  const unsigned kt = k < 8 ? k : 8;
-  const uint64_t lo_part = pdep_positions(threadIdx.x, pd.lq, kt);
-  const uint64_t s_begin = S * blockIdx.x / gridDim.x, s_end = S * (blockIdx.x + 1) / gridDim.x;
-  for (uint64_t s = s_begin; s < s_end; ++s) {
-    // Per-shot compaction (warp 0, in order): drop failed conditions and
-    // identity Pauli draws; resolve each Pauli to quad masks.
-    if (threadIdx.x < 32) {
-      const uint64_t creg = cregs ? cregs[s] : 0;
-      const uint8_t* sel = pauli_sel + s * num_pauli;
-      uint32_t count = 0;
-      for (uint32_t c0 = 0; c0 < nu; c0 += 32) {
-        const uint32_t i = c0 + threadIdx.x;
-        bool keep = false;
-        Uop u{};
-        if (i < nu) {
-          u = uops[i];
-          keep = true;
-          const DevOp& op = P.ops[u.ref];
-          if ((u.flags & 1) && (creg & op.cond_mask) != op.cond_value) keep = false;
-          if (keep && u.code == UC_PAULI) {
-            const DevTerm tm = P.terms[op.aux + sel[op.site]];
-            if (tm.identity) {
-              keep = false;
-            } else {
-              uint32_t xq = 0, zq = 0;
-              for (unsigned b = 0; b < op.nq; ++b) {
-                const uint32_t qb = (u.qb >> b) & 1u;
-                xq |= ((tm.x >> op.q[b]) & 1u) << qb;
-                zq |= ((tm.z >> op.q[b]) & 1u) << qb;
-              }
-              u.pauli = static_cast<uint8_t>(xq | (zq << 2) | ((tm.num_y & 3u) << 4));
-            }
-          }
-        }
-        const unsigned ballot = __ballot_sync(0xffffffffu, keep);
-        const uint32_t at = count + __popc(ballot & ((1u << threadIdx.x) - 1));
-        if (i < nu) pre[i] = static_cast<uint16_t>(at);
-        if (keep) eops[at] = u;
-        count += __popc(ballot);
-      }
-      if (threadIdx.x == 0) pre[nu] = static_cast<uint16_t>(count);
-    }
-    __syncthreads();
-    double2* seg = state + (s << n);
-    for (uint64_t t = 0; t < tiles; ++t) {
-      const uint64_t base = pdep_positions(t, hpos, n - k);
-      if (pd.first) {
-        for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) {
-          const uint64_t g = base | lo_part | pdep_positions(i, pd.lq + kt, k - kt);
-          tile[l] = make_double2(g == 0 ? 1.0 : 0.0, 0.0);
-        }
-      } else {
-        for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
-          tile[l] = seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)];
-      }
-      __syncthreads();
-      for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
-        const Item it = P.items[it_i];
-        const uint32_t b = pre[it.begin], e = pre[it.end];
-        if (b == e && it.sigma == 0xE4) continue;  // nothing to apply and no relabeling to store
-        if (k < 2) {
-          run_ops_per_op(tile, k, it.begin, it.end, P.pass_ops + pd.po_begin, P.ops, P.mats, P.terms,
-                         cregs ? cregs[s] : 0, pauli_sel + s * num_pauli);
-        } else {
-          run_segment_staged(tile, k, it, eops, b, e, smats, P.ops);
-        }
-      }
-      for (uint64_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
-        seg[base | lo_part | pdep_positions(i, pd.lq + kt, k - kt)] = tile[l];
-    }
-    __syncthreads();  // compaction of the next shot rewrites eops/pre
-  }
+static __global__ void __launch_bounds__(NT, SSB_TILE_MINB) tile_pass_kernel(SSB_TILE_PASS_PARAMS) {
+  tile_pass_body(P, pass_index, state, S, cregs, pauli_sel, num_pauli);
 }
 
 // Per-(shot, Pauli site) term choice for a wave: sel[s][site] (u8).
@@ -659,6 +513,97 @@ static __global__ void g_sample_scan_kernel(ProgView P, const double2* st, uint6
   cregs[s] = apply_sample_outcome(P, cregs[s], o);
 }
 
+// Terminal sampling with every qubit sampled, parallel and still exact
+// (statevector.cpp:142-164 + 185-197 with groups = 1: p_m = |a[idx(m)]|^2, then
+// the first m with u < the SEQUENTIAL cumulative S_m).
+//
+// Phase 1 (sample_block_kernel): one warp per (shot, block of SAMPLE_BLOCK
+// outcomes) sums the block's p_m in any order and records its last nonzero
+// outcome. Phase 2 (sample_guard_kernel): one thread per shot accumulates
+// block sums to the block before u, then walks outcomes with its own
+// sequential cumulative C_m. Every C_m and the reference's S_m are fl sums of
+// the same non-negative terms, so |S_m - C_m| <= Delta = (2*2^n + blocks +
+// 2*SAMPLE_BLOCK + 64) * 2^-52 * total (Higham's bound for recursive
+// summation, with slack). If the first m with C_m > u - Delta is also the first
+// with C_m > u + Delta, it is exactly the reference's pick; otherwise (|u -
+// boundary| < Delta, probability ~1e-9 per shot at n = 24) the shot is
+// re-decided by the exact single-thread sequential scan (scan_full) on device
+// and counted in `guard_hits`.
+constexpr uint32_t SAMPLE_BLOCK = 1024;
+
+static __global__ void sample_block_kernel(ProgView P, const double2* st, uint64_t S, double* bsum, int32_t* blast) {
+  const unsigned n = P.n;
+  const uint64_t nb = ((uint64_t{1} << n) + SAMPLE_BLOCK - 1) / SAMPLE_BLOCK;
+  const uint64_t warp = (uint64_t{blockIdx.x} * blockDim.x + threadIdx.x) / 32;
+  const unsigned lane = threadIdx.x & 31;
+  if (warp >= S * nb) return;
+  const uint64_t s = warp / nb, j = warp % nb;
+  const double2* a = st + (s << n);
+  const uint64_t m0 = j * SAMPLE_BLOCK, m1 = min(m0 + SAMPLE_BLOCK, uint64_t{1} << n);
+  double acc = 0.0;
+  int32_t last = -1;
+  for (uint64_t m = m0 + lane; m < m1; m += 32) {
+    const double p = c_norm(a[P.sample_identity ? m : scatter_bits(m, P.sample_qubits, n)]);
+    acc = __dadd_rn(acc, p);
+    if (p > 0.0) last = static_cast<int32_t>(m - m0);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off /= 2) {
+    acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, off));
+    last = max(last, __shfl_down_sync(0xffffffffu, last, off));
+  }
+  if (lane == 0) {
+    bsum[warp] = acc;
+    blast[warp] = last;
+  }
+}
+
+static __global__ void sample_guard_kernel(ProgView P, const double2* st, uint64_t S, uint64_t seed,
+                                           const uint64_t* ids, uint64_t begin, const double* bsum,
+                                           const int32_t* blast, uint64_t* cregs, unsigned long long* guard_hits,
+                                           int* err, double delta_scale) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const unsigned n = P.n;
+  const uint64_t A = uint64_t{1} << n, nb = (A + SAMPLE_BLOCK - 1) / SAMPLE_BLOCK;
+  const double2* a = st + (s << n);
+  const double* B = bsum + s * nb;
+  const int32_t* Z = blast + s * nb;
+  const double u = keyed_uniform(seed, shot_of(ids, begin, s), P.num_events);
+  auto amp = [&](uint64_t m) { return a[P.sample_identity ? m : scatter_bits(m, P.sample_qubits, n)]; };
+  double tot = 0.0;
+  int64_t last_nz = -1;
+  for (uint64_t j = 0; j < nb; ++j) {
+    tot = __dadd_rn(tot, B[j]);
+    if (Z[j] >= 0) last_nz = static_cast<int64_t>(j * SAMPLE_BLOCK + Z[j]);
+  }
+  const double delta = (2.0 * double(A) + double(nb) + 2.0 * SAMPLE_BLOCK + 64.0) * 0x1p-52 * (tot * 1.0001) * delta_scale;
+  // Skip whole blocks that end at or below u - 2 Delta.
+  double c = 0.0;
+  uint64_t j = 0;
+  while (j < nb && __dadd_rn(c, B[j]) <= u - 2.0 * delta) c = __dadd_rn(c, B[j++]);
+  int64_t hi = -1, lo = -1;
+  for (uint64_t m = j * SAMPLE_BLOCK; m < A && lo < 0; ++m) {
+    c = __dadd_rn(c, c_norm(amp(m)));
+    if (hi < 0 && c > u - delta) hi = static_cast<int64_t>(m);
+    if (c > u + delta) lo = static_cast<int64_t>(m);
+  }
+  uint64_t o = 0;
+  bool ok = true;
+  if (lo >= 0 && lo == hi) {
+    o = static_cast<uint64_t>(lo);
+  } else if (lo < 0 && hi < 0) {
+    // No crossing anywhere (C_last <= u - Delta): the last outcome with p > 0.
+    ok = last_nz >= 0;
+    o = ok ? static_cast<uint64_t>(last_nz) : 0;
+  } else {
+    atomicAdd(guard_hits, 1ull);
+    ok = scan_full(amp, A, true, nullptr, 0, u, &o);
+  }
+  if (!ok) raise(err, DEV_DEGENERATE);
+  cregs[s] = apply_sample_outcome(P, cregs[s], o);
+}
+
 // Terminal sampling over k < n qubits: pick over precomputed probabilities.
 static __global__ void g_sample_pick_kernel(ProgView P, const double* val, uint64_t S, uint64_t seed, const uint64_t* ids,
                                      uint64_t begin, uint64_t* cregs, int* err) {
@@ -678,6 +623,24 @@ static __global__ void g_init_kernel(double2* st, uint64_t S, unsigned n, uint64
     st[idx] = make_double2((idx & ((uint64_t{1} << n) - 1)) == 0 ? 1.0 : 0.0, 0.0);
     if ((idx & ((uint64_t{1} << n) - 1)) == 0 && cregs) cregs[idx >> n] = 0;
   }
+}
+
+// FP64-pipe probe: 8 independent DMUL/DADD chains per thread (16 rounded ops
+// per iteration, no FMA — the engine's instruction mix without its overhead).
+__host__ __device__ constexpr int fp64_probe_ops_per_iter() { return 16; }
+template <int ITERS>
+static __global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x[j] = 1.0 + 1e-3 * (threadIdx.x + j);
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = __dadd_rn(__dmul_rn(x[j], a), b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s = __dadd_rn(s, x[j]);
+  if (s == 12345.678) *sink = s;  // keep the chains alive
 }
 
 static __global__ void g_histogram_kernel(const uint64_t* values, uint64_t count, uint32_t bits, unsigned long long* hist) {

@@ -327,14 +327,13 @@ struct Quad4 {
   double2 e[4];
 };
 
-// Rare micro-ops on one quad through its logical view (kept out of line so
-// the hot path's register allocation is unaffected).
-static __device__ __noinline__ Quad4 generic_quad_op(Quad4 x, Uop u, const double2* m, const DevOp* ops) {
+// A non-U micro-op on one quad through its logical view (gcls: the gate's
+// entry classes for UC_GEN1 / UC_GEN2).
+static __device__ __forceinline__ Quad4 logical_quad_op(Quad4 x, Uop u, const double2* m, uint64_t gcls) {
   double2 L[4];
   double2 v[4] = {x.e[0], x.e[1], x.e[2], x.e[3]};
   gather_logical(v, u.sigma, L);
   double2 one[1][4] = {{L[0], L[1], L[2], L[3]}};
-  const uint64_t gcls = (u.code == UC_GEN1 || u.code == UC_GEN2) ? ops[u.ref].cls : 0;
   switch (u.code) {
     case UC_U:
     case UC_REAL:
@@ -369,6 +368,26 @@ static __device__ __noinline__ Quad4 generic_quad_op(Quad4 x, Uop u, const doubl
   return Quad4{{v[0], v[1], v[2], v[3]}};
 }
 
+// Out-of-line form for the interpreter's rare path.
+static __device__ __noinline__ Quad4 generic_quad_op(Quad4 x, Uop u, const double2* m, const DevOp* ops) {
+  const uint64_t gcls = (u.code == UC_GEN1 || u.code == UC_GEN2) ? ops[u.ref].cls : 0;
+  return logical_quad_op(x, u, m, gcls);
+}
+
+// Rare micro-op on one quad that lives in shared memory at its logical
+// addresses (base, +dla, +dlb, +both). Out of line and register-free at the
+// call site: the hot loop's quad registers are dead across the call (spilled
+// to their own tile addresses first), so its register allocation never has to
+// meet the call ABI.
+static __device__ __noinline__ void rare_quad_op_smem(double2* st, uint64_t base, uint64_t dla, uint64_t dlb, Uop u,
+                                                      const double2* m, const DevOp* ops) {
+  double2* a[4] = {st + base, st + (base | dla), st + (base | dlb), st + (base | dla | dlb)};
+  Quad4 x{{*a[0], *a[1], *a[2], *a[3]}};
+  u.sigma = 0xE4;  // operate on the logical view directly
+  x = generic_quad_op(x, u, m, ops);
+  for (int e = 0; e < 4; ++e) *a[e] = x.e[e];
+}
+
 template <bool FULL>
 static __device__ __forceinline__ void run_segment_staged_t(double2* st, unsigned k, const Item& it, const Uop* eops,
                                                             uint32_t begin, uint32_t end, const double2* smats,
@@ -394,56 +413,68 @@ static __device__ __forceinline__ void run_segment_staged_t(double2* st, unsigne
         v[q][3] = st[base[q] | dla | dlb];
       }
     }
-    for (uint32_t i = begin; i < end; ++i) {
-      const Uop u = eops[i];
-      const double2* m = smats + u.mat;
-      if (FULL && u.code == UC_U) {
-        // Hot path (QV: 8 of 11 block ops): compile-time register pairs for
-        // the relabelings a CX / SWAP run produces; anything else below.
+    uint32_t i = begin;
+    while (i < end) {
+      // Hot inner loop: consecutive 1q U micro-ops on the six register-pair
+      // layouts a CX / SWAP relabeling produces (QV: 8 of 11 block ops). It
+      // has a single loop-carried path, so the quad registers stay put.
+      for (; i < end; ++i) {
+        const Uop u = eops[i];
+        if (u.code != UC_U) break;
+        const double2* m = smats + u.mat;
         const double2 mm[4] = {m[0], m[1], m[2], m[3]};
-        bool done = true;
+        bool hit = true;
 #define SSB_P1(a0, a1, b0, b1) \
-  case (a0 | (a1 << 2) | (b0 << 4) | (b1 << 6)): quad_apply1p<a0, a1, b0, b1, MK_1Q_U, true>(v, mm, 0, nq); break;
+  case (a0 | (a1 << 2) | (b0 << 4) | (b1 << 6)): quad_apply1p<a0, a1, b0, b1, MK_1Q_U, FULL>(v, mm, 0, nq); break;
         switch (u.qb) {
           SSB_P1(0, 1, 2, 3) SSB_P1(0, 2, 1, 3) SSB_P1(0, 3, 2, 1) SSB_P1(0, 2, 3, 1) SSB_P1(0, 1, 3, 2)
           SSB_P1(0, 3, 1, 2)
-          default: done = false; break;
+          default: hit = false; break;
         }
 #undef SSB_P1
-        if (done) continue;
+        if (!hit) break;
       }
-      switch (u.code) {
-        case UC_SWAP:
-          switch (u.qb) {
-            case 0 | (1 << 2): quad_swap<0, 1>(v, nq); break;
-            case 0 | (2 << 2): quad_swap<0, 2>(v, nq); break;
-            case 0 | (3 << 2): quad_swap<0, 3>(v, nq); break;
-            case 1 | (2 << 2): quad_swap<1, 2>(v, nq); break;
-            case 1 | (3 << 2): quad_swap<1, 3>(v, nq); break;
-            default: quad_swap<2, 3>(v, nq); break;
-          }
-          break;
-        case UC_PHASE: {
-          const double2 ph = m[0];
-          switch (u.qb) {
-            case 0: quad_phase<0>(v, ph, u.mcls, nq); break;
-            case 1: quad_phase<1>(v, ph, u.mcls, nq); break;
-            case 2: quad_phase<2>(v, ph, u.mcls, nq); break;
-            default: quad_phase<3>(v, ph, u.mcls, nq); break;
-          }
-          break;
+      if (i >= end) break;
+      const Uop u = eops[i++];
+      const double2* m = smats + u.mat;
+      if (u.code == UC_SWAP) {
+        switch (u.qb) {
+          case 0 | (1 << 2): quad_swap<0, 1>(v, nq); break;
+          case 0 | (2 << 2): quad_swap<0, 2>(v, nq); break;
+          case 0 | (3 << 2): quad_swap<0, 3>(v, nq); break;
+          case 1 | (2 << 2): quad_swap<1, 2>(v, nq); break;
+          case 1 | (3 << 2): quad_swap<1, 3>(v, nq); break;
+          default: quad_swap<2, 3>(v, nq); break;
         }
-        default: {  // everything else through the logical view of each quad (rare)
-#pragma unroll
-          for (int q = 0; q < QPT; ++q) {
-            if (!FULL && q >= nq) break;
-            Quad4 x{{v[q][0], v[q][1], v[q][2], v[q][3]}};
-            x = generic_quad_op(x, u, m, ops);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) v[q][e] = x.e[e];
-          }
-          break;
+        continue;
+      }
+      if (u.code == UC_PHASE) {
+        const double2 ph = m[0];
+        switch (u.qb) {
+          case 0: quad_phase<0>(v, ph, u.mcls, nq); break;
+          case 1: quad_phase<1>(v, ph, u.mcls, nq); break;
+          case 2: quad_phase<2>(v, ph, u.mcls, nq); break;
+          default: quad_phase<3>(v, ph, u.mcls, nq); break;
         }
+        continue;
+      }
+      // Everything else (rare): each quad goes through shared memory at its
+      // logical addresses, is transformed out of line, and is reloaded.
+#pragma unroll
+      for (int q = 0; q < QPT; ++q) {
+        if (!FULL && q >= nq) break;
+        double2 L[4];
+        gather_logical(v[q], u.sigma, L);
+        st[base[q]] = L[0];
+        st[base[q] | dla] = L[1];
+        st[base[q] | dlb] = L[2];
+        st[base[q] | dla | dlb] = L[3];
+        rare_quad_op_smem(st, base[q], dla, dlb, u, m, ops);
+        L[0] = st[base[q]];
+        L[1] = st[base[q] | dla];
+        L[2] = st[base[q] | dlb];
+        L[3] = st[base[q] | dla | dlb];
+        scatter_logical(v[q], u.sigma, L);
       }
     }
     const uint8_t sg = it.sigma;

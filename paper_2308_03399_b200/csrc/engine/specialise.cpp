@@ -1,0 +1,116 @@
+// Run-time shape specialisation of the HBM tile pass.
+//
+// plan_passes() names every distinct segment "shape" of a streamed plan (the
+// segment's micro-op sequence when all its Pauli draws are identity and all
+// conditions hold — per shot the common case); shape_source() emits one
+// straight-line executor per shape. Here that source is compiled with NVRTC
+// for sm_100a together with the engine's device headers (embedded at build
+// time) into a specialised tile_pass_kernel, cached per distinct shape set for
+// the life of the process. The specialised kernel runs the exact same
+// arithmetic; segments whose shot drew a non-identity Pauli (or failed a
+// condition) still go through the interpreter inside it. If NVRTC is missing
+// or fails, the caller falls back to the static interpreter kernel (still on
+// the GPU; there is no CPU path).
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "devprog.hpp"
+
+namespace ssb {
+
+extern const int kJitHeaderCount;
+extern const char* const kJitHeaderNames[];
+extern const char* const kJitHeaderTexts[];
+
+namespace {
+
+#ifndef SSB_QPT
+#define SSB_QPT 2
+#endif
+#ifndef SSB_TILE_MINB
+#define SSB_TILE_MINB 2
+#endif
+#define SSB_STR2(x) #x
+#define SSB_STR(x) SSB_STR2(x)
+
+const char* kMain =
+    "#include \"tile_pass.cuh\"\n"
+    "extern \"C\" __global__ void __launch_bounds__(ssb::NT, SSB_TILE_MINB)\n"
+    "ssb_tile_pass_jit(SSB_TILE_PASS_PARAMS) {\n"
+    "  ssb::tile_pass_body(P, pass_index, state, S, cregs, pauli_sel, num_pauli);\n"
+    "}\n";
+
+struct Entry {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kernel = nullptr;
+};
+
+std::mutex g_mu;
+std::map<std::string, Entry> g_cache;  // shape source -> kernel (nullptr: failed)
+bool g_warned = false;
+
+void warn(const std::string& what) {
+  if (g_warned) return;
+  g_warned = true;
+  std::fprintf(stderr, "shotsim_b200: shape specialisation unavailable (%s); using the interpreter kernel\n",
+               what.c_str());
+}
+
+Entry compile(const std::string& shapes) {
+  Entry e;
+  std::vector<const char*> names(kJitHeaderNames, kJitHeaderNames + kJitHeaderCount);
+  std::vector<const char*> texts(kJitHeaderTexts, kJitHeaderTexts + kJitHeaderCount);
+  names.push_back("ssb_shapes.inc");
+  texts.push_back(shapes.c_str());
+  nvrtcProgram prog = nullptr;
+  if (nvrtcCreateProgram(&prog, kMain, "ssb_tile_pass_jit.cu", static_cast<int>(names.size()), texts.data(),
+                         names.data()) != NVRTC_SUCCESS) {
+    warn("nvrtcCreateProgram failed");
+    return e;
+  }
+  const char* opts[] = {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES",
+                        "-DSSB_QPT=" SSB_STR(SSB_QPT), "-DSSB_TILE_MINB=" SSB_STR(SSB_TILE_MINB)};
+  const nvrtcResult r = nvrtcCompileProgram(prog, static_cast<int>(sizeof opts / sizeof opts[0]), opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, log.data());
+    warn(std::string(nvrtcGetErrorString(r)) + ": " + log.substr(0, 2000));
+    nvrtcDestroyProgram(&prog);
+    return e;
+  }
+  size_t size = 0;
+  nvrtcGetCUBINSize(prog, &size);
+  std::vector<char> cubin(size);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  if (cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+      cudaLibraryGetKernel(&e.kernel, e.lib, "ssb_tile_pass_jit") != cudaSuccess) {
+    cudaGetLastError();
+    warn("loading the specialised cubin failed");
+    e = Entry{};
+  }
+  return e;
+}
+
+}  // namespace
+
+const void* specialised_tile_kernel(const HostDevProgram& h) {
+  if (h.shapes.empty()) return nullptr;
+  if (const char* off = std::getenv("SHOTSIM_B200_NO_SPECIALISE"); off && *off && *off != '0') return nullptr;
+  const std::string src = shape_source(h);
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto it = g_cache.find(src);
+  if (it == g_cache.end()) it = g_cache.emplace(src, compile(src)).first;
+  return reinterpret_cast<const void*>(it->second.kernel);
+}
+
+}  // namespace ssb

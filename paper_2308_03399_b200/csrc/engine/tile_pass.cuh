@@ -1,0 +1,191 @@
+// The HBM-streamed executor's fused tile pass (shared by the static kernel in
+// kernels.cuh and the run-time shape-specialised kernel, specialise.cu).
+#pragma once
+
+#include "shapes.cuh"
+
+namespace ssb {
+
+enum DevError : int { DEV_OK = 0, DEV_DEGENERATE = 1 };
+
+// What the executors need from an engine (stream, device error flag, launch
+// counter).
+struct EngineView {
+  cudaStream_t stream;
+  int* err;
+  uint64_t* launches;
+};
+
+struct ProgView {
+  const DevOp* ops;
+  const DevTerm* terms;
+  const DevChannel* channels;
+  const double2* mats;        // 16 double2 per slot
+  const uint64_t* scaled_cls; // per slot
+  const uint8_t* sample_qubits;
+  const uint8_t* write_clbit;
+  const uint8_t* write_pos;
+  const PassDesc* passes;
+  const Item* items;
+  const PassOp* pass_ops;
+  const Uop* uops;
+  const double2* uop_mats;
+  const uint32_t* pauli_site_ops;  // site ordinal -> op index
+  uint32_t num_pauli;
+  uint32_t n, end, nsample, nwrites;
+  uint64_t num_events;
+  uint32_t eligible, sample_identity;
+};
+
+__device__ __forceinline__ void raise(int* err, int code) { atomicCAS(err, 0, code); }
+
+__device__ __forceinline__ uint64_t shot_of(const uint64_t* ids, uint64_t begin, uint64_t s) {
+  return ids ? ids[s] : begin + s;
+}
+
+// ---------------------------------------------------------------------------
+// Streamed executor: fused tile pass. Grid: S * 2^(n-k) CTAs; CTA (s, t) owns
+// tile t of shot s: local index l <-> global index pdep(t, ~lmask) | pdep(l, lmask).
+__device__ __forceinline__ uint64_t pdep_positions(uint64_t v, const uint8_t* pos, unsigned k) {
+  uint64_t out = 0;
+  for (unsigned j = 0; j < k; ++j) out |= ((v >> j) & 1) << pos[j];
+  return out;
+}
+
+// Shared-memory layout of the tile pass: tile | matrix table | uops |
+// compacted uops | kept-uop prefix (u16, nu + 1) | kept-Pauli prefix (u16,
+// nu + 1) | high-part tile offsets (u32, 2^(k - 8)).
+__host__ __device__ inline uint64_t tile_smem_bytes(unsigned k, uint32_t nuops, uint32_t nmats) {
+  const unsigned kt = k < 8 ? k : 8;
+  return (uint64_t{1} << k) * 16 + uint64_t{nmats} * 16 + uint64_t{nuops} * 32 + (uint64_t{nuops} + 1) * 4 + 16 +
+         (uint64_t{1} << (k - kt)) * 4;
+}
+
+// Persistent: each CTA owns a contiguous range of (shot, tile) units, stages
+// the pass's micro-op stream once, and compacts it once per shot it touches.
+static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_t pass_index, double2* state, uint64_t S,
+                                                      const uint64_t* cregs, const uint8_t* pauli_sel,
+                                                      uint32_t num_pauli) {
+  extern __shared__ double2 tile[];
+  const PassDesc& pd = P.passes[pass_index];
+  const unsigned n = P.n, k = pd.k;
+  const unsigned kt = k < 8 ? k : 8;
+  const uint64_t tiles = uint64_t{1} << (n - k);
+  const uint32_t L = 1u << k;
+  const uint32_t nu = pd.uop_end - pd.uop_begin;
+  double2* smats = tile + L;
+  Uop* uops = reinterpret_cast<Uop*>(smats + pd.mat_count);
+  Uop* eops = uops + nu;
+  uint16_t* pre = reinterpret_cast<uint16_t*>(eops + nu);
+  uint16_t* ppre = pre + (nu + 1);
+  uint32_t* hi_off = reinterpret_cast<uint32_t*>((reinterpret_cast<unsigned long long>(ppre + (nu + 1)) + 7) & ~7ull);
+  __shared__ uint8_t hpos[32];
+
+  for (uint32_t i = threadIdx.x; i < pd.mat_count; i += NT) smats[i] = P.uop_mats[pd.mat_begin + i];
+  for (uint32_t i = threadIdx.x; i < nu; i += NT) uops[i] = P.uops[pd.uop_begin + i];
+  for (uint32_t i = threadIdx.x; i < (1u << (k - kt)); i += NT)
+    hi_off[i] = static_cast<uint32_t>(pdep_positions(i, pd.lq + kt, k - kt));
+  if (threadIdx.x == 0)
+    for (unsigned q = 0, j = 0; q < n; ++q)
+      if (!((pd.lmask >> q) & 1)) hpos[j++] = static_cast<uint8_t>(q);
+  __syncthreads();
+
+  const uint32_t lo_part = static_cast<uint32_t>(pdep_positions(threadIdx.x, pd.lq, kt));
+  // Shape-specialised straight-line executors need every register round full.
+  const bool full_rounds = k >= 2 && ((1u << (k - 2)) % (NT * QPT)) == 0;
+  // Work units are (shot, tile) pairs in shot-major order; each CTA owns a
+  // contiguous unit range, so it sees at most a few shot boundaries (one
+  // compaction each) while waves of only a few huge shots (n = 24: 64 shots
+  // per 16 GiB wave) still spread over every SM.
+  const uint64_t units = S * tiles;
+  const uint64_t u_begin = units * blockIdx.x / gridDim.x, u_end = units * (blockIdx.x + 1) / gridDim.x;
+  for (uint64_t s = u_begin / tiles; s * tiles < u_end; ++s) {
+    // Per-shot compaction (warp 0, in order): drop failed conditions and
+    // identity Pauli draws; resolve each Pauli to quad masks.
+    if (threadIdx.x < 32) {
+      const uint64_t creg = cregs ? cregs[s] : 0;
+      const uint8_t* sel = pauli_sel + s * num_pauli;
+      uint32_t count = 0, pcount = 0;
+      for (uint32_t c0 = 0; c0 < nu; c0 += 32) {
+        const uint32_t i = c0 + threadIdx.x;
+        bool keep = false;
+        Uop u{};
+        if (i < nu) {
+          u = uops[i];
+          keep = true;
+          const DevOp& op = P.ops[u.ref];
+          if ((u.flags & 1) && (creg & op.cond_mask) != op.cond_value) keep = false;
+          if (keep && u.code == UC_PAULI) {
+            const DevTerm tm = P.terms[op.aux + sel[op.site]];
+            if (tm.identity) {
+              keep = false;
+            } else {
+              uint32_t xq = 0, zq = 0;
+              for (unsigned b = 0; b < op.nq; ++b) {
+                const uint32_t qb = (u.qb >> b) & 1u;
+                xq |= ((tm.x >> op.q[b]) & 1u) << qb;
+                zq |= ((tm.z >> op.q[b]) & 1u) << qb;
+              }
+              u.pauli = static_cast<uint8_t>(xq | (zq << 2) | ((tm.num_y & 3u) << 4));
+            }
+          }
+        }
+        const unsigned lanes_below = (1u << threadIdx.x) - 1;
+        const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+        const unsigned pballot = __ballot_sync(0xffffffffu, keep && u.code == UC_PAULI);
+        const uint32_t at = count + __popc(ballot & lanes_below);
+        if (i < nu) {
+          pre[i] = static_cast<uint16_t>(at);
+          ppre[i] = static_cast<uint16_t>(pcount + __popc(pballot & lanes_below));
+        }
+        if (keep) eops[at] = u;
+        count += __popc(ballot);
+        pcount += __popc(pballot);
+      }
+      if (threadIdx.x == 0) {
+        pre[nu] = static_cast<uint16_t>(count);
+        ppre[nu] = static_cast<uint16_t>(pcount);
+      }
+    }
+    __syncthreads();
+    double2* seg = state + (s << n);
+    const uint64_t t_begin = u_begin > s * tiles ? u_begin - s * tiles : 0;
+    const uint64_t t_end = u_end < (s + 1) * tiles ? u_end - s * tiles : tiles;
+    for (uint64_t t = t_begin; t < t_end; ++t) {
+      double2* tbase = seg + pdep_positions(t, hpos, n - k);
+      if (pd.first) {
+        const bool origin = (tbase == seg);
+        for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
+          tile[l] = make_double2((origin && (lo_part | hi_off[i]) == 0) ? 1.0 : 0.0, 0.0);
+      } else {
+        for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) tile[l] = tbase[lo_part | hi_off[i]];
+      }
+      __syncthreads();
+      for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
+        const Item it = P.items[it_i];
+        const uint32_t b = pre[it.begin], e = pre[it.end];
+        if (full_rounds && it.shape != kNoShape && ppre[it.begin] == ppre[it.end] && e - b == it.nfast) {
+          // This shot runs the segment's common case: every Pauli draw
+          // identity, every condition true.
+          if (it.nfast == 0 && it.sigma == 0xE4) continue;
+          if (ssb_run_shape(it.shape, tile, k, it.la, it.lb, smats + uops[it.begin].mat)) continue;
+        }
+        if (b == e && it.sigma == 0xE4) continue;  // nothing to apply and no relabeling to store
+        if (k < 2) {
+          run_ops_per_op(tile, k, it.begin, it.end, P.pass_ops + pd.po_begin, P.ops, P.mats, P.terms,
+                         cregs ? cregs[s] : 0, pauli_sel + s * num_pauli);
+        } else {
+          run_segment_staged(tile, k, it, eops, b, e, smats, P.ops);
+        }
+      }
+      for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) tbase[lo_part | hi_off[i]] = tile[l];
+    }
+    __syncthreads();  // compaction of the next shot rewrites eops/pre
+  }
+}
+
+#define SSB_TILE_PASS_PARAMS                                                                            \
+  ssb::ProgView P, uint32_t pass_index, double2 *state, uint64_t S, const uint64_t *cregs, const uint8_t *pauli_sel, \
+      uint32_t num_pauli
+
+}  // namespace ssb

@@ -1,6 +1,6 @@
 """Profiling driver (ncu target): one batch of a config through the C ABI."""
 import sys
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2308_03399_b200 import Engine, Program, RunOptions, circuits as cc
 key = sys.argv[1] if len(sys.argv) > 1 else "C2"
 shots = int(sys.argv[2]) if len(sys.argv) > 2 else 2048

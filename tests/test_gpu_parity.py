@@ -78,6 +78,24 @@ def test_kraus_thermal_all_paths(engine, oracle, n, tile):
     assert (values(engine.run_branch(prog, RunOptions(shots=200, seed=3, branch_budget=16))) == want).all()
 
 
+@pytest.mark.parametrize("interpret_only", [False, True])
+@pytest.mark.parametrize("tile", [11, 12])
+def test_streamed_shapes_random_bursts(engine, oracle, tile, interpret_only):
+    """Every gate kind, relabelings, conditionals and Pauli / Kraus noise through
+    the HBM tile passes at tile sizes where the run-time shape-specialised
+    kernel is used (and, interpret_only, the interpreter kernel)."""
+    rng = cc.SplitMix64(4242 + tile)
+    for rep in range(6):
+        circ = cc.random_bursts(rng, n=12 + rep % 2)
+        noise = cc.depolarizing_model(0.02 + 0.03 * (rep % 3), as_kraus=rep == 5)
+        prog = Program.from_text(circ, noise)
+        want = oracle.run_shots(prog, np.arange(96), 77 + rep, threads=8)
+        r = engine.run_batch(prog, RunOptions(shots=96, seed=77 + rep, resident_max_qubits=1, tile_qubits=tile,
+                                              interpret_only=interpret_only))
+        assert (values(r) == want).all(), (rep, circ, noise)
+        assert (r.specialised_shapes > 0) == (not interpret_only)
+
+
 def test_qv14_streamed_default_tiles(engine, oracle):
     prog = Program.from_text(cc.quantum_volume(14, depth=6, seed=5), cc.qv_noise())
     want = oracle.run_shots(prog, np.arange(48), 9, threads=8)
@@ -92,6 +110,9 @@ def test_c2_qv16_reference_sample(engine):
     prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
     r = engine.run_batch(prog, RunOptions(shots=24, seed=1))
     assert [int(v) for v in values(r)] == s["values"][:24]
+    assert r.specialised_shapes > 0
+    r = engine.run_batch(prog, RunOptions(shots=24, seed=1, interpret_only=True))
+    assert [int(v) for v in values(r)] == s["values"][:24] and r.specialised_shapes == 0
     r = engine.run_batch(prog, RunOptions(shots=1, seed=1), shot_begin=99_999, shot_count=1)
     assert int(values(r)[0]) == s["values"][24]
 
@@ -103,6 +124,15 @@ def test_c4_rnd20_reference_sample(engine):
     got = []
     for sid in s["ids"]:
         got.append(int(values(engine.run_batch(prog, RunOptions(shots=1, seed=1), shot_begin=sid, shot_count=1))[0]))
+    assert got == s["values"]
+
+
+def test_c5_qv24_reference_sample(engine):
+    s = golden("config_samples.json")["C5"]
+    cfg = cc.CONFIGS["C5"]
+    prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
+    got = [int(values(engine.run_batch(prog, RunOptions(shots=1, seed=1), shot_begin=sid, shot_count=1))[0])
+           for sid in s["ids"]]
     assert got == s["values"]
 
 
@@ -199,3 +229,16 @@ def test_shard_concatenation(engine, oracle):
              for b, c in ((0, 300), (300, 1), (301, 699))]
     assert (np.concatenate(parts) == whole).all()
     assert (oracle.run_shots(prog, np.arange(1000), 4) == whole).all()
+
+
+def test_guarded_terminal_sampling_fallback(engine, oracle, monkeypatch):
+    """The parallel sampler's exact re-decision path: with the guard band
+    widened every shot is re-decided by the sequential scan; both paths must
+    give the reference's outcomes."""
+    prog = Program.from_text(cc.quantum_volume(12, depth=3, seed=8), cc.qv_noise())
+    want = oracle.run_shots(prog, np.arange(64), 5)
+    r = engine.run_batch(prog, RunOptions(shots=64, seed=5, resident_max_qubits=1))
+    assert (values(r) == want).all() and r.sampling_guard_hits == 0
+    monkeypatch.setenv("SHOTSIM_B200_GUARD_SCALE", "1e15")
+    r = engine.run_batch(prog, RunOptions(shots=64, seed=5, resident_max_qubits=1))
+    assert (values(r) == want).all() and r.sampling_guard_hits == 64
