@@ -434,6 +434,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
           std::sort(R.sorted, R.sorted + ch.arity);
           R.nq = ch.nmat;
           R.mats = P.mats + 16 * ch.mat_begin;
+      R.cls = P.scaled_cls + ch.mat_begin;
           if (ch.arity == 1) {
             R.mode = R_EXPVAL1;
             const uint64_t pairs = A / 2;
@@ -469,9 +470,9 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
         CKB(cudaMemcpyAsync(active, ha.data(), nn, cudaMemcpyHostToDevice, s));
         double* part = dpart.get(nn * R.nq * R.nb);
         vals = dvals.get(nn * R.nq);
-        g_reduce_kernel<<<gridn(nn * R.nq * R.nb), NT, 0, s>>>(pool, nn, R, active, part, slots);
+        launch_reduce(s, pool, nn, R, active, part, slots);
         launched();
-        g_finish_kernel<<<gridn(nn * R.nq), NT, 0, s>>>(nn, R.nq, R.nb, tree, active, part, vals);
+        g_finish_kernel<<<static_cast<unsigned>(std::min<uint64_t>(nn * R.nq, 1u << 20)), NT, 0, s>>>(nn, R.nq, R.nb, tree, active, part, vals);
         launched();
         CKB(cudaStreamSynchronize(s));
       }
@@ -629,9 +630,9 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
           CKB(cudaMemcpyAsync(slots, hs.data(), nl * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
           double* part = dpart.get(nl * R.nq * R.nb);
           double* probs = dvals.get(nl * R.nq);
-          g_reduce_kernel<<<gridn(nl * R.nq * R.nb), NT, 0, s>>>(pool, nl, R, nullptr, part, slots);
+          launch_reduce(s, pool, nl, R, nullptr, part, slots);
           launched();
-          g_finish_kernel<<<gridn(nl * R.nq), NT, 0, s>>>(nl, R.nq, R.nb, 0, nullptr, part, probs);
+          g_finish_kernel<<<static_cast<unsigned>(std::min<uint64_t>(nl * R.nq, 1u << 20)), NT, 0, s>>>(nl, R.nq, R.nb, 0, nullptr, part, probs);
           launched();
           b_leaf_cum_probs<<<gridn(nl, 64), 64, 0, s>>>(probs, nl, cnt, cum, last);
           launched();

@@ -182,6 +182,7 @@ namespace {
 constexpr size_t kMaxPassStageBytes = 28 * 1024;
 size_t stage_bytes(const DevOp& o) {
   if (o.kind == K_PAULI) return 32;
+  if (o.kind == K_KRAUS) return 32 + 16 * 16;
   return 32 + 16 * ((o.nq == 2 && o.mk != MK_2Q_MONO) ? 16 : 4);
 }
 
@@ -234,6 +235,11 @@ void assign_shape(HostDevProgram& d, Item& it, uint32_t uop_base) {
   char buf[96];
   for (uint32_t i = it.begin; i < it.end; ++i) {
     const Uop& u = d.uops[uop_base + i];
+    if (u.code == UC_KRAUS1 || u.code == UC_KRAUS2) {  // per-shot matrix: interpreter only
+      it.shape = kNoShape;
+      it.nfast = 0;
+      return;
+    }
     if (u.code == UC_PAULI) continue;
     const uint64_t cls = (u.code == UC_GEN1 || u.code == UC_GEN2) ? d.ops[u.ref].cls : 0;
     std::snprintf(buf, sizeof buf, "%u.%u.%u.%u.%u.%llx.%u;", u.code, u.qb, u.src, u.mcls, u.sigma,
@@ -290,6 +296,12 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
       if (o.kind == K_PAULI) {
         u.code = UC_PAULI;
         u.qb = static_cast<uint8_t>((po.qb[0] & 1) | (o.nq > 1 ? (po.qb[1] & 1) << 1 : 0));
+      } else if (o.kind == K_KRAUS) {
+        // Per-shot matrix: staged by the tile kernel into the pass's Kraus slot.
+        u.code = o.nq == 1 ? UC_KRAUS1 : UC_KRAUS2;
+        u.qb = o.nq == 1 ? static_cast<uint8_t>(0) : po.qb[0];
+        u.src = po.qb[0];
+        u.mat = static_cast<uint16_t>(0xFFFF);  // patched to pd.kraus_mat below
       } else if (o.nq == 1) {
         u.code = o.mk == MK_1Q_U ? UC_U : o.mk == MK_1Q_REAL ? UC_REAL : UC_GEN1;
         const int bit = 1 << po.qb[0];
@@ -352,10 +364,26 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
     it.begin = ubegin;
     it.end = static_cast<uint32_t>(d.uops.size()) - pd.uop_begin;
     it.sigma = pack(sg);
-    assign_shape(d, it, pd.uop_begin);
   }
   pd.uop_end = static_cast<uint32_t>(d.uops.size());
+  // Per-shot Kraus matrix slot (16 entries) after the static matrices.
+  pd.kraus_mat = mat;
+  bool has_kraus = false;
+  for (uint32_t i = pd.uop_begin; i < pd.uop_end; ++i)
+    if (d.uops[i].code == UC_KRAUS1 || d.uops[i].code == UC_KRAUS2) {
+      d.uops[i].mat = static_cast<uint16_t>(mat);
+      has_kraus = true;
+    }
+  if (has_kraus) {
+    for (int e = 0; e < 16; ++e) {
+      d.uop_mats.push_back(0.0);
+      d.uop_mats.push_back(0.0);
+    }
+    mat += 16;
+  }
+  if (mat > 0xFFFF) throw std::length_error("pass matrix table too large");
   pd.mat_count = mat;
+  for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) assign_shape(d, d.items[it_i], pd.uop_begin);
 }
 
 }  // namespace
@@ -366,7 +394,7 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
 // (gates on disjoint qubits do not commute bitwise in floating point); Kraus /
 // measure / reset sites end a pass. Inside a pass, ops are grouped into
 // register segments (segment_ops).
-void plan_passes(HostDevProgram& d, unsigned tile_k) {
+void plan_passes(HostDevProgram& d, unsigned tile_k, bool fuse_kraus) {
   d.shapes.clear();
   d.passes.clear();
   d.items.clear();
@@ -416,19 +444,29 @@ void plan_passes(HostDevProgram& d, unsigned tile_k) {
     cur_ops.clear();
   };
 
+  auto add = [&](uint32_t i) {
+    const DevOp& o = d.ops[i];
+    uint32_t qm = 0;
+    for (unsigned b = 0; b < o.nq; ++b) qm |= 1u << o.q[b];
+    if (static_cast<unsigned>(std::popcount(cur | qm)) > k || staged + stage_bytes(o) > kMaxPassStageBytes) {
+      close(false);
+      staged = 0;
+    }
+    cur |= qm;
+    cur_ops.push_back(i);
+    staged += stage_bytes(o);
+  };
   for (uint32_t i = 0; i < d.end; ++i) {
     const DevOp& o = d.ops[i];
     if (o.kind == K_BARRIER || (o.kind == K_GATE && o.skip)) continue;
     if (fused_kind(o)) {
-      uint32_t qm = 0;
-      for (unsigned b = 0; b < o.nq; ++b) qm |= 1u << o.q[b];
-      if (static_cast<unsigned>(std::popcount(cur | qm)) > k || staged + stage_bytes(o) > kMaxPassStageBytes) {
-        close(false);
-        staged = 0;
-      }
-      cur |= qm;
-      cur_ops.push_back(i);
-      staged += stage_bytes(o);
+      add(i);
+    } else if (o.kind == K_KRAUS && fuse_kraus && k >= 2) {
+      // Probabilities and per-shot choice between passes; the apply becomes
+      // the first micro-op of the next pass (no separate HBM sweep).
+      close(true);
+      d.steps.push_back({S_KRAUS_DECIDE, i});
+      add(i);
     } else {
       close(true);
       d.steps.push_back({S_SPECIAL, i});

@@ -43,7 +43,8 @@ struct HostDevProgram {
 uint64_t classify_matrix(const double* m, unsigned k, bool scaled);
 HostDevProgram build_device_program(const shotsim::NoisyCircuit& p);
 // Streamed plan: HBM tile passes (gates / Pauli sites) + special steps.
-void plan_passes(HostDevProgram& d, unsigned tile_k);
+// fuse_kraus: Kraus applies run inside the next pass (S_KRAUS_DECIDE steps).
+void plan_passes(HostDevProgram& d, unsigned tile_k, bool fuse_kraus = true);
 // Resident plan: one pass (k = n) whose items cover the whole program.
 void plan_resident(HostDevProgram& d);
 // CUDA source of straight-line executors for the plan's segment shapes

@@ -73,6 +73,8 @@ struct PassDesc {
   uint32_t uop_begin, uop_end;
   uint32_t mat_begin, mat_count;
   uint32_t po_begin;   // first pass_op of this pass (per-op fallback, k < 2)
+  uint32_t kraus_mat;  // matrix-table slot (16 double2) of the per-shot Kraus
+                       // matrix when the pass starts with a Kraus apply
 };
 
 // Micro-op codes of a streamed pass (one per gate / Pauli site).
@@ -91,6 +93,10 @@ enum UopCode : uint8_t {
   UC_SWAP = 6,     // conditional 2q transposition (qb: physical e0 | e1 << 2)
   UC_PHASE = 7,    // 2q diagonal with one non-unit entry (qb: element; mcls:
                    // its class) — CP
+  UC_KRAUS1 = 8,   // apply of a 1q Kraus site's per-shot choice M_sel/sqrt(p)
+                   // (qb: physical pairs, src: logical bit; matrix + classes
+                   // staged per shot from the decide step)
+  UC_KRAUS2 = 9,   // 2q Kraus apply (qb: swapped)
 };
 
 // 16-byte micro-op. After per-shot compaction (identity Pauli draws and
@@ -132,7 +138,9 @@ struct PassOp {
   uint8_t qb[4];       // quad bit (0 -> la, 1 -> lb) of each op qubit
 };
 
-enum StepKind : uint8_t { S_PASS = 0, S_SPECIAL = 1, S_SAMPLE = 2 };
+// S_KRAUS_DECIDE: probabilities + per-shot choice of a Kraus site whose apply
+// is the first micro-op of the next pass (streamed executor).
+enum StepKind : uint8_t { S_PASS = 0, S_SPECIAL = 1, S_SAMPLE = 2, S_KRAUS_DECIDE = 3 };
 struct Step {
   StepKind kind;
   uint32_t index;      // pass index, or op index for S_SPECIAL

@@ -185,9 +185,9 @@ struct SegCtx {
 void run_reduction(ssb_engine* E, const SegCtx& c, const RedSpec& R, int leaves_tree, const uint8_t* active,
                    double* val) {
   double* part = static_cast<double*>(scratch(E, "part", c.S * R.nq * R.nb * sizeof(double)));
-  g_reduce_kernel<<<grid_for(c.S * R.nq * R.nb), NT, 0, E->stream>>>(c.state, c.S, R, active, part);
+  launch_reduce(E->stream, c.state, c.S, R, active, part);
   launched(E);
-  g_finish_kernel<<<grid_for(c.S * R.nq), NT, 0, E->stream>>>(c.S, R.nq, R.nb, leaves_tree, active, part, val);
+  g_finish_kernel<<<static_cast<unsigned>(std::min<uint64_t>(c.S * R.nq, 1u << 20)), NT, 0, E->stream>>>(c.S, R.nq, R.nb, leaves_tree, active, part, val);
   launched(E);
 }
 
@@ -203,6 +203,31 @@ RedSpec outcome_spec(unsigned n, const uint8_t* q, unsigned k) {
   R.nq = static_cast<uint32_t>(uint64_t{1} << k);
   R.nb = G <= SUM_BLOCK ? 1 : G / SUM_BLOCK;
   R.blk = G <= SUM_BLOCK ? G : SUM_BLOCK;
+  return R;
+}
+
+// Kraus probabilities: expval_matrix1_scalar (512-pair blocks + pairwise) for
+// 1q channels, expval_generic (per-group sums; leaves of 8 + tree) for 2q.
+RedSpec kraus_spec(const ProgView& P, const DevOp& op, const DevChannel& ch, unsigned n) {
+  RedSpec R{};
+  R.n = n;
+  R.k = ch.arity;
+  for (unsigned i = 0; i < ch.arity; ++i) R.q[i] = R.sorted[i] = op.q[i];
+  std::sort(R.sorted, R.sorted + ch.arity);
+  R.nq = ch.nmat;
+  R.mats = P.mats + 16 * ch.mat_begin;
+  R.cls = P.scaled_cls + ch.mat_begin;
+  if (ch.arity == 1) {
+    R.mode = R_EXPVAL1;
+    const uint64_t pairs = uint64_t{1} << (n - 1);
+    R.nb = pairs <= SUM_BLOCK ? 1 : pairs / SUM_BLOCK;
+    R.blk = pairs <= SUM_BLOCK ? pairs : SUM_BLOCK;
+  } else {
+    R.mode = R_EXPVAL2;
+    const uint64_t G = uint64_t{1} << (n - 2);
+    R.blk = G <= 8 ? G : 8;
+    R.nb = G / R.blk;
+  }
   return R;
 }
 
@@ -244,26 +269,8 @@ uint64_t apply_op(ssb_engine* E, DevProgram& dp, uint32_t op_index, const SegCtx
     }
     case K_KRAUS: {
       const DevChannel ch = dp.host.channels[op.aux];
-      RedSpec R{};
-      R.n = n;
-      R.k = ch.arity;
-      for (unsigned i = 0; i < ch.arity; ++i) R.q[i] = R.sorted[i] = op.q[i];
-      std::sort(R.sorted, R.sorted + ch.arity);
-      R.nq = ch.nmat;
-      R.mats = P.mats + 16 * ch.mat_begin;
-      int tree = 0;
-      if (ch.arity == 1) {
-        R.mode = R_EXPVAL1;
-        const uint64_t pairs = uint64_t{1} << (n - 1);
-        R.nb = pairs <= SUM_BLOCK ? 1 : pairs / SUM_BLOCK;
-        R.blk = pairs <= SUM_BLOCK ? pairs : SUM_BLOCK;
-      } else {
-        R.mode = R_EXPVAL2;
-        const uint64_t G = uint64_t{1} << (n - 2);
-        R.blk = G <= 8 ? G : 8;
-        R.nb = G / R.blk;
-        tree = 1;
-      }
+      const RedSpec R = kraus_spec(P, op, ch, n);
+      const int tree = ch.arity == 2;
       const uint64_t chunk = chunk_for(c.S, (R.nq * R.nb + R.nq) * sizeof(double) + 16 * 16 + 32);
       for (uint64_t off = 0; off < c.S; off += chunk) {
         const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
@@ -318,6 +325,31 @@ double guard_scale() {
   const char* v = std::getenv("SHOTSIM_B200_GUARD_SCALE");
   const double s = v ? std::strtod(v, nullptr) : 1.0;
   return s >= 1.0 ? s : 1.0;
+}
+
+// Kraus site probabilities + per-shot choice for a whole wave (the streamed
+// executor's S_KRAUS_DECIDE step): scaled[s] = M_sel / sqrt(p_sel) and its
+// classes for the apply micro-op at the head of the next tile pass; inactive
+// shots (failed condition) get chosen = -1 and their apply is compacted away.
+void kraus_decide_wave(ssb_engine* E, DevProgram& dp, uint32_t op_index, const SegCtx& c, double2* scaled,
+                       uint64_t* cls, int* chosen) {
+  const DevOp op = dp.host.ops[op_index];
+  const unsigned n = dp.host.n;
+  const ProgView& P = dp.view;
+  const DevChannel ch = dp.host.channels[op.aux];
+  const RedSpec R = kraus_spec(P, op, ch, n);
+  const uint64_t chunk = chunk_for(c.S, (R.nq * R.nb + R.nq) * sizeof(double) + 32);
+  for (uint64_t off = 0; off < c.S; off += chunk) {
+    const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
+    uint8_t* active = static_cast<uint8_t*>(scratch(E, "active", cc.S));
+    double* val = static_cast<double*>(scratch(E, "val", cc.S * R.nq * sizeof(double)));
+    g_active_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(op, cc.S, cc.cregs, active);
+    launched(E);
+    run_reduction(E, cc, R, ch.arity == 2, active, val);
+    g_kraus_decide_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(P, op, cc.S, cc.seed, cc.ids, cc.begin, cc.u, active,
+                                                                val, scaled + 16 * off, cls + off, chosen + off, E->err);
+    launched(E);
+  }
 }
 
 void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c) {
@@ -464,6 +496,15 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
     wave = std::min<uint64_t>(largest, (uint64_t{1} << 31) / tiles);
     double2* state = static_cast<double2*>(scratch(E, "state", wave * seg));
     uint8_t* psel = dp.num_pauli ? static_cast<uint8_t*>(scratch(E, "psel", wave * dp.num_pauli)) : nullptr;
+    // Per-shot Kraus choices of the wave (S_KRAUS_DECIDE -> next pass).
+    double2* kmat = nullptr;
+    uint64_t* kcls = nullptr;
+    int* kchosen = nullptr;
+    if (h.has_kraus) {
+      kmat = static_cast<double2*>(scratch(E, "wave_kmat", wave * 16 * sizeof(double2)));
+      kcls = static_cast<uint64_t*>(scratch(E, "wave_kcls", wave * sizeof(uint64_t)));
+      kchosen = static_cast<int*>(scratch(E, "wave_kchosen", wave * sizeof(int)));
+    }
     size_t tsmem = 0;
     for (const PassDesc& pd : h.passes)
       tsmem = std::max<size_t>(tsmem, tile_smem_bytes(pd.k, pd.uop_end - pd.uop_begin, pd.mat_count));
@@ -488,13 +529,18 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       }
       fused = 0;
       for (const Step& st : h.steps) {
-        if (st.kind == S_PASS) {
+        if (st.kind == S_KRAUS_DECIDE) {
+          timer.begin(1);
+          kraus_decide_wave(E, dp, st.index, c, kmat, kcls, kchosen);
+          timer.end(1);
+        } else if (st.kind == S_PASS) {
           timer.begin(0);
           const unsigned grid =
               static_cast<unsigned>(std::min<uint64_t>(S * tiles, uint64_t(std::max(per_sm, 1)) * E->num_sms));
           uint32_t pass_index = st.index, num_pauli = dp.num_pauli;
           uint64_t* cregs = c.cregs;
-          void* args[] = {&dp.view, &pass_index, &state, const_cast<uint64_t*>(&S), &cregs, &psel, &num_pauli};
+          void* args[] = {&dp.view, &pass_index, &state, const_cast<uint64_t*>(&S), &cregs, &psel, &num_pauli,
+                          &kmat, &kcls};
           CK(cudaLaunchKernel(kfn, dim3(grid), dim3(NT), args, tsmem, E->stream));
           launched(E);
           timer.end(0);

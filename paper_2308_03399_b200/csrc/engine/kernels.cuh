@@ -192,7 +192,7 @@ static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint
 }
 
 static __global__ void __launch_bounds__(NT, SSB_TILE_MINB) tile_pass_kernel(SSB_TILE_PASS_PARAMS) {
-  tile_pass_body(P, pass_index, state, S, cregs, pauli_sel, num_pauli);
+  tile_pass_body(P, pass_index, state, S, cregs, pauli_sel, num_pauli, kmat, kcls);
 }
 
 // Per-(shot, Pauli site) term choice for a wave: sel[s][site] (u8).
@@ -304,74 +304,192 @@ struct RedSpec {
   uint64_t nb;          // blocks per quantity
   uint64_t blk;         // elements per block
   const double2* mats;  // R_EXPVAL*: nq consecutive matrix slots
+  const uint64_t* cls;  // R_EXPVAL*: their entry classes (zero entries skipped: exact for norms)
 };
 
-static __global__ void g_reduce_kernel(const double2* st, uint64_t S, RedSpec R, const uint8_t* active, double* part,
-                                const uint32_t* slots = nullptr) {
-  const uint64_t total = S * R.nq * R.nb;
+// Threads: R_OUTCOME — one per (shot, outcome, block); R_EXPVAL1 — one per
+// (shot, matrix, 512-pair block); R_EXPVAL2 — one per (shot, 8-group leaf),
+// computing every matrix's leaf from the same 32 amplitudes held in registers.
+// Each partial keeps the reference's sequential order; the block loops load 8
+// elements ahead of the dependent add chain.
+__host__ __device__ inline uint64_t reduce_threads(const RedSpec& R, uint64_t S) {
+  return S * (R.mode == R_EXPVAL2 ? 1 : R.nq) * R.nb;
+}
+
+static __global__ void __launch_bounds__(NT) g_reduce_kernel(const double2* st, uint64_t S, RedSpec R,
+                                                              const uint8_t* active, double* part,
+                                                              const uint32_t* slots = nullptr) {
+  const uint64_t total = reduce_threads(R, S);
   for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
        idx += uint64_t{gridDim.x} * blockDim.x) {
-    const uint64_t b = idx % R.nb, qs = idx / R.nb, qi = qs % R.nq, s = qs / R.nq;
-    if (active && !active[s]) continue;
-    const double2* a = st + (seg_of(slots, s) << R.n);
-    double acc = 0.0;
-    if (R.mode == R_OUTCOME) {
-      const uint64_t off = scatter_bits(qi, R.q, R.k);
-      for (uint64_t g = b * R.blk; g < (b + 1) * R.blk; ++g)
-        acc = __dadd_rn(acc, c_norm(a[expand_sorted(g, R.sorted, R.k) | off]));
-    } else if (R.mode == R_EXPVAL1) {
-      const double2* m = R.mats + 16 * qi;
-      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
-      const unsigned t = R.q[0];
-      for (uint64_t i = b * R.blk; i < (b + 1) * R.blk; ++i) {
-        const uint64_t i0 = insert_zero(i, t), i1 = i0 | (uint64_t{1} << t);
-        const double2 a0 = a[i0], a1 = a[i1];
-        acc = __dadd_rn(acc, c_norm(c_add(c_mul(m0, a0), c_mul(m1, a1))));
-        acc = __dadd_rn(acc, c_norm(c_add(c_mul(m2, a0), c_mul(m3, a1))));
-      }
-    } else {
-      double2 m[16];
-      load_matrix<4>(R.mats + 16 * qi, m);
-      const uint64_t off[4] = {0, uint64_t{1} << R.q[0], uint64_t{1} << R.q[1],
-                               (uint64_t{1} << R.q[0]) | (uint64_t{1} << R.q[1])};
-      for (uint64_t g = b * R.blk; g < (b + 1) * R.blk; ++g) {
-        const uint64_t base = expand_sorted(g, R.sorted, 2);
-        double2 in[4];
+    if (R.mode == R_OUTCOME || R.mode == R_EXPVAL1) {
+      const uint64_t b = idx % R.nb, qs = idx / R.nb, qi = qs % R.nq, s = qs / R.nq;
+      if (active && !active[s]) continue;
+      const double2* a = st + (seg_of(slots, s) << R.n);
+      const uint64_t g0 = b * R.blk, g1 = g0 + R.blk;
+      double acc = 0.0;
+      if (R.mode == R_OUTCOME) {
+        // outcome_probability (statevector.cpp:142-164): one 512-block
+        const uint64_t off = scatter_bits(qi, R.q, R.k);
+        uint64_t g = g0;
+        for (; g + 8 <= g1; g += 8) {
+          double p[8];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) in[c] = a[base + off[c]];
-        double row = 0.0;
+          for (int j = 0; j < 8; ++j) p[j] = c_norm(a[expand_sorted(g + j, R.sorted, R.k) | off]);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          double2 v = make_double2(0.0, 0.0);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) v = c_add(v, c_mul(m[4 * r + c], in[c]));
-          row = __dadd_rn(row, c_norm(v));
+          for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, p[j]);
         }
-        acc = __dadd_rn(acc, row);
+        for (; g < g1; ++g) acc = __dadd_rn(acc, c_norm(a[expand_sorted(g, R.sorted, R.k) | off]));
+      } else {
+        // expval_matrix1_scalar (kernels_scalar.cpp:103-126): one 512-pair block
+        double2 m[4];
+        load_matrix<2>(R.mats + 16 * qi, m);
+        const uint64_t cls = R.cls[qi];
+        const unsigned t = R.q[0];
+        const uint64_t bit = uint64_t{1} << t;
+        uint64_t i = g0;
+        for (; i + 4 <= g1; i += 4) {
+          double p[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t i0 = insert_zero(i + j, t);
+            const double2 in[2] = {a[i0], a[i0 | bit]};
+            p[2 * j] = c_norm(row_apply<2>(m, cls, 0, in));
+            p[2 * j + 1] = c_norm(row_apply<2>(m, cls, 1, in));
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, p[j]);
+        }
+        for (; i < g1; ++i) {
+          const uint64_t i0 = insert_zero(i, t);
+          const double2 in[2] = {a[i0], a[i0 | bit]};
+          acc = __dadd_rn(acc, c_norm(row_apply<2>(m, cls, 0, in)));
+          acc = __dadd_rn(acc, c_norm(row_apply<2>(m, cls, 1, in)));
+        }
       }
+      part[idx] = acc;
     }
-    part[idx] = acc;
   }
 }
 
-// part (nb per quantity) -> val[s*nq + q] (one thread each). 512-block
-// partials finish with pairwise_sum over the partials (common.cpp:12-26);
-// expval_generic leaves (already the 8-element leaves of pairwise_sum over
-// all groups) finish with the balanced tree above them.
-static __global__ void g_finish_kernel(uint64_t S, uint32_t nq, uint64_t nb, int leaves_tree, const uint8_t* active,
-                                double* part, double* val) {
-  const uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
-  if (idx >= S * nq) return;
-  if (active && !active[idx / nq]) return;
-  double* v = part + idx * nb;
-  if (nb == 1) {
-    val[idx] = v[0];
-  } else if (!leaves_tree) {
-    val[idx] = pairwise_inplace(v, nb);
+static __global__ void __launch_bounds__(128) g_expval2_kernel(const double2* st, uint64_t S, RedSpec R,
+                                                               const uint8_t* active, double* part,
+                                                               const uint32_t* slots = nullptr) {
+  const uint64_t total = reduce_threads(R, S);
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    // expval_generic (statevector.cpp:56-80): per-group row sums, 8-group leaves
+    const uint64_t b = idx % R.nb, s = idx / R.nb;
+    if (active && !active[s]) continue;
+    const double2* a = st + (seg_of(slots, s) << R.n);
+    const uint64_t off[4] = {0, uint64_t{1} << R.q[0], uint64_t{1} << R.q[1],
+                             (uint64_t{1} << R.q[0]) | (uint64_t{1} << R.q[1])};
+    double2 in[8][4];
+    const uint64_t cnt = R.blk;  // <= 8
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < cnt) {
+        const uint64_t base = expand_sorted(b * R.blk + j, R.sorted, 2);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) in[j][c] = a[base + off[c]];
+      }
+    }
+    for (uint32_t qi = 0; qi < R.nq; ++qi) {
+      double2 m[16];
+      load_matrix<4>(R.mats + 16 * qi, m);
+      const uint64_t cls = R.cls[qi];
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < cnt) {
+          double row = 0.0;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) row = __dadd_rn(row, c_norm(row_apply<4>(m, cls, r, in[j])));
+          acc = __dadd_rn(acc, row);
+        }
+      }
+      part[(s * R.nq + qi) * R.nb + b] = acc;
+    }
+  }
+}
+
+// Launches the partial reduction for R (the 2q expval has its own kernel).
+inline void launch_reduce(cudaStream_t stream, const double2* st, uint64_t S, const RedSpec& R, const uint8_t* active,
+                          double* part, const uint32_t* slots = nullptr) {
+  const uint64_t work = reduce_threads(R, S);
+  if (R.mode == R_EXPVAL2) {
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((work + 127) / 128, 1u << 30)));
+    g_expval2_kernel<<<grid, 128, 0, stream>>>(st, S, R, active, part, slots);
   } else {
-    for (uint64_t w = nb; w > 1; w /= 2)
-      for (uint64_t i = 0; i < w / 2; ++i) v[i] = __dadd_rn(v[2 * i], v[2 * i + 1]);
-    val[idx] = v[0];
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((work + NT - 1) / NT, 1u << 30)));
+    g_reduce_kernel<<<grid, NT, 0, stream>>>(st, S, R, active, part, slots);
+  }
+}
+
+// Exact pairwise_sum (common.cpp:12-26) of an aligned power-of-two run of
+// tree elements: element i is v[i] (leaf8 == false) or the sequential sum of
+// v[8i..8i+8) (leaf8 == true, the recursion's count <= 8 leaves). A binary
+// counter stack combines equal-sized neighbours left + right, which is exactly
+// the recursive halving tree (for power-of-two counts).
+__device__ __forceinline__ double tree_sum_run(const double* v, uint64_t first, uint64_t count, bool leaf8) {
+  double stk[40];
+  int top = 0;
+  for (uint64_t i = first; i < first + count; ++i) {
+    double x;
+    if (leaf8) {
+      x = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x = __dadd_rn(x, v[8 * i + j]);
+    } else {
+      x = v[i];
+    }
+    // Merge while the low bits of (i - first + 1) are zero: one merge per
+    // completed power-of-two subtree.
+    stk[top++] = x;
+    for (uint64_t c = i - first + 1; (c & 1) == 0; c >>= 1) {
+      --top;
+      stk[top - 1] = __dadd_rn(stk[top - 1], stk[top]);
+    }
+  }
+  return stk[0];
+}
+
+// part (nb per quantity) -> val[s*nq + q]: one CTA per (shot, quantity). nb is
+// a power of two (2^n-derived). 512-block partials finish with pairwise_sum
+// over the partials (leaves of 8, then the tree); expval_generic leaves
+// (leaves_tree: already the 8-group leaves of pairwise_sum over all groups)
+// finish with the balanced tree above them. Each thread reduces an aligned
+// subtree, then the CTA combines the subtree roots level by level — the same
+// additions as the reference's recursion, in parallel.
+static __global__ void __launch_bounds__(NT) g_finish_kernel(uint64_t S, uint32_t nq, uint64_t nb, int leaves_tree,
+                                                             const uint8_t* active, double* part, double* val) {
+  __shared__ double roots[NT];
+  for (uint64_t idx = blockIdx.x; idx < S * nq; idx += gridDim.x) {
+    if (active && !active[idx / nq]) continue;
+    const double* v = part + idx * nb;
+    if (nb <= 8) {  // recursion base: sequential
+      if (threadIdx.x == 0) {
+        double x = 0.0;
+        for (uint64_t i = 0; i < nb; ++i) x = __dadd_rn(x, v[i]);
+        val[idx] = x;
+      }
+      continue;
+    }
+    const bool leaf8 = !leaves_tree;
+    const uint64_t elems = leaf8 ? nb / 8 : nb;  // tree elements (power of two)
+    const uint64_t nthr = elems < NT ? elems : NT;
+    const uint64_t per = elems / nthr;
+    if (threadIdx.x < nthr) roots[threadIdx.x] = tree_sum_run(v, threadIdx.x * per, per, leaf8);
+    __syncthreads();
+    for (uint64_t w = nthr; w > 1; w /= 2) {
+      double x = 0.0;
+      if (threadIdx.x < w / 2) x = __dadd_rn(roots[2 * threadIdx.x], roots[2 * threadIdx.x + 1]);
+      __syncthreads();
+      if (threadIdx.x < w / 2) roots[threadIdx.x] = x;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) val[idx] = roots[0];
+    __syncthreads();
   }
 }
 

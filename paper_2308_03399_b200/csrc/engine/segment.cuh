@@ -338,10 +338,11 @@ static __device__ __forceinline__ Quad4 logical_quad_op(Quad4 x, Uop u, const do
     case UC_U:
     case UC_REAL:
     case UC_GEN1:
+    case UC_KRAUS1:
       if (u.src) {
         if (u.code == UC_U) quad_apply1p<0, 2, 1, 3, MK_1Q_U, true, 1>(one, m, 0, 1);
         else if (u.code == UC_REAL) quad_apply1p<0, 2, 1, 3, MK_1Q_REAL, true, 1>(one, m, 0, 1);
-        else quad_apply1p<0, 2, 1, 3, MK_1Q_GEN, true, 1>(one, m, gcls, 1);
+        else quad_apply1p<0, 2, 1, 3, MK_1Q_GEN, true, 1>(one, m, gcls, 1);  // GEN1 / KRAUS1
       } else {
         if (u.code == UC_U) quad_apply1p<0, 1, 2, 3, MK_1Q_U, true, 1>(one, m, 0, 1);
         else if (u.code == UC_REAL) quad_apply1p<0, 1, 2, 3, MK_1Q_REAL, true, 1>(one, m, 0, 1);
@@ -368,10 +369,12 @@ static __device__ __forceinline__ Quad4 logical_quad_op(Quad4 x, Uop u, const do
   return Quad4{{v[0], v[1], v[2], v[3]}};
 }
 
-// Out-of-line form for the interpreter's rare path.
-static __device__ __noinline__ Quad4 generic_quad_op(Quad4 x, Uop u, const double2* m, const DevOp* ops) {
-  const uint64_t gcls = (u.code == UC_GEN1 || u.code == UC_GEN2) ? ops[u.ref].cls : 0;
-  return logical_quad_op(x, u, m, gcls);
+// Entry classes a generic micro-op applies with: the gate's (GEN1 / GEN2) or
+// the shot's chosen Kraus matrix's (KRAUS1 / KRAUS2).
+__device__ __forceinline__ uint64_t generic_cls(const Uop& u, const DevOp* ops, uint64_t kraus_cls) {
+  if (u.code == UC_GEN1 || u.code == UC_GEN2) return ops[u.ref].cls;
+  if (u.code == UC_KRAUS1 || u.code == UC_KRAUS2) return kraus_cls;
+  return 0;
 }
 
 // Rare micro-op on one quad that lives in shared memory at its logical
@@ -380,18 +383,18 @@ static __device__ __noinline__ Quad4 generic_quad_op(Quad4 x, Uop u, const doubl
 // to their own tile addresses first), so its register allocation never has to
 // meet the call ABI.
 static __device__ __noinline__ void rare_quad_op_smem(double2* st, uint64_t base, uint64_t dla, uint64_t dlb, Uop u,
-                                                      const double2* m, const DevOp* ops) {
+                                                      const double2* m, uint64_t gcls) {
   double2* a[4] = {st + base, st + (base | dla), st + (base | dlb), st + (base | dla | dlb)};
   Quad4 x{{*a[0], *a[1], *a[2], *a[3]}};
   u.sigma = 0xE4;  // operate on the logical view directly
-  x = generic_quad_op(x, u, m, ops);
+  x = logical_quad_op(x, u, m, gcls);
   for (int e = 0; e < 4; ++e) *a[e] = x.e[e];
 }
 
 template <bool FULL>
 static __device__ __forceinline__ void run_segment_staged_t(double2* st, unsigned k, const Item& it, const Uop* eops,
                                                             uint32_t begin, uint32_t end, const double2* smats,
-                                                            const DevOp* ops) {
+                                                            const DevOp* ops, uint64_t kraus_cls) {
   const unsigned la = it.la, lb = it.lb;
   const uint64_t dla = uint64_t{1} << la, dlb = uint64_t{1} << lb;
   const uint64_t nquads = uint64_t{1} << (k - 2);
@@ -469,7 +472,7 @@ static __device__ __forceinline__ void run_segment_staged_t(double2* st, unsigne
         st[base[q] | dla] = L[1];
         st[base[q] | dlb] = L[2];
         st[base[q] | dla | dlb] = L[3];
-        rare_quad_op_smem(st, base[q], dla, dlb, u, m, ops);
+        rare_quad_op_smem(st, base[q], dla, dlb, u, m, generic_cls(u, ops, kraus_cls));
         L[0] = st[base[q]];
         L[1] = st[base[q] | dla];
         L[2] = st[base[q] | dlb];
@@ -499,11 +502,11 @@ static __device__ __forceinline__ void run_segment_staged_t(double2* st, unsigne
 }
 
 static __device__ void run_segment_staged(double2* st, unsigned k, const Item& it, const Uop* eops, uint32_t begin,
-                                          uint32_t end, const double2* smats, const DevOp* ops) {
+                                          uint32_t end, const double2* smats, const DevOp* ops, uint64_t kraus_cls) {
   if ((uint64_t{1} << (k - 2)) % (uint64_t{NT} * QPT) == 0)
-    run_segment_staged_t<true>(st, k, it, eops, begin, end, smats, ops);
+    run_segment_staged_t<true>(st, k, it, eops, begin, end, smats, ops, kraus_cls);
   else
-    run_segment_staged_t<false>(st, k, it, eops, begin, end, smats, ops);
+    run_segment_staged_t<false>(st, k, it, eops, begin, end, smats, ops, kraus_cls);
 }
 
 }  // namespace ssb

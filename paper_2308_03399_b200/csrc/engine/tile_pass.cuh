@@ -63,9 +63,11 @@ __host__ __device__ inline uint64_t tile_smem_bytes(unsigned k, uint32_t nuops, 
 
 // Persistent: each CTA owns a contiguous range of (shot, tile) units, stages
 // the pass's micro-op stream once, and compacts it once per shot it touches.
+// kmat / kcls: per-shot chosen Kraus matrix (16 double2, scaled by
+// 1/sqrt(p)) and its classes for a pass that starts with a Kraus apply.
 static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_t pass_index, double2* state, uint64_t S,
                                                       const uint64_t* cregs, const uint8_t* pauli_sel,
-                                                      uint32_t num_pauli) {
+                                                      uint32_t num_pauli, const double2* kmat, const uint64_t* kcls) {
   extern __shared__ double2 tile[];
   const PassDesc& pd = P.passes[pass_index];
   const unsigned n = P.n, k = pd.k;
@@ -80,6 +82,8 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
   uint16_t* ppre = pre + (nu + 1);
   uint32_t* hi_off = reinterpret_cast<uint32_t*>((reinterpret_cast<unsigned long long>(ppre + (nu + 1)) + 7) & ~7ull);
   __shared__ uint8_t hpos[32];
+  __shared__ uint64_t kraus_cls;
+  const bool has_kraus = pd.kraus_mat < pd.mat_count;
 
   for (uint32_t i = threadIdx.x; i < pd.mat_count; i += NT) smats[i] = P.uop_mats[pd.mat_begin + i];
   for (uint32_t i = threadIdx.x; i < nu; i += NT) uops[i] = P.uops[pd.uop_begin + i];
@@ -146,6 +150,12 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
         pre[nu] = static_cast<uint16_t>(count);
         ppre[nu] = static_cast<uint16_t>(pcount);
       }
+    } else if (has_kraus && threadIdx.x < 48) {  // stage this shot's Kraus choice
+      if (threadIdx.x < 48) {
+        const uint32_t e = threadIdx.x - 32;
+        smats[pd.kraus_mat + e] = kmat[s * 16 + e];
+        if (e == 0) kraus_cls = kcls[s];
+      }
     }
     __syncthreads();
     double2* seg = state + (s << n);
@@ -175,7 +185,7 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
           run_ops_per_op(tile, k, it.begin, it.end, P.pass_ops + pd.po_begin, P.ops, P.mats, P.terms,
                          cregs ? cregs[s] : 0, pauli_sel + s * num_pauli);
         } else {
-          run_segment_staged(tile, k, it, eops, b, e, smats, P.ops);
+          run_segment_staged(tile, k, it, eops, b, e, smats, P.ops, kraus_cls);
         }
       }
       for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) tbase[lo_part | hi_off[i]] = tile[l];
@@ -186,6 +196,6 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
 
 #define SSB_TILE_PASS_PARAMS                                                                            \
   ssb::ProgView P, uint32_t pass_index, double2 *state, uint64_t S, const uint64_t *cregs, const uint8_t *pauli_sel, \
-      uint32_t num_pauli
+      uint32_t num_pauli, const double2 *kmat, const uint64_t *kcls
 
 }  // namespace ssb

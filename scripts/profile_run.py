@@ -7,5 +7,9 @@ shots = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 cfg = cc.CONFIGS[key]
 eng = Engine(0)
 prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
-r = eng.run_batch(prog, RunOptions(shots=shots, seed=1))
+mode = sys.argv[3] if len(sys.argv) > 3 else "batch"
+if mode == "batch":
+    r = eng.run_batch(prog, RunOptions(shots=shots, seed=1))
+else:  # branch:<budget>
+    r = eng.run_branch(prog, RunOptions(shots=shots, seed=1, branch_budget=int(mode.split(":")[1])))
 print(key, shots, "shots", r.device_seconds, "s", shots / r.device_seconds, "shots/s")
