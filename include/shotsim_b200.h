@@ -158,8 +158,9 @@ typedef struct ssb_stats {
   double sample_seconds;     /* terminal sampling                             */
   uint64_t specialised_shapes; /* streamed: segment shapes run straight-line
                                   (run-time specialised kernel); 0: interpreter */
-  uint64_t sampling_guard_hits; /* terminal samples re-decided by the exact
-                                   sequential scan (guard band) */
+  uint64_t sampling_serial_chunks; /* terminal-sampling chunks replayed with the
+                                      reference's sequential adds (binade
+                                      changes, ties, the deciding chunk) */
 } ssb_stats;
 
 SSB_API const char* ssb_last_error(void);

@@ -77,7 +77,7 @@ class StatsC(C.Structure):
         ("fused_passes", C.c_uint64), ("device_seconds", C.c_double), ("wall_seconds", C.c_double),
         ("pass_seconds", C.c_double), ("pass_launches", C.c_uint64), ("special_seconds", C.c_double),
         ("sample_seconds", C.c_double), ("specialised_shapes", C.c_uint64),
-        ("sampling_guard_hits", C.c_uint64),
+        ("sampling_serial_chunks", C.c_uint64),
     ]
 
 

@@ -123,7 +123,7 @@ class RunResult:
     wall_seconds: float = 0.0
     fused_passes: int = 0
     specialised_shapes: int = 0
-    sampling_guard_hits: int = 0
+    sampling_serial_chunks: int = 0
 
 
 def bitstring(value: int, width: int) -> str:
@@ -193,7 +193,7 @@ class Engine:
                       branch=BranchStats(st.peak_states, st.passes), strategy=name, shots=count,
                       seed=opts.seed, device_seconds=st.device_seconds, wall_seconds=st.wall_seconds,
                       fused_passes=st.fused_passes, specialised_shapes=st.specialised_shapes,
-                      sampling_guard_hits=st.sampling_guard_hits)
+                      sampling_serial_chunks=st.sampling_serial_chunks)
         r._values = values
         return r
 

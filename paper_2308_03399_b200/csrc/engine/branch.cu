@@ -277,21 +277,10 @@ struct HostNode {
 };
 
 template <class T>
-struct DBuf {  // grow-only device buffer
-  T* p = nullptr;
-  size_t cap = 0;
-  T* get(size_t n) {
-    if (n > cap) {
-      if (p) cudaFree(p);
-      p = nullptr;
-      CKB(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-      cap = std::max<size_t>(n, 1);
-    }
-    return p;
-  }
-  ~DBuf() {
-    if (p) cudaFree(p);
-  }
+struct DBuf {  // named view of a persistent grow-only engine buffer
+  const EngineView* E;
+  const char* name;
+  T* get(size_t n) { return static_cast<T*>(E->scratch(E->ctx, name, std::max<size_t>(n, 1) * sizeof(T))); }
 };
 
 }  // namespace
@@ -316,9 +305,10 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   if (max_slots * seg > mem_limit_bytes)
     throw shotsim::CapacityError("branch budget of " + std::to_string(budget) + " states at " + std::to_string(n) +
                                  " qubits needs " + std::to_string(max_slots * seg) + " bytes");
-  DBuf<double2> pool_buf;
+  // The pool lives in the engine across runs (grown by doubling, contents
+  // preserved), so repeated runs never reallocate.
   uint64_t pool_cap = std::min<uint64_t>(max_slots, 64);
-  double2* pool = pool_buf.get(pool_cap * A);
+  double2* pool = static_cast<double2*>(E.grow(E.ctx, "branch.pool", pool_cap * seg, 0));
   std::vector<uint32_t> free_slots;
   uint32_t next_slot = 0;
   auto alloc_slot = [&]() -> uint32_t {
@@ -330,20 +320,13 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
     if (next_slot >= pool_cap) {  // grow (rare): copy live slots over
       const uint64_t ncap = std::min<uint64_t>(max_slots, pool_cap * 2);
       if (ncap <= pool_cap) throw std::logic_error("branch slot pool exhausted");
-      double2* np = nullptr;
-      CKB(cudaMalloc(&np, ncap * seg));
-      CKB(cudaMemcpyAsync(np, pool_buf.p, pool_cap * seg, cudaMemcpyDeviceToDevice, s));
-      CKB(cudaStreamSynchronize(s));
-      cudaFree(pool_buf.p);
-      pool_buf.p = np;
-      pool_buf.cap = ncap * A;
-      pool = np;
+      pool = static_cast<double2*>(E.grow(E.ctx, "branch.pool", ncap * seg, pool_cap * seg));
       pool_cap = ncap;
     }
     return next_slot++;
   };
 
-  DBuf<uint64_t> shots_a, shots_b, waiting_buf;
+  DBuf<uint64_t> shots_a{&E, "branch.shots_a"}, shots_b{&E, "branch.shots_b"}, waiting_buf{&E, "branch.waiting"};
   uint64_t* cur_shots = shots_a.get(count);
   uint64_t* nxt_shots = shots_b.get(count);
   uint64_t* waiting = waiting_buf.get(count);
@@ -351,15 +334,15 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   launched();
   uint64_t nwaiting = count;
 
-  DBuf<DevNode> dnodes;
-  DBuf<uint32_t> dkeys, dslots;
-  DBuf<unsigned> dcounts;
-  DBuf<uint64_t> ddst, dlast, dcreg;
-  DBuf<unsigned long long> dcursor;
-  DBuf<double> dvals, dpart, dcum;
-  DBuf<uint2> dpairs;
-  DBuf<ChildOp> dkids;
-  DBuf<uint8_t> dactive;
+  DBuf<DevNode> dnodes{&E, "branch.nodes"};
+  DBuf<uint32_t> dkeys{&E, "branch.keys"}, dslots{&E, "branch.slots"};
+  DBuf<unsigned> dcounts{&E, "branch.counts"};
+  DBuf<uint64_t> ddst{&E, "branch.dst"}, dlast{&E, "branch.last"}, dcreg{&E, "branch.creg"};
+  DBuf<unsigned long long> dcursor{&E, "branch.cursor"};
+  DBuf<double> dvals{&E, "branch.vals"}, dpart{&E, "branch.part"}, dcum{&E, "branch.cum"};
+  DBuf<uint2> dpairs{&E, "branch.pairs"};
+  DBuf<ChildOp> dkids{&E, "branch.kids"};
+  DBuf<uint8_t> dactive{&E, "branch.active"};
 
   uint64_t peak = 0, passes = 0;
   std::vector<HostNode> live;

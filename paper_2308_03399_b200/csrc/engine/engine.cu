@@ -47,7 +47,7 @@ struct ssb_engine {
   int num_sms = 0;
   size_t smem_optin = 0;
   int* err = nullptr;
-  unsigned long long* guard_hits = nullptr;  // guarded-sampling exact re-decisions
+  unsigned long long* serial_chunks = nullptr;  // sampling chunks replayed sequentially
   std::map<std::pair<uint64_t, unsigned>, std::unique_ptr<ssb::DevProgram>> programs;
   std::map<std::string, std::pair<void*, size_t>> scratch;
   uint64_t launches = 0;
@@ -80,6 +80,24 @@ void* scratch(ssb_engine* E, const char* name, size_t bytes) {
     slot.second = bytes;
   }
   return slot.first;
+}
+
+void* engine_scratch(void* ctx, const char* name, size_t bytes) {
+  return scratch(static_cast<ssb_engine*>(ctx), name, bytes);
+}
+
+void* engine_grow(void* ctx, const char* name, size_t bytes, size_t keep) {
+  ssb_engine* E = static_cast<ssb_engine*>(ctx);
+  auto& slot = E->scratch[name];
+  if (slot.second >= bytes) return slot.first;
+  void* np = nullptr;
+  CK(cudaMalloc(&np, bytes));
+  if (slot.first && keep) CK(cudaMemcpyAsync(np, slot.first, std::min(keep, slot.second), cudaMemcpyDeviceToDevice, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  if (slot.first) CK(cudaFree(slot.first));
+  slot.first = np;
+  slot.second = bytes;
+  return np;
 }
 
 template <class T>
@@ -319,12 +337,11 @@ uint64_t apply_op(ssb_engine* E, DevProgram& dp, uint32_t op_index, const SegCtx
   return 0;
 }
 
-// Test hook: SHOTSIM_B200_GUARD_SCALE widens the sampling guard band (e.g.
-// 1e12 sends every shot through the exact sequential re-decision).
-double guard_scale() {
-  const char* v = std::getenv("SHOTSIM_B200_GUARD_SCALE");
-  const double s = v ? std::strtod(v, nullptr) : 1.0;
-  return s >= 1.0 ? s : 1.0;
+// Test hook: SHOTSIM_B200_SAMPLE_SERIAL=1 replays every sampling chunk with the
+// sequential adds (the exact-advance path off).
+int sample_force_serial() {
+  const char* v = std::getenv("SHOTSIM_B200_SAMPLE_SERIAL");
+  return v && *v && *v != '0';
 }
 
 // Kraus site probabilities + per-shot choice for a whole wave (the streamed
@@ -337,18 +354,25 @@ void kraus_decide_wave(ssb_engine* E, DevProgram& dp, uint32_t op_index, const S
   const unsigned n = dp.host.n;
   const ProgView& P = dp.view;
   const DevChannel ch = dp.host.channels[op.aux];
-  const RedSpec R = kraus_spec(P, op, ch, n);
-  const uint64_t chunk = chunk_for(c.S, (R.nq * R.nb + R.nq) * sizeof(double) + 32);
-  for (uint64_t off = 0; off < c.S; off += chunk) {
-    const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
-    uint8_t* active = static_cast<uint8_t*>(scratch(E, "active", cc.S));
-    double* val = static_cast<double*>(scratch(E, "val", cc.S * R.nq * sizeof(double)));
-    g_active_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(op, cc.S, cc.cregs, active);
-    launched(E);
-    run_reduction(E, cc, R, ch.arity == 2, active, val);
-    g_kraus_decide_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(P, op, cc.S, cc.seed, cc.ids, cc.begin, cc.u, active,
-                                                                val, scaled + 16 * off, cls + off, chosen + off, E->err);
-    launched(E);
+  uint8_t* pending = static_cast<uint8_t*>(scratch(E, "kpending", c.S));
+  double* cum = static_cast<double*>(scratch(E, "kcum", c.S * sizeof(double)));
+  g_kraus_begin_kernel<<<grid_for(c.S), NT, 0, E->stream>>>(op, c.S, c.cregs, pending, cum, chosen);
+  launched(E);
+  for (uint32_t mi = 0; mi < ch.nmat; ++mi) {
+    RedSpec R = kraus_spec(P, op, ch, n);
+    R.nq = 1;  // matrix mi only
+    R.mats += 16 * mi;
+    R.cls += mi;
+    const uint64_t chunk = chunk_for(c.S, R.nb * sizeof(double) + 16);
+    for (uint64_t off = 0; off < c.S; off += chunk) {
+      const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
+      double* val = static_cast<double*>(scratch(E, "val", cc.S * sizeof(double)));
+      run_reduction(E, cc, R, ch.arity == 2, pending + off, val);
+      g_kraus_step_kernel<<<grid_for(cc.S), NT, 0, E->stream>>>(P, op, mi, cc.S, cc.seed, cc.ids, cc.begin, cc.u,
+                                                                pending + off, val, cum + off, scaled + 16 * off,
+                                                                cls + off, chosen + off, E->err);
+      launched(E);
+    }
   }
 }
 
@@ -356,18 +380,11 @@ void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c) {
   const unsigned n = dp.host.n;
   const ProgView& P = dp.view;
   if (P.nsample == n && n >= 12) {
-    // Parallel guarded sampling (sample_block_kernel / sample_guard_kernel).
-    const uint64_t nb = ((uint64_t{1} << n) + SAMPLE_BLOCK - 1) / SAMPLE_BLOCK;
-    const uint64_t chunk = chunk_for(c.S, nb * (sizeof(double) + sizeof(int32_t)));
-    for (uint64_t off = 0; off < c.S; off += chunk) {
-      const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
-      double* bsum = static_cast<double*>(scratch(E, "bsum", cc.S * nb * sizeof(double)));
-      int32_t* blast = static_cast<int32_t*>(scratch(E, "blast", cc.S * nb * sizeof(int32_t)));
-      sample_block_kernel<<<grid_for(cc.S * nb * 32), NT, 0, E->stream>>>(P, cc.state, cc.S, bsum, blast);
-      launched(E);
-      sample_guard_kernel<<<grid_for(cc.S, 64), 64, 0, E->stream>>>(P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, bsum,
-                                                                    blast, cc.cregs, E->guard_hits, E->err,
-                                                                    guard_scale());
+    // Chunked exact parallel sampler (sample_exact_kernel), one CTA per shot.
+    for (uint64_t off = 0; off < c.S; off += (1u << 30)) {
+      const SegCtx cc = c.sub(off, std::min<uint64_t>(1u << 30, c.S - off), n);
+      sample_exact_kernel<<<static_cast<unsigned>(cc.S), SAMPLE_NT, 0, E->stream>>>(
+          P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs, E->serial_chunks, E->err, sample_force_serial());
       launched(E);
     }
     return;
@@ -456,7 +473,7 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
   const RunConfig rc = config_of(opts);
   const unsigned n = prog->dev.n;
   const uint64_t launches0 = E->launches;
-  CK(cudaMemsetAsync(E->guard_hits, 0, sizeof(unsigned long long), E->stream));
+  CK(cudaMemsetAsync(E->serial_chunks, 0, sizeof(unsigned long long), E->stream));
   const size_t rsmem = resident_smem(prog->dev);
   KernelTimer timer;
   timer.on = opts && opts->profile;
@@ -566,9 +583,9 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
   if (stats) {
     stats->dispatch_count = E->launches - launches0;
     unsigned long long hits = 0;
-    CK(cudaMemcpyAsync(&hits, E->guard_hits, sizeof hits, cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaMemcpyAsync(&hits, E->serial_chunks, sizeof hits, cudaMemcpyDeviceToHost, E->stream));
     CK(cudaStreamSynchronize(E->stream));
-    stats->sampling_guard_hits = hits;
+    stats->sampling_serial_chunks = hits;
   }
   timer.collect(stats);
 }
@@ -609,8 +626,8 @@ SSB_API int ssb_engine_create(int device, ssb_engine** out) {
     CK(cudaEventCreate(&E->ev1));
     CK(cudaMalloc(&E->err, sizeof(int)));
     CK(cudaMemset(E->err, 0, sizeof(int)));
-    CK(cudaMalloc(&E->guard_hits, sizeof(unsigned long long)));
-    CK(cudaMemset(E->guard_hits, 0, sizeof(unsigned long long)));
+    CK(cudaMalloc(&E->serial_chunks, sizeof(unsigned long long)));
+    CK(cudaMemset(E->serial_chunks, 0, sizeof(unsigned long long)));
     *out = E.release();
   });
 }
@@ -622,7 +639,7 @@ SSB_API void ssb_engine_destroy(ssb_engine* E) {
   E->programs.clear();
   for (auto& [name, slot] : E->scratch) cudaFree(slot.first);
   cudaFree(E->err);
-  cudaFree(E->guard_hits);
+  cudaFree(E->serial_chunks);
   cudaEventDestroy(E->ev0);
   cudaEventDestroy(E->ev1);
   cudaStreamDestroy(E->stream);
@@ -672,7 +689,7 @@ SSB_API int ssb_run_branch(ssb_engine* E, const ssb_program* prog, uint64_t shot
     const auto t0 = std::chrono::steady_clock::now();
     DevProgram& dp = device_program(E, prog, config_of(options).tile_k);
     uint64_t* dv = static_cast<uint64_t*>(scratch(E, "values", shot_count * sizeof(uint64_t)));
-    EngineView view{E->stream, E->err, &E->launches};
+    EngineView view{E->stream, E->err, &E->launches, E, &engine_scratch, &engine_grow};
     ssb_run_options o = options ? *options : ssb_run_options{};
     if (!options) o.branch_budget = 64;
     CK(cudaEventRecord(E->ev0, E->stream));

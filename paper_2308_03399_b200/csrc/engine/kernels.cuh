@@ -17,7 +17,23 @@
 
 #include "tile_pass.cuh"
 
+#include <algorithm>
+
 namespace ssb {
+
+// What the executors need from an engine (stream, device error flag, launch
+// counter, and its persistent grow-only device buffers: scratch(name, bytes)
+// returns a buffer of at least `bytes`; grow(name, bytes, keep) also preserves
+// the first `keep` bytes of the old contents).
+struct EngineView {
+  cudaStream_t stream;
+  int* err;
+  uint64_t* launches;
+  void* ctx;
+  void* (*scratch)(void* ctx, const char* name, size_t bytes);
+  void* (*grow)(void* ctx, const char* name, size_t bytes, size_t keep);
+};
+
 
 __device__ __forceinline__ uint64_t apply_sample_outcome(const ProgView& P, uint64_t creg, uint64_t outcome) {
   for (uint32_t i = 0; i < P.nwrites; ++i) {
@@ -498,6 +514,45 @@ static __global__ void g_active_kernel(DevOp op, uint64_t S, const uint64_t* cre
   if (s < S) active[s] = active_shot(op, cregs, s) ? 1 : 0;
 }
 
+// Early-exit Kraus selection, one matrix at a time (the reference's batch
+// "full loop", exec_batch.cpp:89-124, with apply_kraus_single's decision,
+// exec_naive.cpp:29-42): shots still pending add p_i to their cumulative and
+// settle on the first i with u < cum (or the last matrix, with its own p).
+// Only pending shots are reduced for the next matrix, so p_1.. are computed
+// for the few shots that need them.
+static __global__ void g_kraus_begin_kernel(DevOp op, uint64_t S, const uint64_t* cregs, uint8_t* pending, double* cum,
+                                            int* chosen) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const bool act = active_shot(op, cregs, s);
+  pending[s] = act ? 1 : 0;
+  cum[s] = 0.0;
+  chosen[s] = -1;
+}
+
+static __global__ void g_kraus_step_kernel(ProgView P, DevOp op, uint32_t mi, uint64_t S, uint64_t seed,
+                                           const uint64_t* ids, uint64_t begin, const double* u, uint8_t* pending,
+                                           const double* val, double* cum, double2* scaled, uint64_t* cls,
+                                           int* chosen, int* err) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= S || !pending[s]) return;
+  const DevChannel ch = P.channels[op.aux];
+  double p = val[s];
+  const double c = __dadd_rn(cum[s], p);
+  cum[s] = c;
+  if (!(draw(u, seed, ids, begin, s, op.event) < c) && mi + 1 < ch.nmat) return;
+  pending[s] = 0;
+  if (!(p > 0.0)) {
+    raise(err, DEV_DEGENERATE);
+    p = 1.0;
+  }
+  const double inv = __ddiv_rn(1.0, __dsqrt_rn(p));
+  const uint32_t slot = ch.mat_begin + mi;
+  for (int e = 0; e < 16; ++e) scaled[s * 16 + e] = c_scale(P.mats[16 * slot + e], inv);
+  cls[s] = P.scaled_cls[slot];
+  chosen[s] = static_cast<int>(mi);
+}
+
 // Kraus choice per shot (apply_kraus_single semantics on precomputed p_i):
 // writes the scaled matrix (16 double2) and its class word, or marks inactive.
 static __global__ void g_kraus_decide_kernel(ProgView P, DevOp op, uint64_t S, uint64_t seed, const uint64_t* ids,
@@ -631,95 +686,135 @@ static __global__ void g_sample_scan_kernel(ProgView P, const double2* st, uint6
   cregs[s] = apply_sample_outcome(P, cregs[s], o);
 }
 
-// Terminal sampling with every qubit sampled, parallel and still exact
-// (statevector.cpp:142-164 + 185-197 with groups = 1: p_m = |a[idx(m)]|^2, then
-// the first m with u < the SEQUENTIAL cumulative S_m).
+// Terminal sampling with every qubit sampled, in parallel and exact
+// (statevector.cpp:142-164 + 185-197 with groups = 1: p_m = |a[idx(m)]|^2,
+// then the first m with u < S_m, S_m the SEQUENTIAL fl sum p_0 + ... + p_m).
 //
-// Phase 1 (sample_block_kernel): one warp per (shot, block of SAMPLE_BLOCK
-// outcomes) sums the block's p_m in any order and records its last nonzero
-// outcome. Phase 2 (sample_guard_kernel): one thread per shot accumulates
-// block sums to the block before u, then walks outcomes with its own
-// sequential cumulative C_m. Every C_m and the reference's S_m are fl sums of
-// the same non-negative terms, so |S_m - C_m| <= Delta = (2*2^n + blocks +
-// 2*SAMPLE_BLOCK + 64) * 2^-52 * total (Higham's bound for recursive
-// summation, with slack). If the first m with C_m > u - Delta is also the first
-// with C_m > u + Delta, it is exactly the reference's pick; otherwise (|u -
-// boundary| < Delta, probability ~1e-9 per shot at n = 24) the shot is
-// re-decided by the exact single-thread sequential scan (scan_full) on device
-// and counted in `guard_hits`.
-constexpr uint32_t SAMPLE_BLOCK = 1024;
+// One CTA per shot walks the outcomes in chunks of SAMPLE_CHUNK. S is kept
+// exactly equal to the reference's running sum. For a chunk, with S in the
+// binade [2^E, 2^(E+1)) and ulp w = 2^(E-52), S = a*w with integer a in
+// [2^52, 2^53), and each reference step fl(a*w + p) = w * RNE(a + p/w) equals
+// w * (a + rint(p/w)) unless p/w is a tie (fraction exactly 1/2: the result
+// depends on a's parity) or the sum leaves the binade. So when no element of
+// the chunk is a tie and a + sum(rint(p/w)) < 2^53, the chunk advances S
+// exactly by an integer reduction, all threads in parallel. Otherwise — and
+// in the chunk where u < S first holds, where the exact index is needed —
+// thread 0 replays the chunk with the reference's sequential adds. Binade
+// changes (~n per shot) and ties are the only serial chunks besides the
+// crossing one. Fallback when no crossing: the last outcome with p > 0.
+constexpr uint32_t SAMPLE_CHUNK = 2048;
+constexpr uint32_t SAMPLE_NT = 256;
 
-static __global__ void sample_block_kernel(ProgView P, const double2* st, uint64_t S, double* bsum, int32_t* blast) {
-  const unsigned n = P.n;
-  const uint64_t nb = ((uint64_t{1} << n) + SAMPLE_BLOCK - 1) / SAMPLE_BLOCK;
-  const uint64_t warp = (uint64_t{blockIdx.x} * blockDim.x + threadIdx.x) / 32;
-  const unsigned lane = threadIdx.x & 31;
-  if (warp >= S * nb) return;
-  const uint64_t s = warp / nb, j = warp % nb;
-  const double2* a = st + (s << n);
-  const uint64_t m0 = j * SAMPLE_BLOCK, m1 = min(m0 + SAMPLE_BLOCK, uint64_t{1} << n);
-  double acc = 0.0;
-  int32_t last = -1;
-  for (uint64_t m = m0 + lane; m < m1; m += 32) {
-    const double p = c_norm(a[P.sample_identity ? m : scatter_bits(m, P.sample_qubits, n)]);
-    acc = __dadd_rn(acc, p);
-    if (p > 0.0) last = static_cast<int32_t>(m - m0);
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off /= 2) {
-    acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, off));
-    last = max(last, __shfl_down_sync(0xffffffffu, last, off));
-  }
-  if (lane == 0) {
-    bsum[warp] = acc;
-    blast[warp] = last;
-  }
-}
-
-static __global__ void sample_guard_kernel(ProgView P, const double2* st, uint64_t S, uint64_t seed,
-                                           const uint64_t* ids, uint64_t begin, const double* bsum,
-                                           const int32_t* blast, uint64_t* cregs, unsigned long long* guard_hits,
-                                           int* err, double delta_scale) {
-  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView P, const double2* st, uint64_t S,
+                                                                        uint64_t seed, const uint64_t* ids,
+                                                                        uint64_t begin, uint64_t* cregs,
+                                                                        unsigned long long* serial_chunks, int* err,
+                                                                        int force_serial) {
+  __shared__ double pbuf[SAMPLE_CHUNK];
+  __shared__ long long wsum[SAMPLE_NT / 32];
+  __shared__ int wflag[SAMPLE_NT / 32];
+  __shared__ long long wlast[SAMPLE_NT / 32];
+  __shared__ int decided;
+  __shared__ uint64_t outcome;
+  __shared__ double Ssh;
+  const uint64_t s = blockIdx.x;
   if (s >= S) return;
-  const unsigned n = P.n;
-  const uint64_t A = uint64_t{1} << n, nb = (A + SAMPLE_BLOCK - 1) / SAMPLE_BLOCK;
+  const unsigned n = P.n, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t A = uint64_t{1} << n;
   const double2* a = st + (s << n);
-  const double* B = bsum + s * nb;
-  const int32_t* Z = blast + s * nb;
   const double u = keyed_uniform(seed, shot_of(ids, begin, s), P.num_events);
-  auto amp = [&](uint64_t m) { return a[P.sample_identity ? m : scatter_bits(m, P.sample_qubits, n)]; };
-  double tot = 0.0;
-  int64_t last_nz = -1;
-  for (uint64_t j = 0; j < nb; ++j) {
-    tot = __dadd_rn(tot, B[j]);
-    if (Z[j] >= 0) last_nz = static_cast<int64_t>(j * SAMPLE_BLOCK + Z[j]);
+  if (threadIdx.x == 0) {
+    decided = 0;
+    Ssh = 0.0;
   }
-  const double delta = (2.0 * double(A) + double(nb) + 2.0 * SAMPLE_BLOCK + 64.0) * 0x1p-52 * (tot * 1.0001) * delta_scale;
-  // Skip whole blocks that end at or below u - 2 Delta.
-  double c = 0.0;
-  uint64_t j = 0;
-  while (j < nb && __dadd_rn(c, B[j]) <= u - 2.0 * delta) c = __dadd_rn(c, B[j++]);
-  int64_t hi = -1, lo = -1;
-  for (uint64_t m = j * SAMPLE_BLOCK; m < A && lo < 0; ++m) {
-    c = __dadd_rn(c, c_norm(amp(m)));
-    if (hi < 0 && c > u - delta) hi = static_cast<int64_t>(m);
-    if (c > u + delta) lo = static_cast<int64_t>(m);
+  long long last_nz = -1;  // per thread, reduced at the end
+  __syncthreads();
+  for (uint64_t c0 = 0; c0 < A; c0 += SAMPLE_CHUNK) {
+    const double Scur = Ssh;
+    // Exact-advance eligibility: S normal, its binade's ulp w.
+    int e = 0;
+    const bool normal = Scur >= 0x1p-1022;
+    const double w = normal ? ldexp(1.0, (frexp(Scur, &e), e - 53)) : 0.0;
+    long long dsum = 0;
+    int bad = (!normal || force_serial) ? 1 : 0;
+    for (uint32_t j = threadIdx.x; j < SAMPLE_CHUNK; j += SAMPLE_NT) {
+      const uint64_t m = c0 + j;
+      double p = 0.0;
+      if (m < A) p = c_norm(a[P.sample_identity ? m : scatter_bits(m, P.sample_qubits, n)]);
+      pbuf[j] = p;
+      if (p > 0.0) last_nz = static_cast<long long>(m);
+      if (normal) {
+        const double x = p / w;  // exact: division by a power of two
+        if (x >= 0x1p42) {
+          bad = 1;  // leaves the binade (and keeps the integer sum far from overflow)
+        } else {
+          if (x - floor(x) == 0.5) bad = 1;  // tie: result depends on a's parity
+          dsum += static_cast<long long>(rint(x));
+        }
+      }
+    }
+    // CTA reduction of dsum / bad.
+#pragma unroll
+    for (int off = 16; off > 0; off /= 2) {
+      dsum += __shfl_down_sync(0xffffffffu, dsum, off);
+      bad |= __shfl_down_sync(0xffffffffu, bad, off);
+    }
+    if (lane == 0) {
+      wsum[wid] = dsum;
+      wflag[wid] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long D = 0;
+      int any_bad = 0;
+      for (int i = 0; i < SAMPLE_NT / 32; ++i) {
+        D += wsum[i];
+        any_bad |= wflag[i];
+      }
+      bool serial = true;
+      if (!any_bad) {
+        const long long a0 = static_cast<long long>(Scur / w);
+        const long long a1 = a0 + D;
+        if (a1 < (1ll << 53)) {
+          const double Send = static_cast<double>(a1) * w;  // exact
+          if (!(u < Send)) {
+            Ssh = Send;  // no crossing in this chunk: advance exactly
+            serial = false;
+          }
+        }
+      }
+      if (serial) {  // the reference's own sequential adds over this chunk
+        atomicAdd(serial_chunks, 1ull);
+        double Sx = Scur;
+        const uint32_t cnt = A - c0 < SAMPLE_CHUNK ? static_cast<uint32_t>(A - c0) : SAMPLE_CHUNK;
+        for (uint32_t j = 0; j < cnt; ++j) {
+          Sx = __dadd_rn(Sx, pbuf[j]);
+          if (u < Sx) {
+            outcome = c0 + j;
+            decided = 1;
+            break;
+          }
+        }
+        Ssh = Sx;
+      }
+    }
+    __syncthreads();
+    if (decided) break;
   }
-  uint64_t o = 0;
-  bool ok = true;
-  if (lo >= 0 && lo == hi) {
-    o = static_cast<uint64_t>(lo);
-  } else if (lo < 0 && hi < 0) {
-    // No crossing anywhere (C_last <= u - Delta): the last outcome with p > 0.
-    ok = last_nz >= 0;
-    o = ok ? static_cast<uint64_t>(last_nz) : 0;
-  } else {
-    atomicAdd(guard_hits, 1ull);
-    ok = scan_full(amp, A, true, nullptr, 0, u, &o);
+  if (!decided) {  // no crossing: last outcome with p > 0 (pick_outcome fallback)
+#pragma unroll
+    for (int off = 16; off > 0; off /= 2) last_nz = max(last_nz, __shfl_down_sync(0xffffffffu, last_nz, off));
+    if (lane == 0) wlast[wid] = last_nz;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long l = -1;
+      for (int i = 0; i < SAMPLE_NT / 32; ++i) l = max(l, wlast[i]);
+      if (l < 0) raise(err, DEV_DEGENERATE);
+      outcome = l < 0 ? 0 : static_cast<uint64_t>(l);
+    }
+    __syncthreads();
   }
-  if (!ok) raise(err, DEV_DEGENERATE);
-  cregs[s] = apply_sample_outcome(P, cregs[s], o);
+  if (threadIdx.x == 0) cregs[s] = apply_sample_outcome(P, cregs[s], outcome);
 }
 
 // Terminal sampling over k < n qubits: pick over precomputed probabilities.

@@ -8,14 +8,6 @@ namespace ssb {
 
 enum DevError : int { DEV_OK = 0, DEV_DEGENERATE = 1 };
 
-// What the executors need from an engine (stream, device error flag, launch
-// counter).
-struct EngineView {
-  cudaStream_t stream;
-  int* err;
-  uint64_t* launches;
-};
-
 struct ProgView {
   const DevOp* ops;
   const DevTerm* terms;

@@ -231,14 +231,18 @@ def test_shard_concatenation(engine, oracle):
     assert (oracle.run_shots(prog, np.arange(1000), 4) == whole).all()
 
 
-def test_guarded_terminal_sampling_fallback(engine, oracle, monkeypatch):
-    """The parallel sampler's exact re-decision path: with the guard band
-    widened every shot is re-decided by the sequential scan; both paths must
-    give the reference's outcomes."""
-    prog = Program.from_text(cc.quantum_volume(12, depth=3, seed=8), cc.qv_noise())
-    want = oracle.run_shots(prog, np.arange(64), 5)
-    r = engine.run_batch(prog, RunOptions(shots=64, seed=5, resident_max_qubits=1))
-    assert (values(r) == want).all() and r.sampling_guard_hits == 0
-    monkeypatch.setenv("SHOTSIM_B200_GUARD_SCALE", "1e15")
-    r = engine.run_batch(prog, RunOptions(shots=64, seed=5, resident_max_qubits=1))
-    assert (values(r) == want).all() and r.sampling_guard_hits == 64
+def test_exact_parallel_sampling_paths(engine, oracle, monkeypatch):
+    """Terminal sampling over all qubits: the chunked exact-advance sampler and
+    its sequential replay path (forced for every chunk) both give the
+    reference's outcomes (statevector.cpp:185-197), at 12 and 14 qubits."""
+    for n, depth in ((12, 3), (14, 2)):
+        prog = Program.from_text(cc.quantum_volume(n, depth=depth, seed=8), cc.qv_noise())
+        want = oracle.run_shots(prog, np.arange(64), 5, threads=8)
+        r = engine.run_batch(prog, RunOptions(shots=64, seed=5, resident_max_qubits=1))
+        assert (values(r) == want).all()
+        if n == 14:  # 8 chunks per shot: some advance exactly in parallel
+            assert r.sampling_serial_chunks < 64 * 8
+        monkeypatch.setenv("SHOTSIM_B200_SAMPLE_SERIAL", "1")
+        r = engine.run_batch(prog, RunOptions(shots=64, seed=5, resident_max_qubits=1))
+        assert (values(r) == want).all()
+        monkeypatch.delenv("SHOTSIM_B200_SAMPLE_SERIAL")
