@@ -235,11 +235,6 @@ void assign_shape(HostDevProgram& d, Item& it, uint32_t uop_base) {
   char buf[96];
   for (uint32_t i = it.begin; i < it.end; ++i) {
     const Uop& u = d.uops[uop_base + i];
-    if (u.code == UC_KRAUS1 || u.code == UC_KRAUS2) {  // per-shot matrix: interpreter only
-      it.shape = kNoShape;
-      it.nfast = 0;
-      return;
-    }
     if (u.code == UC_PAULI) continue;
     const uint64_t cls = (u.code == UC_GEN1 || u.code == UC_GEN2) ? d.ops[u.ref].cls : 0;
     std::snprintf(buf, sizeof buf, "%u.%u.%u.%u.%u.%llx.%u;", u.code, u.qb, u.src, u.mcls, u.sigma,
@@ -299,8 +294,14 @@ void build_uops(HostDevProgram& d, PassDesc& pd, uint32_t po_begin) {
       } else if (o.kind == K_KRAUS) {
         // Per-shot matrix: staged by the tile kernel into the pass's Kraus slot.
         u.code = o.nq == 1 ? UC_KRAUS1 : UC_KRAUS2;
-        u.qb = o.nq == 1 ? static_cast<uint8_t>(0) : po.qb[0];
         u.src = po.qb[0];
+        if (o.nq == 1) {  // physical register pairs, as for 1q gates
+          const int bit = 1 << po.qb[0];
+          const int l0 = 0, l1 = bit, l2 = bit == 1 ? 2 : 1, l3 = l2 | bit;
+          u.qb = static_cast<uint8_t>(sg[l0] | (sg[l1] << 2) | (sg[l2] << 4) | (sg[l3] << 6));
+        } else {
+          u.qb = po.qb[0];
+        }
         u.mat = static_cast<uint16_t>(0xFFFF);  // patched to pd.kraus_mat below
       } else if (o.nq == 1) {
         u.code = o.mk == MK_1Q_U ? UC_U : o.mk == MK_1Q_REAL ? UC_REAL : UC_GEN1;
@@ -549,7 +550,7 @@ std::string shape_source(const HostDevProgram& d) {
     const std::vector<ShapeOp> ops = parse_shape(d.shapes[id], &fs);
     std::snprintf(buf, sizeof buf,
                   "static __device__ __forceinline__ void ssb_shape_%zu(double2* st, unsigned k, unsigned la, "
-                  "unsigned lb, const double2* m) {\n  SSB_SHAPE_BEGIN\n",
+                  "unsigned lb, const double2* m, uint64_t kcls) {\n  SSB_SHAPE_BEGIN\n",
                   id);
     src += buf;
     for (const ShapeOp& o : ops) {
@@ -564,17 +565,24 @@ std::string shape_source(const HostDevProgram& d) {
                         o.off, o.off + 1, o.off + 2, o.off + 3, a0, a1, b0, b1,
                         o.code == UC_U ? "MK_1Q_U" : o.code == UC_REAL ? "MK_1Q_REAL" : "MK_1Q_GEN", o.cls);
           break;
+        case UC_KRAUS1:  // the shot's chosen M/sqrt(p): runtime entry classes
+          std::snprintf(buf, sizeof buf,
+                        "  { const double2 mm[4] = {m[%u], m[%u], m[%u], m[%u]}; "
+                        "quad_apply1p<%u, %u, %u, %u, MK_1Q_GEN, true>(v, mm, kcls, QPT); }\n",
+                        o.off, o.off + 1, o.off + 2, o.off + 3, a0, a1, b0, b1);
+          break;
         case UC_SWAP:
           std::snprintf(buf, sizeof buf, "  quad_swap<%u, %u>(v, QPT);\n", std::min(a0, a1), std::max(a0, a1));
           break;
         case UC_PHASE:
           std::snprintf(buf, sizeof buf, "  quad_phase<%u>(v, m[%u], %uu, QPT);\n", o.qb & 3, o.off, o.mcls);
           break;
-        default:  // UC_MONO / UC_GEN2 through the logical view (constant relabeling)
+        default:  // UC_MONO / UC_GEN2 / UC_KRAUS2 through the logical view (constant relabeling)
           std::snprintf(buf, sizeof buf,
                         "  { Uop u{}; u.code = %u; u.qb = %u; u.src = %u; u.mcls = %u; u.sigma = %u;\n"
-                        "    SSB_SHAPE_LOGICAL(u, m + %u, 0x%llxull) }\n",
-                        o.code, o.qb, o.src, o.mcls, o.sigma, o.off, o.cls);
+                        "    SSB_SHAPE_LOGICAL(u, m + %u, %s) }\n",
+                        o.code, o.qb, o.src, o.mcls, o.sigma, o.off,
+                        o.code == UC_KRAUS2 ? "kcls" : (std::to_string(o.cls) + "ull").c_str());
           break;
       }
       src += buf;
@@ -583,9 +591,9 @@ std::string shape_source(const HostDevProgram& d) {
     src += buf;
   }
   src += "static __device__ __forceinline__ bool ssb_run_shape(unsigned id, double2* st, unsigned k, unsigned la, "
-         "unsigned lb, const double2* m) {\n  switch (id) {\n";
+         "unsigned lb, const double2* m, uint64_t kcls) {\n  switch (id) {\n";
   for (size_t id = 0; id < d.shapes.size(); ++id) {
-    std::snprintf(buf, sizeof buf, "    case %zu: ssb_shape_%zu(st, k, la, lb, m); return true;\n", id, id);
+    std::snprintf(buf, sizeof buf, "    case %zu: ssb_shape_%zu(st, k, la, lb, m, kcls); return true;\n", id, id);
     src += buf;
   }
   src += "    default: return false;\n  }\n}\n}  // namespace ssb\n";

@@ -59,7 +59,7 @@ __device__ __forceinline__ uint32_t insert_zero32(uint32_t i, uint32_t bit) {
 namespace ssb {
 // Static build: no specialised shapes; every segment is interpreted.
 static __device__ __forceinline__ bool ssb_run_shape(unsigned, double2*, unsigned, unsigned, unsigned,
-                                                     const double2*) {
+                                                     const double2*, uint64_t) {
   return false;
 }
 }  // namespace ssb

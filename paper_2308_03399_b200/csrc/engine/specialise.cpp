@@ -31,12 +31,12 @@ extern const char* const kJitHeaderTexts[];
 
 namespace {
 
-#ifndef SSB_QPT
-#define SSB_QPT 2
-#endif
-#ifndef SSB_TILE_MINB
-#define SSB_TILE_MINB 2
-#endif
+// The specialised kernel's straight-line shapes need few registers: one quad
+// per thread and 3 CTAs per SM (85 registers) hide the tile loads better than
+// the interpreter build's 2 quads x 2 CTAs (scripts/jit_sweep.py: C2 +5-7%,
+// C5 +9% on B200).
+#define SSB_JIT_QPT 1
+#define SSB_JIT_MINB 3
 #define SSB_STR2(x) #x
 #define SSB_STR(x) SSB_STR2(x)
 
@@ -75,8 +75,16 @@ Entry compile(const std::string& shapes) {
     warn("nvrtcCreateProgram failed");
     return e;
   }
-  const char* opts[] = {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES",
-                        "-DSSB_QPT=" SSB_STR(SSB_QPT), "-DSSB_TILE_MINB=" SSB_STR(SSB_TILE_MINB)};
+  // Tuning knobs (experiments): SHOTSIM_B200_JIT_QPT / _MINB override the
+  // quads per thread and CTAs-per-SM launch bound of the specialised kernel.
+  auto knob = [](const char* name, const char* dflt) {
+    const char* v = std::getenv(name);
+    return std::string(v && *v ? v : dflt);
+  };
+  const std::string qpt = "-DSSB_QPT=" + knob("SHOTSIM_B200_JIT_QPT", SSB_STR(SSB_JIT_QPT));
+  const std::string minb = "-DSSB_TILE_MINB=" + knob("SHOTSIM_B200_JIT_MINB", SSB_STR(SSB_JIT_MINB));
+  const char* opts[] = {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES", qpt.c_str(),
+                        minb.c_str()};
   const nvrtcResult r = nvrtcCompileProgram(prog, static_cast<int>(sizeof opts / sizeof opts[0]), opts);
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
@@ -106,7 +114,9 @@ Entry compile(const std::string& shapes) {
 const void* specialised_tile_kernel(const HostDevProgram& h) {
   if (h.shapes.empty()) return nullptr;
   if (const char* off = std::getenv("SHOTSIM_B200_NO_SPECIALISE"); off && *off && *off != '0') return nullptr;
-  const std::string src = shape_source(h);
+  const std::string src = shape_source(h) + "// " + std::to_string(std::getenv("SHOTSIM_B200_JIT_QPT") != nullptr) +
+                          (std::getenv("SHOTSIM_B200_JIT_QPT") ? std::getenv("SHOTSIM_B200_JIT_QPT") : "") +
+                          (std::getenv("SHOTSIM_B200_JIT_MINB") ? std::getenv("SHOTSIM_B200_JIT_MINB") : "") + "\n";
   std::lock_guard<std::mutex> lock(g_mu);
   auto it = g_cache.find(src);
   if (it == g_cache.end()) it = g_cache.emplace(src, compile(src)).first;

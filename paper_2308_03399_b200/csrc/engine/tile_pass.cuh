@@ -170,7 +170,7 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
           // This shot runs the segment's common case: every Pauli draw
           // identity, every condition true.
           if (it.nfast == 0 && it.sigma == 0xE4) continue;
-          if (ssb_run_shape(it.shape, tile, k, it.la, it.lb, smats + uops[it.begin].mat)) continue;
+          if (ssb_run_shape(it.shape, tile, k, it.la, it.lb, smats + uops[it.begin].mat, kraus_cls)) continue;
         }
         if (b == e && it.sigma == 0xE4) continue;  // nothing to apply and no relabeling to store
         if (k < 2) {
