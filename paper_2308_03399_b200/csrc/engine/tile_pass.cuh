@@ -161,6 +161,13 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
           tile[l] = make_double2((origin && (lo_part | hi_off[i]) == 0) ? 1.0 : 0.0, 0.0);
       } else {
         for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) tile[l] = tbase[lo_part | hi_off[i]];
+        // Warm L2 with the next tile of this shot while this one is computed,
+        // so its loads return at L2 latency (no registers, no shared memory).
+        if (t + 1 < t_end) {
+          const double2* nb = seg + pdep_positions(t + 1, hpos, n - k);
+          for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + (lo_part | hi_off[i])));
+        }
       }
       __syncthreads();
       for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
