@@ -69,8 +69,11 @@ def test_more_random_programs_vs_oracle(engine, oracle):
         assert (values(r) == want).all()
 
 
-@pytest.mark.parametrize("n,tile", [(6, 3), (8, 5), (10, 10)])
+@pytest.mark.parametrize("n,tile", [(6, 3), (8, 5), (10, 10), (12, 11), (12, 12)])
 def test_kraus_thermal_all_paths(engine, oracle, n, tile):
+    """Kraus sites through the resident kernel, the streamed passes (apply in
+    the next pass; at n >= 11 / tile >= 11 matrix 0's partials come from the
+    preceding pass's tiles) and the branch executor."""
     prog = Program.from_text(cc.random_layers(n, depth=4, seed=n), cc.thermal_noise(0.05, 0.1))
     want = oracle.run_shots(prog, np.arange(200), 3)
     for kw in ({}, dict(resident_max_qubits=1, tile_qubits=tile)):
