@@ -16,10 +16,18 @@
 // sequential scan returns because the cumulative is monotone).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <string>
 #include <cmath>
 #include <chrono>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "../capi_internal.hpp"
@@ -283,6 +291,57 @@ struct DBuf {  // named view of a persistent grow-only engine buffer
   T* get(size_t n) { return static_cast<T*>(E->scratch(E->ctx, name, std::max<size_t>(n, 1) * sizeof(T))); }
 };
 
+// Nonzero (node, key) groups, compacted in (node, key) order by CUB: gather
+// their counts and node-level parameters for the host planner.
+__global__ void b_gather_groups(const uint32_t* sel, const unsigned* num, const unsigned* counts, const double* vals,
+                                unsigned* out_cnt, double* out_val) {
+  const unsigned j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *num) return;
+  out_cnt[j] = counts[sel[j]];
+  if (vals) out_val[j] = vals[sel[j]];
+}
+
+// Dense destination table from the planner's per-group destinations.
+__global__ void b_set_dst(const uint32_t* sel, const uint64_t* gdst, uint64_t ng, uint64_t* dst) {
+  const uint64_t j = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (j < ng) dst[sel[j]] = gdst[j];
+}
+
+// advance_node for every live node in one launch when a state fits shared
+// memory (n <= 13): one CTA per node loads its state once, applies the gate
+// run [op_begin, op_end) in place (reference per-gate arithmetic,
+// kernels_scalar.cpp:24-56; conditions against the node's register) and
+// stores it once — instead of one HBM sweep of every node per gate.
+__global__ void __launch_bounds__(NT) b_gate_run_kernel(ProgView P, double2* pool, const uint32_t* slots,
+                                                        const uint64_t* cregs, uint64_t nn, unsigned n,
+                                                        uint32_t op_begin, uint32_t op_end) {
+  extern __shared__ double2 st[];
+  const uint64_t A = uint64_t{1} << n;
+  for (uint64_t x = blockIdx.x; x < nn; x += gridDim.x) {
+    double2* g = pool + (uint64_t{slots[x]} << n);
+    for (uint64_t j = threadIdx.x; j < A; j += NT) st[j] = g[j];
+    __syncthreads();
+    const uint64_t creg = cregs[x];
+    for (uint32_t i = op_begin; i < op_end; ++i) {
+      const DevOp& op = P.ops[i];
+      if (op.kind != K_GATE || op.skip) continue;
+      if (op.has_cond && (creg & op.cond_mask) != op.cond_value) continue;
+      if (op.nq == 1) {
+        double2 m[4];
+        load_matrix<2>(P.mats + 16 * op.aux, m);
+        cta_apply1(st, n, op.q[0], m, op.cls);
+      } else {
+        double2 m[16];
+        load_matrix<4>(P.mats + 16 * op.aux, m);
+        cta_apply2(st, n, op.q[0], op.q[1], m, op.cls);
+      }
+      __syncthreads();
+    }
+    for (uint64_t j = threadIdx.x; j < A; j += NT) g[j] = st[j];
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h, uint64_t shot_begin,
@@ -343,9 +402,52 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   DBuf<uint2> dpairs{&E, "branch.pairs"};
   DBuf<ChildOp> dkids{&E, "branch.kids"};
   DBuf<uint8_t> dactive{&E, "branch.active"};
+  DBuf<uint32_t> dsel{&E, "branch.sel"};
+  DBuf<unsigned> dnumsel{&E, "branch.numsel"}, dgcnt{&E, "branch.gcnt"};
+  DBuf<double> dgval{&E, "branch.gval"};
+  DBuf<uint64_t> dgdst{&E, "branch.gdst"};
+  DBuf<uint8_t> dcubtmp{&E, "branch.cubtmp"};
 
+  // Node-resident gate runs when a state fits shared memory.
+  int smem_optin = 0, dev = 0;
+  CKB(cudaGetDevice(&dev));
+  CKB(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const uint64_t gate_run_smem_max = static_cast<uint64_t>(smem_optin);
+  if (seg <= gate_run_smem_max)
+    CKB(cudaFuncSetAttribute(b_gate_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(seg)));
+  // SHOTSIM_B200_BRANCH_TRACE=1: per-phase host wall time (sync points) to stderr.
+  const bool tracing = [] {
+    const char* v = std::getenv("SHOTSIM_B200_BRANCH_TRACE");
+    return v && *v && *v != '0';
+  }();
+  std::map<std::string, double> trace_t;
+  auto trace_last = std::chrono::steady_clock::now();
+  auto trace_sync = [&](const char* tag) {
+    CKB(cudaStreamSynchronize(s));
+    if (!tracing) return;
+    const auto now = std::chrono::steady_clock::now();
+    trace_t[tag] += std::chrono::duration<double>(now - trace_last).count();
+    trace_last = now;
+  };
+  // Pinned staging for every host->device table (async copies, no pageable
+  // bounce); each name is rewritten only after the next stream sync.
+  auto pinned = [&](const char* name, size_t count, auto* type_tag) {
+    using T = std::remove_pointer_t<decltype(type_tag)>;
+    return static_cast<T*>(E.host(E.ctx, name, std::max<size_t>(count, 1) * sizeof(T)));
+  };
   uint64_t peak = 0, passes = 0;
   std::vector<HostNode> live;
+  // Planner work arrays, reused across sites (no per-site allocation).
+  struct Cand {
+    uint64_t parent;
+    uint32_t key;
+    uint64_t count;
+    double val;
+  };
+  std::vector<Cand> groups;
+  std::vector<uint8_t> keep, parent_used, parent_kept;
+  std::vector<uint2> pairs;
+  std::vector<ChildOp> kids;
   while (nwaiting > 0) {
     ++passes;
     std::swap(cur_shots, waiting);  // waiting list becomes this pass's root
@@ -369,36 +471,44 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       const uint64_t nn = live.size();
       // advance_node (exec_branch.cpp:155-162): gates over all live nodes.
       if (j > i) {
-        std::vector<uint32_t> hs(nn);
-        std::vector<uint64_t> hc(nn);
+        uint32_t* hs = pinned("branch.h_gslots", nn, (uint32_t*)nullptr);
+        uint64_t* hc = pinned("branch.h_gcregs", nn, (uint64_t*)nullptr);
         for (uint64_t x = 0; x < nn; ++x) {
           hs[x] = live[x].slot;
           hc[x] = live[x].creg;
         }
         uint32_t* slots = dslots.get(nn);
         uint64_t* cregs = dcreg.get(nn);
-        CKB(cudaMemcpyAsync(slots, hs.data(), nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        CKB(cudaMemcpyAsync(cregs, hc.data(), nn * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-        for (uint32_t k = i; k < j; ++k) {
-          const DevOp& op = h.ops[k];
-          if (op.kind != K_GATE || op.skip) continue;
-          const uint64_t work = nn << (n - op.nq);
-          if (op.nq == 1) g_gate_kernel<1><<<gridn(work), NT, 0, s>>>(pool, nn, n, op, P.mats, cregs, slots);
-          else g_gate_kernel<2><<<gridn(work), NT, 0, s>>>(pool, nn, n, op, P.mats, cregs, slots);
+        CKB(cudaMemcpyAsync(slots, hs, nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        CKB(cudaMemcpyAsync(cregs, hc, nn * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        uint32_t ngates = 0;
+        for (uint32_t k = i; k < j; ++k) ngates += h.ops[k].kind == K_GATE && !h.ops[k].skip;
+        if (ngates > 1 && seg <= gate_run_smem_max) {
+          b_gate_run_kernel<<<static_cast<unsigned>(std::min<uint64_t>(nn, 1u << 20)), NT, seg, s>>>(
+              P, pool, slots, cregs, nn, n, i, j);
           launched();
+        } else {
+          for (uint32_t k = i; k < j; ++k) {
+            const DevOp& op = h.ops[k];
+            if (op.kind != K_GATE || op.skip) continue;
+            const uint64_t work = nn << (n - op.nq);
+            if (op.nq == 1) g_gate_kernel<1><<<gridn(work), NT, 0, s>>>(pool, nn, n, op, P.mats, cregs, slots);
+            else g_gate_kernel<2><<<gridn(work), NT, 0, s>>>(pool, nn, n, op, P.mats, cregs, slots);
+            launched();
+          }
         }
-        CKB(cudaStreamSynchronize(s));  // host vectors hs/hc die here
+        trace_sync("gates");  // host vectors hs/hc die here
       }
       if (j == h.end) break;
       const DevOp site = h.ops[j];
 
       // Node table with condition flags.
-      std::vector<DevNode> hn(nn);
+      DevNode* hn = pinned("branch.h_nodes", nn, (DevNode*)nullptr);
       for (uint64_t x = 0; x < nn; ++x)
         hn[x] = {live[x].slot, !site.has_cond || (live[x].creg & site.cond_mask) == site.cond_value ? 1u : 0u,
                  live[x].off, live[x].len, live[x].creg};
       DevNode* nodes = dnodes.get(nn);
-      CKB(cudaMemcpyAsync(nodes, hn.data(), nn * sizeof(DevNode), cudaMemcpyHostToDevice, s));
+      CKB(cudaMemcpyAsync(nodes, hn, nn * sizeof(DevNode), cudaMemcpyHostToDevice, s));
 
       uint32_t nkeys = 1;
       double* vals = nullptr;
@@ -441,23 +551,23 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
           R.blk = G <= SUM_BLOCK ? G : SUM_BLOCK;
           nkeys = R.nq;
         }
-        std::vector<uint32_t> hs(nn);
-        std::vector<uint8_t> ha(nn);
+        uint32_t* hs = pinned("branch.h_rslots", nn, (uint32_t*)nullptr);
+        uint8_t* ha = pinned("branch.h_ractive", nn, (uint8_t*)nullptr);
         for (uint64_t x = 0; x < nn; ++x) {
           hs[x] = live[x].slot;
           ha[x] = static_cast<uint8_t>(hn[x].cond_ok);
         }
         uint32_t* slots = dslots.get(nn);
         uint8_t* active = dactive.get(nn);
-        CKB(cudaMemcpyAsync(slots, hs.data(), nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        CKB(cudaMemcpyAsync(active, ha.data(), nn, cudaMemcpyHostToDevice, s));
+        CKB(cudaMemcpyAsync(slots, hs, nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        CKB(cudaMemcpyAsync(active, ha, nn, cudaMemcpyHostToDevice, s));
         double* part = dpart.get(nn * R.nq * R.nb);
         vals = dvals.get(nn * R.nq);
         launch_reduce(s, pool, nn, R, active, part, slots);
         launched();
         g_finish_kernel<<<static_cast<unsigned>(std::min<uint64_t>(nn * R.nq, 1u << 20)), NT, 0, s>>>(nn, R.nq, R.nb, tree, active, part, vals);
         launched();
-        CKB(cudaStreamSynchronize(s));
+        trace_sync("reduce");
       }
 
       // Per-shot decisions and group counts.
@@ -469,26 +579,37 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       b_decide<<<gridn(total), NT, 0, s>>>(P, site, nodes, nn, cur_shots, total, seed, vals, nkeys, keys, counts,
                                            E.err);
       launched();
-      std::vector<unsigned> hcount(nn * nkeys);
-      std::vector<double> hvals;
-      CKB(cudaMemcpyAsync(hcount.data(), counts, hcount.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-      if (vals) {
-        hvals.resize(nn * nkeys);
-        CKB(cudaMemcpyAsync(hvals.data(), vals, hvals.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-      }
-      CKB(cudaStreamSynchronize(s));
+      // Compact the nonzero groups on the device; only they cross to the host.
+      const uint64_t ncells = nn * nkeys;
+      if (ncells >= (uint64_t{1} << 32)) throw std::length_error("branch group table too large");
+      uint32_t* sel = dsel.get(ncells);
+      unsigned* dnum = dnumsel.get(1);
+      size_t tmp_bytes = 0;
+      cub::CountingInputIterator<uint32_t> cells(0);
+      CKB(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, cells, counts, sel, dnum, static_cast<int>(ncells), s));
+      void* tmp = dcubtmp.get(tmp_bytes);
+      CKB(cub::DeviceSelect::Flagged(tmp, tmp_bytes, cells, counts, sel, dnum, static_cast<int>(ncells), s));
+      unsigned* gcnt = dgcnt.get(ncells);
+      double* gval = vals ? dgval.get(ncells) : nullptr;
+      b_gather_groups<<<gridn(ncells), NT, 0, s>>>(sel, dnum, counts, vals, gcnt, gval);
+      launched();
+      unsigned* hnum = static_cast<unsigned*>(E.host(E.ctx, "branch.hnum", sizeof(unsigned)));
+      CKB(cudaMemcpyAsync(hnum, dnum, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      trace_sync("decide_num");
+      const uint64_t ng = *hnum;
+      uint32_t* hsel = static_cast<uint32_t*>(E.host(E.ctx, "branch.hsel", std::max<uint64_t>(ng, 1) * 4));
+      unsigned* hgc = static_cast<unsigned*>(E.host(E.ctx, "branch.hgc", std::max<uint64_t>(ng, 1) * 4));
+      double* hgv = static_cast<double*>(E.host(E.ctx, "branch.hgv", std::max<uint64_t>(ng, 1) * 8));
+      CKB(cudaMemcpyAsync(hsel, sel, ng * 4, cudaMemcpyDeviceToHost, s));
+      CKB(cudaMemcpyAsync(hgc, gcnt, ng * 4, cudaMemcpyDeviceToHost, s));
+      if (gval) CKB(cudaMemcpyAsync(hgv, gval, ng * 8, cudaMemcpyDeviceToHost, s));
+      trace_sync("decide_groups");
 
       // Groups in (parent, key) order; budget policy (exec_branch.cpp:217-255).
-      struct Cand {
-        uint64_t parent;
-        uint32_t key;
-        uint64_t count;
-      };
-      std::vector<Cand> groups;
-      for (uint64_t x = 0; x < nn; ++x)
-        for (uint32_t k = 0; k < nkeys; ++k)
-          if (hcount[x * nkeys + k]) groups.push_back({x, k, hcount[x * nkeys + k]});
-      std::vector<uint8_t> keep(groups.size(), 1);
+      groups.resize(ng);
+      for (uint64_t g = 0; g < ng; ++g)
+        groups[g] = {hsel[g] / nkeys, hsel[g] % nkeys, hgc[g], gval ? hgv[g] : 0.0};
+      keep.assign(groups.size(), 1);
       if (groups.size() > budget) {
         std::vector<size_t> order(groups.size());
         std::iota(order.begin(), order.end(), 0);
@@ -502,22 +623,23 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       }
       // Children (materialize, exec_branch.cpp:141-153) and shot destinations.
       std::vector<HostNode> next;
-      std::vector<uint64_t> hdst(nn * nkeys, 0);
-      std::vector<uint2> pairs;
-      std::vector<ChildOp> kids;
+      next.reserve(std::min<uint64_t>(ng, budget));
+      uint64_t* hgdst = static_cast<uint64_t*>(E.host(E.ctx, "branch.hgdst", std::max<uint64_t>(ng, 1) * 8));
+      pairs.clear();
+      kids.clear();
       uint64_t new_off = 0, wait_off = nwaiting;
       // Parents without a kept child die first, so the pool never holds more
       // than `budget` live states (+ the root).
-      std::vector<uint8_t> parent_used(nn, 0), parent_kept(nn, 0);
+      parent_used.assign(nn, 0);
+      parent_kept.assign(nn, 0);
       for (size_t g = 0; g < groups.size(); ++g)
         if (keep[g]) parent_kept[groups[g].parent] = 1;
       for (uint64_t x = 0; x < nn; ++x)
         if (!parent_kept[x]) free_slots.push_back(live[x].slot);
       for (size_t g = 0; g < groups.size(); ++g) {
         const Cand& c = groups[g];
-        const uint64_t gi = c.parent * nkeys + c.key;
         if (!keep[g]) {
-          hdst[gi] = (uint64_t{1} << 63) | wait_off;
+          hgdst[g] = (uint64_t{1} << 63) | wait_off;
           wait_off += c.count;
           continue;
         }
@@ -536,7 +658,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
         if (transform) {
           double inv = 1.0;
           if (site.kind != K_PAULI) {
-            const double param = hvals[c.parent * nkeys + c.key];
+            const double param = c.val;
             if (!(param > 0.0)) throw shotsim::DegenerateDistribution("branch has zero probability");
             inv = 1.0 / std::sqrt(param);
           }
@@ -545,30 +667,37 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
             for (unsigned b = 0; b < site.nq; ++b)
               creg = (creg & ~(uint64_t{1} << site.c[b])) | (((uint64_t{c.key} >> b) & 1) << site.c[b]);
         }
-        hdst[gi] = new_off;
+        hgdst[g] = new_off;
         next.push_back({slot, new_off, c.count, creg});
         new_off += c.count;
       }
 
       uint64_t* dst = ddst.get(nn * nkeys);
       unsigned long long* cursor = dcursor.get(nn * nkeys);
-      CKB(cudaMemcpyAsync(dst, hdst.data(), hdst.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+      uint64_t* gdst = dgdst.get(std::max<uint64_t>(ng, 1));
+      CKB(cudaMemcpyAsync(gdst, hgdst, ng * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+      b_set_dst<<<gridn(std::max<uint64_t>(ng, 1)), NT, 0, s>>>(sel, gdst, ng, dst);
+      launched();
       CKB(cudaMemsetAsync(cursor, 0, nn * nkeys * sizeof(unsigned long long), s));
       b_scatter<<<gridn(total), NT, 0, s>>>(nodes, nn, cur_shots, total, keys, nkeys, dst, cursor, nxt_shots, waiting);
       launched();
       if (!pairs.empty()) {
         uint2* dp = dpairs.get(pairs.size());
-        CKB(cudaMemcpyAsync(dp, pairs.data(), pairs.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+        uint2* hp = pinned("branch.h_pairs", pairs.size(), (uint2*)nullptr);
+        std::copy(pairs.begin(), pairs.end(), hp);
+        CKB(cudaMemcpyAsync(dp, hp, pairs.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
         b_copy_slots<<<gridn(pairs.size() * A), NT, 0, s>>>(pool, dp, pairs.size(), n);
         launched();
       }
       if (!kids.empty()) {
         ChildOp* dk = dkids.get(kids.size());
-        CKB(cudaMemcpyAsync(dk, kids.data(), kids.size() * sizeof(ChildOp), cudaMemcpyHostToDevice, s));
+        ChildOp* hk = pinned("branch.h_kids", kids.size(), (ChildOp*)nullptr);
+        std::copy(kids.begin(), kids.end(), hk);
+        CKB(cudaMemcpyAsync(dk, hk, kids.size() * sizeof(ChildOp), cudaMemcpyHostToDevice, s));
         b_apply<<<gridn(kids.size() * (A / 2)), NT, 0, s>>>(P, site, pool, dk, kids.size(), n);
         launched();
       }
-      CKB(cudaStreamSynchronize(s));
+      trace_sync("apply");
       nwaiting = wait_off;
       std::swap(cur_shots, nxt_shots);
       live = std::move(next);
@@ -628,6 +757,8 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       CKB(cudaStreamSynchronize(s));
     }
   }
+  if (tracing)
+    for (auto& [k, v] : trace_t) std::fprintf(stderr, "branch trace %-14s %.3f s\n", k.c_str(), v);
   if (stats) {
     stats->peak_states = peak;
     stats->passes = passes;

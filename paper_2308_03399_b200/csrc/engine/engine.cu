@@ -50,6 +50,7 @@ struct ssb_engine {
   unsigned long long* serial_chunks = nullptr;  // sampling chunks replayed sequentially
   std::map<std::pair<uint64_t, unsigned>, std::unique_ptr<ssb::DevProgram>> programs;
   std::map<std::string, std::pair<void*, size_t>> scratch;
+  std::map<std::string, std::pair<void*, size_t>> host_scratch;  // pinned
   uint64_t launches = 0;
 };
 
@@ -98,6 +99,21 @@ void* engine_grow(void* ctx, const char* name, size_t bytes, size_t keep) {
   slot.first = np;
   slot.second = bytes;
   return np;
+}
+
+void* engine_host(void* ctx, const char* name, size_t bytes) {
+  ssb_engine* E = static_cast<ssb_engine*>(ctx);
+  auto& slot = E->host_scratch[name];
+  if (slot.second < bytes) {
+    CK(cudaStreamSynchronize(E->stream));
+    if (slot.first) CK(cudaFreeHost(slot.first));
+    slot.first = nullptr;
+    slot.second = 0;
+    const size_t cap = std::max<size_t>(bytes, 1 << 16) * 2;
+    CK(cudaMallocHost(&slot.first, cap));
+    slot.second = cap;
+  }
+  return slot.first;
 }
 
 template <class T>
@@ -638,6 +654,7 @@ SSB_API void ssb_engine_destroy(ssb_engine* E) {
   cudaStreamSynchronize(E->stream);
   E->programs.clear();
   for (auto& [name, slot] : E->scratch) cudaFree(slot.first);
+  for (auto& [name, slot] : E->host_scratch) cudaFreeHost(slot.first);
   cudaFree(E->err);
   cudaFree(E->serial_chunks);
   cudaEventDestroy(E->ev0);
@@ -689,7 +706,7 @@ SSB_API int ssb_run_branch(ssb_engine* E, const ssb_program* prog, uint64_t shot
     const auto t0 = std::chrono::steady_clock::now();
     DevProgram& dp = device_program(E, prog, config_of(options).tile_k);
     uint64_t* dv = static_cast<uint64_t*>(scratch(E, "values", shot_count * sizeof(uint64_t)));
-    EngineView view{E->stream, E->err, &E->launches, E, &engine_scratch, &engine_grow};
+    EngineView view{E->stream, E->err, &E->launches, E, &engine_scratch, &engine_grow, &engine_host};
     ssb_run_options o = options ? *options : ssb_run_options{};
     if (!options) o.branch_budget = 64;
     CK(cudaEventRecord(E->ev0, E->stream));

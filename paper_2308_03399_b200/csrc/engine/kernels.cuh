@@ -32,6 +32,7 @@ struct EngineView {
   void* ctx;
   void* (*scratch)(void* ctx, const char* name, size_t bytes);
   void* (*grow)(void* ctx, const char* name, size_t bytes, size_t keep);
+  void* (*host)(void* ctx, const char* name, size_t bytes);  // pinned host, grow-only
 };
 
 
