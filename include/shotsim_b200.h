@@ -210,6 +210,13 @@ SSB_API int ssb_run_branch(ssb_engine* engine, const ssb_program* program, uint6
 SSB_API int ssb_histogram_device(ssb_engine* engine, const uint64_t* values_device,
                                  uint64_t count, uint32_t num_clbits, uint64_t* hist_device);
 
+/* Plans `program` for the HBM-streamed executor with `tile_qubits` local
+ * qubits (0: default) and compiles its shape-specialised tile kernel with
+ * NVRTC for sm_100a without loading it (no GPU needed). *shapes receives the
+ * number of distinct segment shapes; on failure the NVRTC log is in
+ * ssb_last_error(). */
+SSB_API int ssb_program_specialise_check(const ssb_program* program, uint32_t tile_qubits, uint32_t* shapes);
+
 /* FP64-pipe roofline probe: the sustained rate of rounded DMUL/DADD (no FMA,
  * the engine's arithmetic) over the whole device, in FP64 ops per second,
  * measured with CUDA events (the denominator of bench.py's fp64 roofline). */

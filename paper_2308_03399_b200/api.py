@@ -48,6 +48,13 @@ class Program:
         check(load().ssb_program_flat(self._h, C.byref(f)))
         return f
 
+    def specialise_check(self, tile_qubits: int = 0) -> int:
+        """Compiles the program's shape-specialised tile kernel with NVRTC
+        (no GPU needed); returns the number of segment shapes."""
+        n = C.c_uint32(0)
+        check(load().ssb_program_specialise_check(self._h, tile_qubits, C.byref(n)))
+        return n.value
+
     def dump(self) -> str:
         n = C.c_size_t()
         check(load().ssb_program_dump(self._h, None, 0, C.byref(n)))

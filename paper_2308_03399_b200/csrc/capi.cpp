@@ -88,3 +88,19 @@ SSB_API int ssb_counts_checksum(const uint64_t* values, uint64_t count, uint32_t
 }
 
 }  // extern "C"
+
+namespace ssb {
+bool specialise_compile_check(const HostDevProgram& h, std::string* log);
+}
+
+extern "C" SSB_API int ssb_program_specialise_check(const ssb_program* program, uint32_t tile_qubits,
+                                                   uint32_t* shapes) {
+  return ssb::guard([&] {
+    if (!program || !shapes) throw std::invalid_argument("null argument");
+    ssb::HostDevProgram h = program->dev;
+    ssb::plan_passes(h, tile_qubits ? std::max(3u, std::min(13u, tile_qubits)) : 12u);
+    *shapes = static_cast<uint32_t>(h.shapes.size());
+    std::string log;
+    if (!ssb::specialise_compile_check(h, &log)) throw ssb::CudaError("shape specialisation failed: " + log);
+  });
+}

@@ -63,8 +63,9 @@ void warn(const std::string& what) {
                what.c_str());
 }
 
-Entry compile(const std::string& shapes) {
-  Entry e;
+// NVRTC: shape source + embedded engine headers -> sm_100a cubin. Returns an
+// empty vector (and the log) on failure. Needs no GPU.
+std::vector<char> build_cubin(const std::string& shapes, std::string* log_out) {
   std::vector<const char*> names(kJitHeaderNames, kJitHeaderNames + kJitHeaderCount);
   std::vector<const char*> texts(kJitHeaderTexts, kJitHeaderTexts + kJitHeaderCount);
   names.push_back("ssb_shapes.inc");
@@ -72,8 +73,8 @@ Entry compile(const std::string& shapes) {
   nvrtcProgram prog = nullptr;
   if (nvrtcCreateProgram(&prog, kMain, "ssb_tile_pass_jit.cu", static_cast<int>(names.size()), texts.data(),
                          names.data()) != NVRTC_SUCCESS) {
-    warn("nvrtcCreateProgram failed");
-    return e;
+    *log_out = "nvrtcCreateProgram failed";
+    return {};
   }
   // Tuning knobs (experiments): SHOTSIM_B200_JIT_QPT / _MINB override the
   // quads per thread and CTAs-per-SM launch bound of the specialised kernel.
@@ -91,15 +92,26 @@ Entry compile(const std::string& shapes) {
     nvrtcGetProgramLogSize(prog, &n);
     std::string log(n, '\0');
     nvrtcGetProgramLog(prog, log.data());
-    warn(std::string(nvrtcGetErrorString(r)) + ": " + log.substr(0, 2000));
+    *log_out = std::string(nvrtcGetErrorString(r)) + ": " + log.substr(0, 4000);
     nvrtcDestroyProgram(&prog);
-    return e;
+    return {};
   }
   size_t size = 0;
   nvrtcGetCUBINSize(prog, &size);
   std::vector<char> cubin(size);
   nvrtcGetCUBIN(prog, cubin.data());
   nvrtcDestroyProgram(&prog);
+  return cubin;
+}
+
+Entry compile(const std::string& shapes) {
+  Entry e;
+  std::string log;
+  const std::vector<char> cubin = build_cubin(shapes, &log);
+  if (cubin.empty()) {
+    warn(log);
+    return e;
+  }
   if (cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
       cudaLibraryGetKernel(&e.kernel, e.lib, "ssb_tile_pass_jit") != cudaSuccess) {
     cudaGetLastError();
@@ -110,6 +122,14 @@ Entry compile(const std::string& shapes) {
 }
 
 }  // namespace
+
+bool specialise_compile_check(const HostDevProgram& h, std::string* log) {
+  if (h.shapes.empty()) {
+    *log = "plan has no segment shapes";
+    return false;
+  }
+  return !build_cubin(shape_source(h), log).empty();
+}
 
 const void* specialised_tile_kernel(const HostDevProgram& h) {
   if (h.shapes.empty()) return nullptr;

@@ -46,3 +46,13 @@ def test_flat_program_roundtrip():
     _lib.check(_lib.load().ssb_program_from_flat(C.byref(flat), C.byref(h)))
     q = Program(h.value)
     assert q.dump() == p.dump()
+
+
+@pytest.mark.parametrize("key,tile", [("C2", 12), ("C4", 12), ("C5", 12), ("C2", 11)])
+def test_shape_specialisation_compiles_without_gpu(key, tile):
+    """The run-time specialiser's generated source (shape executors + the
+    engine's embedded device headers) compiles with NVRTC for sm_100a."""
+    from paper_2308_03399_b200 import Program, circuits as cc
+    cfg = cc.CONFIGS[key]
+    prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
+    assert prog.specialise_check(tile) > 0
