@@ -235,7 +235,12 @@ void assign_shape(HostDevProgram& d, Item& it, uint32_t uop_base) {
   char buf[96];
   for (uint32_t i = it.begin; i < it.end; ++i) {
     const Uop& u = d.uops[uop_base + i];
-    if (u.code == UC_PAULI) continue;
+    if (u.code == UC_PAULI) {
+      // Position and register map only: the draw is per shot (noisy variant).
+      std::snprintf(buf, sizeof buf, "P.%u.%u;", u.sigma, i - it.begin);
+      key += buf;
+      continue;
+    }
     const uint64_t cls = (u.code == UC_GEN1 || u.code == UC_GEN2) ? d.ops[u.ref].cls : 0;
     std::snprintf(buf, sizeof buf, "%u.%u.%u.%u.%u.%llx.%u;", u.code, u.qb, u.src, u.mcls, u.sigma,
                   static_cast<unsigned long long>(cls), static_cast<unsigned>(u.mat - mat0));
@@ -518,6 +523,7 @@ namespace {
 struct ShapeOp {
   unsigned code, qb, src, mcls, sigma, off;
   unsigned long long cls;
+  unsigned pos;  // UC_PAULI: index within the item (per-shot draw table)
 };
 
 std::vector<ShapeOp> parse_shape(const std::string& key, unsigned* final_sigma) {
@@ -525,6 +531,13 @@ std::vector<ShapeOp> parse_shape(const std::string& key, unsigned* final_sigma) 
   size_t i = 0;
   while (i < key.size() && key[i] != '|') {
     ShapeOp o{};
+    if (key[i] == 'P') {
+      o.code = UC_PAULI;
+      if (std::sscanf(key.c_str() + i, "P.%u.%u;", &o.sigma, &o.pos) != 2) throw std::logic_error("bad shape key");
+      ops.push_back(o);
+      i = key.find(';', i) + 1;
+      continue;
+    }
     if (std::sscanf(key.c_str() + i, "%u.%u.%u.%u.%u.%llx.%u;", &o.code, &o.qb, &o.src, &o.mcls, &o.sigma, &o.cls,
                     &o.off) != 7)
       throw std::logic_error("bad shape key");
@@ -548,14 +561,20 @@ std::string shape_source(const HostDevProgram& d) {
   for (size_t id = 0; id < d.shapes.size(); ++id) {
     unsigned fs = 0;
     const std::vector<ShapeOp> ops = parse_shape(d.shapes[id], &fs);
+    // NOISY = 0: every Pauli draw of the shot identity (skipped); NOISY = 1:
+    // some drew a Pauli — applied where pinfo[pos] != 0xFF (uniform branch).
     std::snprintf(buf, sizeof buf,
-                  "static __device__ __forceinline__ void ssb_shape_%zu(double2* st, unsigned k, unsigned la, "
-                  "unsigned lb, const double2* m, uint64_t kcls) {\n  SSB_SHAPE_BEGIN\n",
+                  "template <int NOISY>\nstatic __device__ __forceinline__ void ssb_shape_%zu(double2* st, unsigned k, "
+                  "unsigned la, unsigned lb, const double2* m, uint64_t kcls, const uint8_t* pinfo) {\n"
+                  "  SSB_SHAPE_BEGIN\n",
                   id);
     src += buf;
     for (const ShapeOp& o : ops) {
       const unsigned a0 = o.qb & 3, a1 = (o.qb >> 2) & 3, b0 = (o.qb >> 4) & 3, b1 = (o.qb >> 6) & 3;
       switch (o.code) {
+        case UC_PAULI:
+          std::snprintf(buf, sizeof buf, "  if (NOISY) { SSB_SHAPE_PAULI(%u, pinfo[%u]) }\n", o.sigma, o.pos);
+          break;
         case UC_U:
         case UC_REAL:
         case UC_GEN1:
@@ -590,10 +609,13 @@ std::string shape_source(const HostDevProgram& d) {
     std::snprintf(buf, sizeof buf, "  SSB_SHAPE_END(%u)\n}\n", fs);
     src += buf;
   }
-  src += "static __device__ __forceinline__ bool ssb_run_shape(unsigned id, double2* st, unsigned k, unsigned la, "
-         "unsigned lb, const double2* m, uint64_t kcls) {\n  switch (id) {\n";
+  src += "static __device__ __forceinline__ bool ssb_run_shape(unsigned id, bool noisy, double2* st, unsigned k, "
+         "unsigned la, unsigned lb, const double2* m, uint64_t kcls, const uint8_t* pinfo) {\n  switch (id) {\n";
   for (size_t id = 0; id < d.shapes.size(); ++id) {
-    std::snprintf(buf, sizeof buf, "    case %zu: ssb_shape_%zu(st, k, la, lb, m, kcls); return true;\n", id, id);
+    std::snprintf(buf, sizeof buf,
+                  "    case %zu: if (noisy) ssb_shape_%zu<1>(st, k, la, lb, m, kcls, pinfo); "
+                  "else ssb_shape_%zu<0>(st, k, la, lb, m, kcls, pinfo); return true;\n",
+                  id, id, id);
     src += buf;
   }
   src += "    default: return false;\n  }\n}\n}  // namespace ssb\n";

@@ -39,6 +39,21 @@ __device__ __forceinline__ uint32_t insert_zero32(uint32_t i, uint32_t bit) {
     _Pragma("unroll") for (int e = 0; e < 4; ++e) v[q][e] = x.e[e];                  \
   }
 
+// A drawn Pauli on every quad through the (constant) logical view; pv packs
+// xq | zq << 2 | (num_y & 3) << 4 (tile_pass compaction).
+#define SSB_SHAPE_PAULI(SIGMA, PV)                                                   \
+  {                                                                                  \
+    const unsigned pv_ = (PV);                                                       \
+    if (pv_ != 0xFFu) {                                                              \
+      _Pragma("unroll") for (int q = 0; q < QPT; ++q) {                              \
+        double2 L[4];                                                                \
+        gather_logical(v[q], SIGMA, L);                                              \
+        quad_pauli1(L, pv_ & 3u, (pv_ >> 2) & 3u, (pv_ >> 4) & 3u);                  \
+        scatter_logical(v[q], SIGMA, L);                                             \
+      }                                                                              \
+    }                                                                                \
+  }
+
 #define SSB_SHAPE_END(SIGMA)                                                         \
     _Pragma("unroll") for (int q = 0; q < QPT; ++q) {                                \
       double2 L[4];                                                                  \
@@ -58,8 +73,8 @@ __device__ __forceinline__ uint32_t insert_zero32(uint32_t i, uint32_t bit) {
 #else
 namespace ssb {
 // Static build: no specialised shapes; every segment is interpreted.
-static __device__ __forceinline__ bool ssb_run_shape(unsigned, double2*, unsigned, unsigned, unsigned,
-                                                     const double2*, uint64_t) {
+static __device__ __forceinline__ bool ssb_run_shape(unsigned, bool, double2*, unsigned, unsigned, unsigned,
+                                                     const double2*, uint64_t, const uint8_t*) {
   return false;
 }
 }  // namespace ssb

@@ -14,8 +14,12 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <unistd.h>
+
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <filesystem>
 #include <map>
 #include <mutex>
 #include <string>
@@ -104,10 +108,71 @@ std::vector<char> build_cubin(const std::string& shapes, std::string* log_out) {
   return cubin;
 }
 
+// On-disk cubin cache: $SHOTSIM_B200_CACHE (default ~/.cache/shotsim_b200),
+// keyed by a 64-bit FNV-1a hash of everything that determines the cubin (the
+// shape source, the embedded headers, the compile knobs).
+std::string cache_path(const std::string& shapes) {
+  const char* dir = std::getenv("SHOTSIM_B200_CACHE");
+  std::string d;
+  if (dir && *dir) {
+    d = dir;
+  } else if (const char* home = std::getenv("HOME"); home && *home) {
+    d = std::string(home) + "/.cache/shotsim_b200";
+  } else {
+    return "";
+  }
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&h](const char* p, size_t n) {
+    for (size_t i = 0; i < n; ++i) h = (h ^ static_cast<unsigned char>(p[i])) * 1099511628211ull;
+  };
+  mix(shapes.data(), shapes.size());
+  for (int i = 0; i < kJitHeaderCount; ++i) mix(kJitHeaderTexts[i], std::strlen(kJitHeaderTexts[i]));
+  for (const char* k : {"SHOTSIM_B200_JIT_QPT", "SHOTSIM_B200_JIT_MINB"})
+    if (const char* v = std::getenv(k)) mix(v, std::strlen(v));
+  char name[64];
+  std::snprintf(name, sizeof name, "/tile_pass_%016llx.cubin", static_cast<unsigned long long>(h));
+  return d + name;
+}
+
+std::vector<char> read_file(const std::string& path) {
+  std::vector<char> out;
+  if (path.empty()) return out;
+  if (FILE* f = std::fopen(path.c_str(), "rb")) {
+    std::fseek(f, 0, SEEK_END);
+    const long n = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    if (n > 0) {
+      out.resize(static_cast<size_t>(n));
+      if (std::fread(out.data(), 1, out.size(), f) != out.size()) out.clear();
+    }
+    std::fclose(f);
+  }
+  return out;
+}
+
+void write_file_atomic(const std::string& path, const std::vector<char>& data) {
+  if (path.empty()) return;
+  const std::string dir = path.substr(0, path.rfind('/'));
+  std::error_code ec;
+  std::filesystem::create_directories(dir, ec);
+  const std::string tmp = path + ".tmp" + std::to_string(static_cast<long long>(getpid()));
+  if (FILE* f = std::fopen(tmp.c_str(), "wb")) {
+    const bool ok = std::fwrite(data.data(), 1, data.size(), f) == data.size();
+    std::fclose(f);
+    if (ok) std::filesystem::rename(tmp, path, ec);
+    else std::filesystem::remove(tmp, ec);
+  }
+}
+
 Entry compile(const std::string& shapes) {
   Entry e;
   std::string log;
-  const std::vector<char> cubin = build_cubin(shapes, &log);
+  const std::string cpath = cache_path(shapes);
+  std::vector<char> cubin = read_file(cpath);
+  if (cubin.empty()) {
+    cubin = build_cubin(shapes, &log);
+    if (!cubin.empty()) write_file_atomic(cpath, cubin);
+  }
   if (cubin.empty()) {
     warn(log);
     return e;
@@ -132,7 +197,9 @@ bool specialise_compile_check(const HostDevProgram& h, std::string* log) {
 }
 
 const void* specialised_tile_kernel(const HostDevProgram& h) {
-  if (h.shapes.empty()) return nullptr;
+  // Shapes only run when every register round is full: 2^(k-2) quads must be
+  // a multiple of NT * QPT (= 256 at one quad per thread), i.e. k >= 10.
+  if (h.shapes.empty() || h.tile_k < 10) return nullptr;
   if (const char* off = std::getenv("SHOTSIM_B200_NO_SPECIALISE"); off && *off && *off != '0') return nullptr;
   const std::string src = shape_source(h) + "// " + std::to_string(std::getenv("SHOTSIM_B200_JIT_QPT") != nullptr) +
                           (std::getenv("SHOTSIM_B200_JIT_QPT") ? std::getenv("SHOTSIM_B200_JIT_QPT") : "") +

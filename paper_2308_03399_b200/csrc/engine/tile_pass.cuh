@@ -50,7 +50,7 @@ __device__ __forceinline__ uint64_t pdep_positions(uint64_t v, const uint8_t* po
 __host__ __device__ inline uint64_t tile_smem_bytes(unsigned k, uint32_t nuops, uint32_t nmats) {
   const unsigned kt = k < 8 ? k : 8;
   return (uint64_t{1} << k) * 16 + uint64_t{nmats} * 16 + uint64_t{nuops} * 32 + (uint64_t{nuops} + 1) * 4 + 16 +
-         (uint64_t{1} << (k - kt)) * 4;
+         (uint64_t{1} << (k - kt)) * 4 + uint64_t{nuops} + 16;
 }
 
 // Persistent: each CTA owns a contiguous range of (shot, tile) units, stages
@@ -73,6 +73,7 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
   uint16_t* pre = reinterpret_cast<uint16_t*>(eops + nu);
   uint16_t* ppre = pre + (nu + 1);
   uint32_t* hi_off = reinterpret_cast<uint32_t*>((reinterpret_cast<unsigned long long>(ppre + (nu + 1)) + 7) & ~7ull);
+  uint8_t* pinfo = reinterpret_cast<uint8_t*>(hi_off + (1u << (k - (k < 8 ? k : 8))));  // per-uop drawn Pauli (0xFF: none)
   __shared__ uint8_t hpos[32];
   __shared__ uint64_t kraus_cls;
   const bool has_kraus = pd.kraus_mat < pd.mat_count;
@@ -133,6 +134,7 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
         if (i < nu) {
           pre[i] = static_cast<uint16_t>(at);
           ppre[i] = static_cast<uint16_t>(pcount + __popc(pballot & lanes_below));
+          pinfo[i] = (keep && u.code == UC_PAULI) ? u.pauli : static_cast<uint8_t>(0xFF);
         }
         if (keep) eops[at] = u;
         count += __popc(ballot);
@@ -173,11 +175,15 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
       for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
         const Item it = P.items[it_i];
         const uint32_t b = pre[it.begin], e = pre[it.end];
-        if (full_rounds && it.shape != kNoShape && ppre[it.begin] == ppre[it.end] && e - b == it.nfast) {
-          // This shot runs the segment's common case: every Pauli draw
-          // identity, every condition true.
-          if (it.nfast == 0 && it.sigma == 0xE4) continue;
-          if (ssb_run_shape(it.shape, tile, k, it.la, it.lb, smats + uops[it.begin].mat, kraus_cls)) continue;
+        const uint32_t kept_pauli = ppre[it.end] - ppre[it.begin];
+        if (full_rounds && it.shape != kNoShape && e - b - kept_pauli == it.nfast) {
+          // Every condition of the segment holds for this shot: its shape runs
+          // straight-line — skipping the Pauli sites when all drew identity
+          // (the common case), else applying the drawn ones in place.
+          if (kept_pauli == 0 && it.nfast == 0 && it.sigma == 0xE4) continue;
+          if (ssb_run_shape(it.shape, kept_pauli != 0, tile, k, it.la, it.lb, smats + uops[it.begin].mat, kraus_cls,
+                            pinfo + it.begin))
+            continue;
         }
         if (b == e && it.sigma == 0xE4) continue;  // nothing to apply and no relabeling to store
         if (k < 2) {
