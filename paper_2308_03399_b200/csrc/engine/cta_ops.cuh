@@ -13,7 +13,10 @@
 
 namespace ssb {
 
-constexpr int NT = 256;                // threads per CTA
+#ifndef SSB_NT
+#define SSB_NT 256
+#endif
+constexpr int NT = SSB_NT;             // threads per CTA (resident_warp.cu: 32)
 constexpr uint64_t SUM_BLOCK = 512;    // statevector.cpp:82 / kernels_scalar.cpp:91
 
 // Sequential sum of v[0..c) then — for power-of-two c > 8 — the fixed pairwise

@@ -558,6 +558,13 @@ std::vector<ShapeOp> parse_shape(const std::string& key, unsigned* final_sigma) 
 std::string shape_source(const HostDevProgram& d) {
   std::string src = "namespace ssb {\n";
   char buf[512];
+  // Drawn Paulis inline (fastest) while the shape set is small; out of line
+  // (one shared body) when many Pauli positions would make the run-time
+  // compile slow (random circuits: ~60 s -> ~15 s).
+  size_t pauli_positions = 0;
+  for (const std::string& key : d.shapes)
+    for (size_t p = key.find("P."); p != std::string::npos; p = key.find("P.", p + 2)) ++pauli_positions;
+  const char* pauli_macro = pauli_positions <= 100 ? "SSB_SHAPE_PAULI_INLINE" : "SSB_SHAPE_PAULI";
   for (size_t id = 0; id < d.shapes.size(); ++id) {
     unsigned fs = 0;
     const std::vector<ShapeOp> ops = parse_shape(d.shapes[id], &fs);
@@ -573,7 +580,7 @@ std::string shape_source(const HostDevProgram& d) {
       const unsigned a0 = o.qb & 3, a1 = (o.qb >> 2) & 3, b0 = (o.qb >> 4) & 3, b1 = (o.qb >> 6) & 3;
       switch (o.code) {
         case UC_PAULI:
-          std::snprintf(buf, sizeof buf, "  if (NOISY) { SSB_SHAPE_PAULI(%u, pinfo[%u]) }\n", o.sigma, o.pos);
+          std::snprintf(buf, sizeof buf, "  if (NOISY) { %s(%u, pinfo[%u]) }\n", pauli_macro, o.sigma, o.pos);
           break;
         case UC_U:
         case UC_REAL:

@@ -23,6 +23,10 @@ namespace ssb {
     if (e_ != cudaSuccess) throw CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// resident_warp.cu: the resident kernel with one-warp CTAs (small states).
+int launch_resident_warp(const void* view, uint64_t seed, uint64_t shot_begin, uint64_t count, uint64_t* values,
+                         int* err, cudaStream_t stream, size_t smem, int num_sms);
+
 // specialise.cpp: the shape-specialised tile-pass kernel for a plan, or null.
 const void* specialised_tile_kernel(const HostDevProgram& h);
 
@@ -496,14 +500,27 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
   timer.stream = E->stream;
   if (n <= rc.resident_max && rsmem <= E->smem_optin) {
     DevProgram& dp = device_program(E, prog, 0);
-    CK(cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, resident_kernel, NT, rsmem));
-    const uint64_t grid = std::min<uint64_t>(count, static_cast<uint64_t>(std::max(1, per_sm)) * E->num_sms);
+    // One-warp CTAs for small states (SHOTSIM_B200_WARP_RESIDENT_MAX: largest n,
+    // default 10).
+    unsigned warp_max = 10;
+    if (const char* v = std::getenv("SHOTSIM_B200_WARP_RESIDENT_MAX"); v && *v) warp_max = std::atoi(v);
+    uint64_t grid = 0;
     timer.begin(0);
-    resident_kernel<<<static_cast<unsigned>(grid), NT, rsmem, E->stream>>>(dp.view, seed, nullptr, shot_begin, count,
-                                                                           values_dev, E->err);
-    launched(E);
+    if (n <= warp_max) {
+      const int g = launch_resident_warp(&dp.view, seed, shot_begin, count, values_dev, E->err, E->stream, rsmem,
+                                         E->num_sms);
+      if (g < 0) throw CudaError("resident (warp) launch failed");
+      grid = static_cast<uint64_t>(g);
+      launched(E);
+    } else {
+      CK(cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, resident_kernel, NT, rsmem));
+      grid = std::min<uint64_t>(count, static_cast<uint64_t>(std::max(1, per_sm)) * E->num_sms);
+      resident_kernel<<<static_cast<unsigned>(grid), NT, rsmem, E->stream>>>(dp.view, seed, nullptr, shot_begin, count,
+                                                                             values_dev, E->err);
+      launched(E);
+    }
     timer.end(0);
     if (stats) {
       stats->peak_states = std::min<uint64_t>(count, grid);

@@ -39,9 +39,32 @@ __device__ __forceinline__ uint32_t insert_zero32(uint32_t i, uint32_t bit) {
     _Pragma("unroll") for (int e = 0; e < 4; ++e) v[q][e] = x.e[e];                  \
   }
 
-// A drawn Pauli on every quad through the (constant) logical view; pv packs
-// xq | zq << 2 | (num_y & 3) << 4 (tile_pass compaction).
+// A drawn Pauli on every quad through the logical view; pv packs xq | zq << 2
+// | (num_y & 3) << 4 (tile_pass compaction). Out of line: it runs only for
+// shots that drew a Pauli in the segment, and one shared body keeps the
+// run-time compile small.
+static __device__ __noinline__ Quad4 shape_pauli_call(Quad4 x, unsigned sigma, unsigned pv) {
+  double2 v[4] = {x.e[0], x.e[1], x.e[2], x.e[3]};
+  double2 L[4];
+  gather_logical(v, static_cast<uint8_t>(sigma), L);
+  quad_pauli1(L, pv & 3u, (pv >> 2) & 3u, (pv >> 4) & 3u);
+  scatter_logical(v, static_cast<uint8_t>(sigma), L);
+  return Quad4{{v[0], v[1], v[2], v[3]}};
+}
+
 #define SSB_SHAPE_PAULI(SIGMA, PV)                                                   \
+  {                                                                                  \
+    const unsigned pv_ = (PV);                                                       \
+    if (pv_ != 0xFFu) {                                                              \
+      _Pragma("unroll") for (int q = 0; q < QPT; ++q) {                              \
+        Quad4 x_{{v[q][0], v[q][1], v[q][2], v[q][3]}};                              \
+        x_ = shape_pauli_call(x_, (SIGMA), pv_);                                     \
+        _Pragma("unroll") for (int e = 0; e < 4; ++e) v[q][e] = x_.e[e];             \
+      }                                                                              \
+    }                                                                                \
+  }
+
+#define SSB_SHAPE_PAULI_INLINE(SIGMA, PV)                                            \
   {                                                                                  \
     const unsigned pv_ = (PV);                                                       \
     if (pv_ != 0xFFu) {                                                              \
