@@ -291,6 +291,75 @@ struct DBuf {  // named view of a persistent grow-only engine buffer
   T* get(size_t n) { return static_cast<T*>(E->scratch(E->ctx, name, std::max<size_t>(n, 1) * sizeof(T))); }
 };
 
+// Per new live node after a site (materialize + advance_node fused, for states
+// that fit shared memory): apply the child's decision — Pauli term, scaled
+// Kraus matrix, or collapse (+ creg / X-fix), exec_branch.cpp:104-136 — then
+// the gate run up to the next site, with one HBM read + write of the state.
+struct ChildRun {
+  uint32_t slot;
+  uint32_t key;
+  double inv;
+  uint64_t creg;     // register after the decision (gate conditions)
+  uint32_t has_kid;  // transform the state (else gates only)
+  uint32_t pad;
+};
+
+__global__ void __launch_bounds__(NT) b_child_run_kernel(ProgView P, DevOp site, double2* pool, const ChildRun* nodes,
+                                                         uint64_t nn, unsigned n, uint32_t g_begin, uint32_t g_end,
+                                                         int has_gates) {
+  extern __shared__ double2 st[];
+  const uint64_t A = uint64_t{1} << n;
+  for (uint64_t x = blockIdx.x; x < nn; x += gridDim.x) {
+    const ChildRun c = nodes[x];
+    if (!c.has_kid && !has_gates) continue;
+    double2* g = pool + (uint64_t{c.slot} << n);
+    for (uint64_t j = threadIdx.x; j < A; j += NT) st[j] = g[j];
+    __syncthreads();
+    if (c.has_kid) {
+      if (site.kind == K_PAULI) {
+        const DevTerm tm = P.terms[site.aux + c.key];
+        cta_pauli(st, n, tm.x, tm.z, tm.num_y);
+      } else if (site.kind == K_KRAUS) {
+        const DevChannel chn = P.channels[site.aux];
+        const uint32_t slot = chn.mat_begin + c.key;
+        const uint64_t cls = P.scaled_cls[slot];
+        if (chn.arity == 1) {
+          double2 m[4];
+          for (int e = 0; e < 4; ++e) m[e] = c_scale(P.mats[16 * slot + e], c.inv);
+          cta_apply1(st, n, site.q[0], m, cls);
+        } else {
+          double2 m[16];
+          for (int e = 0; e < 16; ++e) m[e] = c_scale(P.mats[16 * slot + e], c.inv);
+          cta_apply2(st, n, site.q[0], site.q[1], m, cls);
+        }
+      } else {
+        uint64_t qmask = 0;
+        for (unsigned b = 0; b < site.nq; ++b) qmask |= uint64_t{1} << site.q[b];
+        const uint64_t off = scatter_bits(c.key, site.q, site.nq);
+        cta_collapse(st, n, qmask, off, c.inv, site.kind == K_RESET ? off : 0);
+      }
+      __syncthreads();
+    }
+    for (uint32_t i = g_begin; i < g_end; ++i) {
+      const DevOp& op = P.ops[i];
+      if (op.kind != K_GATE || op.skip) continue;
+      if (op.has_cond && (c.creg & op.cond_mask) != op.cond_value) continue;
+      if (op.nq == 1) {
+        double2 m[4];
+        load_matrix<2>(P.mats + 16 * op.aux, m);
+        cta_apply1(st, n, op.q[0], m, op.cls);
+      } else {
+        double2 m[16];
+        load_matrix<4>(P.mats + 16 * op.aux, m);
+        cta_apply2(st, n, op.q[0], op.q[1], m, op.cls);
+      }
+      __syncthreads();
+    }
+    for (uint64_t j = threadIdx.x; j < A; j += NT) g[j] = st[j];
+    __syncthreads();
+  }
+}
+
 // Nonzero (node, key) groups, compacted in (node, key) order by CUB: gather
 // their counts and node-level parameters for the host planner.
 __global__ void b_gather_groups(const uint32_t* sel, const unsigned* num, const unsigned* counts, const double* vals,
@@ -401,6 +470,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   DBuf<double> dvals{&E, "branch.vals"}, dpart{&E, "branch.part"}, dcum{&E, "branch.cum"};
   DBuf<uint2> dpairs{&E, "branch.pairs"};
   DBuf<ChildOp> dkids{&E, "branch.kids"};
+  DBuf<ChildRun> dchildrun{&E, "branch.childrun"};
   DBuf<uint8_t> dactive{&E, "branch.active"};
   DBuf<uint32_t> dsel{&E, "branch.sel"};
   DBuf<unsigned> dnumsel{&E, "branch.numsel"}, dgcnt{&E, "branch.gcnt"};
@@ -413,8 +483,10 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   CKB(cudaGetDevice(&dev));
   CKB(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const uint64_t gate_run_smem_max = static_cast<uint64_t>(smem_optin);
-  if (seg <= gate_run_smem_max)
+  if (seg <= gate_run_smem_max) {
     CKB(cudaFuncSetAttribute(b_gate_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(seg)));
+    CKB(cudaFuncSetAttribute(b_child_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(seg)));
+  }
   // SHOTSIM_B200_BRANCH_TRACE=1: per-phase host wall time (sync points) to stderr.
   const bool tracing = [] {
     const char* v = std::getenv("SHOTSIM_B200_BRANCH_TRACE");
@@ -461,6 +533,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
     peak = std::max<uint64_t>(peak, 1);
 
     uint32_t i = 0;
+    bool gates_done = false;  // the previous site's child run already applied ops [i, j)
     while (i < h.end) {
       uint32_t j = i;
       auto is_site = [&](uint32_t k) {
@@ -470,7 +543,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       while (j < h.end && !is_site(j)) ++j;
       const uint64_t nn = live.size();
       // advance_node (exec_branch.cpp:155-162): gates over all live nodes.
-      if (j > i) {
+      if (j > i && !gates_done) {
         uint32_t* hs = pinned("branch.h_gslots", nn, (uint32_t*)nullptr);
         uint64_t* hc = pinned("branch.h_gcregs", nn, (uint64_t*)nullptr);
         for (uint64_t x = 0; x < nn; ++x) {
@@ -499,6 +572,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
         }
         trace_sync("gates");  // host vectors hs/hc die here
       }
+      gates_done = false;
       if (j == h.end) break;
       const DevOp site = h.ops[j];
 
@@ -689,7 +763,33 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
         b_copy_slots<<<gridn(pairs.size() * A), NT, 0, s>>>(pool, dp, pairs.size(), n);
         launched();
       }
-      if (!kids.empty()) {
+      // Next site (end of the gate run that follows this one).
+      uint32_t jn = j + 1;
+      while (jn < h.end && !is_site(jn)) ++jn;
+      bool run_gates = false;
+      for (uint32_t k = j + 1; k < jn; ++k) run_gates |= h.ops[k].kind == K_GATE && !h.ops[k].skip;
+      if (seg <= gate_run_smem_max) {
+        // Fused: each new live node's decision + the following gate run.
+        ChildRun* hr = pinned("branch.h_childrun", next.size(), (ChildRun*)nullptr);
+        size_t kidx = 0;
+        for (size_t x = 0; x < next.size(); ++x) {
+          hr[x] = ChildRun{next[x].slot, 0, 0.0, next[x].creg, 0, 0};
+          if (kidx < kids.size() && kids[kidx].slot == next[x].slot) {
+            hr[x].key = kids[kidx].key;
+            hr[x].inv = kids[kidx].inv;
+            hr[x].has_kid = 1;
+            ++kidx;
+          }
+        }
+        if (!next.empty() && (run_gates || !kids.empty())) {
+          ChildRun* dr = dchildrun.get(next.size());
+          CKB(cudaMemcpyAsync(dr, hr, next.size() * sizeof(ChildRun), cudaMemcpyHostToDevice, s));
+          b_child_run_kernel<<<static_cast<unsigned>(std::min<uint64_t>(next.size(), 1u << 20)), NT, seg, s>>>(
+              P, site, pool, dr, next.size(), n, j + 1, jn, run_gates ? 1 : 0);
+          launched();
+        }
+        gates_done = true;
+      } else if (!kids.empty()) {
         ChildOp* dk = dkids.get(kids.size());
         ChildOp* hk = pinned("branch.h_kids", kids.size(), (ChildOp*)nullptr);
         std::copy(kids.begin(), kids.end(), hk);
