@@ -16,6 +16,7 @@
 // sequential scan returns because the cumulative is monotone).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
@@ -360,6 +361,70 @@ __global__ void __launch_bounds__(NT) b_child_run_kernel(ProgView P, DevOp site,
   }
 }
 
+// Device planner for a site whose nonzero groups all fit the budget (the
+// common case): every group becomes a child in (parent, key) order
+// (exec_branch.cpp:141-153). A parent's first child keeps its slot; the r-th
+// other child (r = g - parent - 1, every parent owning >= 1 group) takes a
+// recycled slot or a fresh one. Shot offsets are the exclusive scan of the
+// group counts. Emits the next live table, each child's decision record for
+// the fused child run, and the copy source of non-first children.
+__global__ void b_plan_kernel(ProgView P, DevOp site, const DevNode* nodes, const uint32_t* sel, const unsigned* gcnt,
+                              const double* gval, const unsigned* goff, uint64_t ng, uint32_t nkeys,
+                              const uint32_t* free_list, uint32_t nfree, uint32_t next_slot, DevNode* next_nodes,
+                              ChildRun* runs, uint32_t* copy_src, uint64_t* gdst, int* err) {
+  const uint64_t g = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const uint32_t cell = sel[g], x = cell / nkeys, key = cell % nkeys;
+  const bool first = g == 0 || sel[g - 1] / nkeys != x;
+  const DevNode par = nodes[x];
+  uint32_t slot = par.slot, src = 0xFFFFFFFFu;
+  if (!first) {
+    const uint32_t r = static_cast<uint32_t>(g) - x - 1;
+    slot = r < nfree ? free_list[nfree - 1 - r] : next_slot + (r - nfree);
+    src = par.slot;
+  }
+  uint64_t creg = par.creg;
+  const bool transform = par.cond_ok && !(site.kind == K_PAULI && P.terms[site.aux + key].identity);
+  double inv = 1.0;
+  if (transform && site.kind != K_PAULI) {
+    const double p = gval[g];
+    if (!(p > 0.0)) raise(err, DEV_DEGENERATE);
+    else inv = __ddiv_rn(1.0, __dsqrt_rn(p));
+  }
+  if (transform && site.kind == K_MEASURE)
+    for (unsigned b = 0; b < site.nq; ++b)
+      creg = (creg & ~(uint64_t{1} << site.c[b])) | (((uint64_t{key} >> b) & 1) << site.c[b]);
+  next_nodes[g] = DevNode{slot, 1u, goff[g], gcnt[g], creg};
+  runs[g] = ChildRun{slot, key, inv, creg, transform ? 1u : 0u, 0u};
+  copy_src[g] = src;
+  gdst[g] = goff[g];
+}
+
+// Non-first children copy their parent's state before any decision is applied.
+__global__ void b_copy_children(double2* pool, const uint32_t* copy_src, const DevNode* next_nodes, uint64_t ng,
+                                unsigned n) {
+  const uint64_t A = uint64_t{1} << n;
+  for (uint64_t g = blockIdx.x; g < ng; g += gridDim.x) {
+    const uint32_t src = copy_src[g];
+    if (src == 0xFFFFFFFFu) continue;
+    const double2* a = pool + (uint64_t{src} << n);
+    double2* b = pool + (uint64_t{next_nodes[g].slot} << n);
+    for (uint64_t j = threadIdx.x; j < A; j += blockDim.x) b[j] = a[j];
+  }
+}
+
+// Live-table fields for the gate / reduction kernels (device-resident table).
+__global__ void b_node_fields(DevNode* nodes, uint64_t nn, DevOp site, int set_cond, uint32_t* slots, uint64_t* cregs,
+                              uint8_t* active) {
+  const uint64_t x = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (x >= nn) return;
+  DevNode& d = nodes[x];
+  if (set_cond) d.cond_ok = !site.has_cond || (d.creg & site.cond_mask) == site.cond_value ? 1u : 0u;
+  if (slots) slots[x] = d.slot;
+  if (cregs) cregs[x] = d.creg;
+  if (active) active[x] = static_cast<uint8_t>(d.cond_ok);
+}
+
 // Nonzero (node, key) groups, compacted in (node, key) order by CUB: gather
 // their counts and node-level parameters for the host planner.
 __global__ void b_gather_groups(const uint32_t* sel, const unsigned* num, const unsigned* counts, const double* vals,
@@ -435,7 +500,9 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
                                  " qubits needs " + std::to_string(max_slots * seg) + " bytes");
   // The pool lives in the engine across runs (grown by doubling, contents
   // preserved), so repeated runs never reallocate.
-  uint64_t pool_cap = std::min<uint64_t>(max_slots, 64);
+  // Reserve the whole bound up front when it is at most half the memory
+  // limit (no growth copies inside the run); otherwise start small and double.
+  uint64_t pool_cap = max_slots * seg <= mem_limit_bytes / 2 ? max_slots : std::min<uint64_t>(max_slots, 64);
   double2* pool = static_cast<double2*>(E.grow(E.ctx, "branch.pool", pool_cap * seg, 0));
   std::vector<uint32_t> free_slots;
   uint32_t next_slot = 0;
@@ -454,6 +521,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
     return next_slot++;
   };
 
+  std::vector<HostNode> live;
   DBuf<uint64_t> shots_a{&E, "branch.shots_a"}, shots_b{&E, "branch.shots_b"}, waiting_buf{&E, "branch.waiting"};
   uint64_t* cur_shots = shots_a.get(count);
   uint64_t* nxt_shots = shots_b.get(count);
@@ -476,8 +544,29 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   DBuf<unsigned> dnumsel{&E, "branch.numsel"}, dgcnt{&E, "branch.gcnt"};
   DBuf<double> dgval{&E, "branch.gval"};
   DBuf<uint64_t> dgdst{&E, "branch.gdst"};
+  DBuf<DevNode> dlive_a{&E, "branch.live_a"}, dlive_b{&E, "branch.live_b"};
+  DBuf<unsigned> dgoff{&E, "branch.goff"};
+  DBuf<uint32_t> dcopysrc{&E, "branch.copysrc"}, dfree{&E, "branch.free"};
+  // The live table is device-resident while sites are planned on the device
+  // (no budget overflow); the host copy `live` is refreshed only for the
+  // overflow planner and the leaves.
+  bool live_on_host = true;
+  DevNode* dlive = nullptr;
+  uint64_t nn_dev = 0, total_live = 0;
+  auto live_to_host = [&](DevNode* staging) {
+    CKB(cudaMemcpyAsync(staging, dlive, nn_dev * sizeof(DevNode), cudaMemcpyDeviceToHost, s));
+    CKB(cudaStreamSynchronize(s));
+    live.resize(nn_dev);
+    for (uint64_t x = 0; x < nn_dev; ++x) live[x] = HostNode{staging[x].slot, staging[x].off, staging[x].len, staging[x].creg};
+    live_on_host = true;
+  };
   DBuf<uint8_t> dcubtmp{&E, "branch.cubtmp"};
 
+  // SHOTSIM_B200_BRANCH_HOST_PLAN=1: plan every site on the host (A/B tests).
+  const bool device_plan = [] {
+    const char* v = std::getenv("SHOTSIM_B200_BRANCH_HOST_PLAN");
+    return !(v && *v && *v != '0');
+  }();
   // Node-resident gate runs when a state fits shared memory.
   int smem_optin = 0, dev = 0;
   CKB(cudaGetDevice(&dev));
@@ -494,6 +583,12 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   }();
   std::map<std::string, double> trace_t;
   auto trace_last = std::chrono::steady_clock::now();
+  auto trace_mark = [&](const char* tag) {  // host-only phase boundary
+    if (!tracing) return;
+    const auto now = std::chrono::steady_clock::now();
+    trace_t[tag] += std::chrono::duration<double>(now - trace_last).count();
+    trace_last = now;
+  };
   auto trace_sync = [&](const char* tag) {
     CKB(cudaStreamSynchronize(s));
     if (!tracing) return;
@@ -508,7 +603,6 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
     return static_cast<T*>(E.host(E.ctx, name, std::max<size_t>(count, 1) * sizeof(T)));
   };
   uint64_t peak = 0, passes = 0;
-  std::vector<HostNode> live;
   // Planner work arrays, reused across sites (no per-site allocation).
   struct Cand {
     uint64_t parent;
@@ -528,6 +622,8 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
     free_slots.clear();
     next_slot = 0;
     live.assign(1, HostNode{alloc_slot(), 0, root_len, 0});
+    live_on_host = true;
+    total_live = root_len;
     b_init_slot<<<gridn(A), NT, 0, s>>>(pool, live[0].slot, n);
     launched();
     peak = std::max<uint64_t>(peak, 1);
@@ -541,19 +637,24 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
         return kd == K_PAULI || kd == K_KRAUS || kd == K_MEASURE || kd == K_RESET;
       };
       while (j < h.end && !is_site(j)) ++j;
-      const uint64_t nn = live.size();
+      const uint64_t nn = live_on_host ? live.size() : nn_dev;
       // advance_node (exec_branch.cpp:155-162): gates over all live nodes.
       if (j > i && !gates_done) {
-        uint32_t* hs = pinned("branch.h_gslots", nn, (uint32_t*)nullptr);
-        uint64_t* hc = pinned("branch.h_gcregs", nn, (uint64_t*)nullptr);
-        for (uint64_t x = 0; x < nn; ++x) {
-          hs[x] = live[x].slot;
-          hc[x] = live[x].creg;
-        }
         uint32_t* slots = dslots.get(nn);
         uint64_t* cregs = dcreg.get(nn);
-        CKB(cudaMemcpyAsync(slots, hs, nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        CKB(cudaMemcpyAsync(cregs, hc, nn * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        if (live_on_host) {
+          uint32_t* hs = pinned("branch.h_gslots", nn, (uint32_t*)nullptr);
+          uint64_t* hc = pinned("branch.h_gcregs", nn, (uint64_t*)nullptr);
+          for (uint64_t x = 0; x < nn; ++x) {
+            hs[x] = live[x].slot;
+            hc[x] = live[x].creg;
+          }
+          CKB(cudaMemcpyAsync(slots, hs, nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+          CKB(cudaMemcpyAsync(cregs, hc, nn * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        } else {
+          b_node_fields<<<gridn(nn), NT, 0, s>>>(dlive, nn, h.ops[i], 0, slots, cregs, nullptr);
+          launched();
+        }
         uint32_t ngates = 0;
         for (uint32_t k = i; k < j; ++k) ngates += h.ops[k].kind == K_GATE && !h.ops[k].skip;
         if (ngates > 1 && seg <= gate_run_smem_max) {
@@ -577,12 +678,20 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       const DevOp site = h.ops[j];
 
       // Node table with condition flags.
-      DevNode* hn = pinned("branch.h_nodes", nn, (DevNode*)nullptr);
-      for (uint64_t x = 0; x < nn; ++x)
-        hn[x] = {live[x].slot, !site.has_cond || (live[x].creg & site.cond_mask) == site.cond_value ? 1u : 0u,
-                 live[x].off, live[x].len, live[x].creg};
-      DevNode* nodes = dnodes.get(nn);
-      CKB(cudaMemcpyAsync(nodes, hn, nn * sizeof(DevNode), cudaMemcpyHostToDevice, s));
+      DevNode* hn = nullptr;  // host copy (host-planned sites only)
+      DevNode* nodes = nullptr;
+      if (live_on_host) {
+        hn = pinned("branch.h_nodes", nn, (DevNode*)nullptr);
+        for (uint64_t x = 0; x < nn; ++x)
+          hn[x] = {live[x].slot, !site.has_cond || (live[x].creg & site.cond_mask) == site.cond_value ? 1u : 0u,
+                   live[x].off, live[x].len, live[x].creg};
+        nodes = dnodes.get(nn);
+        CKB(cudaMemcpyAsync(nodes, hn, nn * sizeof(DevNode), cudaMemcpyHostToDevice, s));
+      } else {
+        nodes = dlive;
+        b_node_fields<<<gridn(nn), NT, 0, s>>>(nodes, nn, site, 1, nullptr, nullptr, nullptr);
+        launched();
+      }
 
       uint32_t nkeys = 1;
       double* vals = nullptr;
@@ -625,16 +734,21 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
           R.blk = G <= SUM_BLOCK ? G : SUM_BLOCK;
           nkeys = R.nq;
         }
-        uint32_t* hs = pinned("branch.h_rslots", nn, (uint32_t*)nullptr);
-        uint8_t* ha = pinned("branch.h_ractive", nn, (uint8_t*)nullptr);
-        for (uint64_t x = 0; x < nn; ++x) {
-          hs[x] = live[x].slot;
-          ha[x] = static_cast<uint8_t>(hn[x].cond_ok);
-        }
         uint32_t* slots = dslots.get(nn);
         uint8_t* active = dactive.get(nn);
-        CKB(cudaMemcpyAsync(slots, hs, nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        CKB(cudaMemcpyAsync(active, ha, nn, cudaMemcpyHostToDevice, s));
+        if (live_on_host) {
+          uint32_t* hs = pinned("branch.h_rslots", nn, (uint32_t*)nullptr);
+          uint8_t* ha = pinned("branch.h_ractive", nn, (uint8_t*)nullptr);
+          for (uint64_t x = 0; x < nn; ++x) {
+            hs[x] = live[x].slot;
+            ha[x] = static_cast<uint8_t>(hn[x].cond_ok);
+          }
+          CKB(cudaMemcpyAsync(slots, hs, nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+          CKB(cudaMemcpyAsync(active, ha, nn, cudaMemcpyHostToDevice, s));
+        } else {
+          b_node_fields<<<gridn(nn), NT, 0, s>>>(nodes, nn, site, 0, slots, nullptr, active);
+          launched();
+        }
         double* part = dpart.get(nn * R.nq * R.nb);
         vals = dvals.get(nn * R.nq);
         launch_reduce(s, pool, nn, R, active, part, slots);
@@ -645,8 +759,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       }
 
       // Per-shot decisions and group counts.
-      uint64_t total = 0;
-      for (const HostNode& x : live) total += x.len;
+      const uint64_t total = total_live;
       uint32_t* keys = dkeys.get(total);
       unsigned* counts = dcounts.get(nn * nkeys);
       CKB(cudaMemsetAsync(counts, 0, nn * nkeys * sizeof(unsigned), s));
@@ -671,6 +784,74 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       CKB(cudaMemcpyAsync(hnum, dnum, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
       trace_sync("decide_num");
       const uint64_t ng = *hnum;
+      // Next site (end of the gate run that follows this one).
+      uint32_t jn = j + 1;
+      while (jn < h.end && !is_site(jn)) ++jn;
+      bool run_gates = false;
+      for (uint32_t k = j + 1; k < jn; ++k) run_gates |= h.ops[k].kind == K_GATE && !h.ops[k].skip;
+      if (device_plan && seg <= gate_run_smem_max && ng <= budget && total < (uint64_t{1} << 32)) {
+        // Device planner (no budget overflow): the live table never leaves HBM.
+        const uint64_t nnew = ng - nn;
+        const uint64_t nfree = free_slots.size(), take = std::min<uint64_t>(nnew, nfree);
+        const uint64_t need = next_slot + (nnew - take);
+        while (need > pool_cap) {
+          const uint64_t ncap = std::min<uint64_t>(max_slots, pool_cap * 2);
+          if (ncap <= pool_cap) throw std::logic_error("branch slot pool exhausted");
+          pool = static_cast<double2*>(E.grow(E.ctx, "branch.pool", ncap * seg, pool_cap * seg));
+          pool_cap = ncap;
+        }
+        uint32_t* dfl = nullptr;
+        if (take) {
+          uint32_t* hf = pinned("branch.h_free", nfree, (uint32_t*)nullptr);
+          std::copy(free_slots.begin(), free_slots.end(), hf);
+          dfl = dfree.get(nfree);
+          CKB(cudaMemcpyAsync(dfl, hf, nfree * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        }
+        unsigned* goff = dgoff.get(ng);
+        size_t scan_bytes = 0;
+        CKB(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, gcnt, goff, static_cast<int>(ng), s));
+        void* scan_tmp = dcubtmp.get(std::max(scan_bytes, tmp_bytes));
+        CKB(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, gcnt, goff, static_cast<int>(ng), s));
+        DevNode* next_tab = (dlive == dlive_a.get(1) ? dlive_b : dlive_a).get(ng);
+        ChildRun* runs = dchildrun.get(ng);
+        uint32_t* csrc = dcopysrc.get(ng);
+        uint64_t* gdst = dgdst.get(ng);
+        b_plan_kernel<<<gridn(ng), NT, 0, s>>>(P, site, nodes, sel, gcnt, gval, goff, ng, nkeys, dfl,
+                                               static_cast<uint32_t>(take ? nfree : 0), next_slot, next_tab, runs,
+                                               csrc, gdst, E.err);
+        launched();
+        uint64_t* dst = ddst.get(nn * nkeys);
+        unsigned long long* cursor = dcursor.get(nn * nkeys);
+        b_set_dst<<<gridn(ng), NT, 0, s>>>(sel, gdst, ng, dst);
+        launched();
+        CKB(cudaMemsetAsync(cursor, 0, nn * nkeys * sizeof(unsigned long long), s));
+        b_scatter<<<gridn(total), NT, 0, s>>>(nodes, nn, cur_shots, total, keys, nkeys, dst, cursor, nxt_shots,
+                                               waiting);
+        launched();
+        if (nnew) {
+          b_copy_children<<<static_cast<unsigned>(std::min<uint64_t>(ng, 1u << 20)), NT, 0, s>>>(pool, csrc, next_tab,
+                                                                                                 ng, n);
+          launched();
+        }
+        b_child_run_kernel<<<static_cast<unsigned>(std::min<uint64_t>(ng, 1u << 20)), NT, seg, s>>>(
+            P, site, pool, runs, ng, n, j + 1, jn, run_gates ? 1 : 0);
+        launched();
+        free_slots.resize(nfree - take);
+        next_slot += static_cast<uint32_t>(nnew - take);
+        dlive = next_tab;
+        nn_dev = ng;
+        live_on_host = false;
+        peak = std::max<uint64_t>(peak, ng);
+        gates_done = true;
+        trace_sync("apply_dev");
+        std::swap(cur_shots, nxt_shots);
+        i = j + 1;
+        continue;
+      }
+      if (!live_on_host) {  // host planner needs the table (and its condition flags)
+        hn = pinned("branch.h_nodes_dl", nn, (DevNode*)nullptr);
+        live_to_host(hn);
+      }
       uint32_t* hsel = static_cast<uint32_t*>(E.host(E.ctx, "branch.hsel", std::max<uint64_t>(ng, 1) * 4));
       unsigned* hgc = static_cast<unsigned*>(E.host(E.ctx, "branch.hgc", std::max<uint64_t>(ng, 1) * 4));
       double* hgv = static_cast<double*>(E.host(E.ctx, "branch.hgv", std::max<uint64_t>(ng, 1) * 8));
@@ -763,11 +944,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
         b_copy_slots<<<gridn(pairs.size() * A), NT, 0, s>>>(pool, dp, pairs.size(), n);
         launched();
       }
-      // Next site (end of the gate run that follows this one).
-      uint32_t jn = j + 1;
-      while (jn < h.end && !is_site(jn)) ++jn;
-      bool run_gates = false;
-      for (uint32_t k = j + 1; k < jn; ++k) run_gates |= h.ops[k].kind == K_GATE && !h.ops[k].skip;
+      trace_mark("plan_host");
       if (seg <= gate_run_smem_max) {
         // Fused: each new live node's decision + the following gate run.
         ChildRun* hr = pinned("branch.h_childrun", next.size(), (ChildRun*)nullptr);
@@ -801,11 +978,14 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       nwaiting = wait_off;
       std::swap(cur_shots, nxt_shots);
       live = std::move(next);
+      live_on_host = true;
+      total_live = new_off;
       peak = std::max<uint64_t>(peak, live.size());
       i = j + 1;
     }
 
     // Leaves (exec_branch.cpp:267-281).
+    if (!live_on_host) live_to_host(pinned("branch.h_nodes_dl", nn_dev, (DevNode*)nullptr));
     const uint64_t nl = live.size();
     uint64_t total = 0;
     std::vector<DevNode> hl(nl);
