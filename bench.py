@@ -57,7 +57,7 @@ def workload(key, shots_override=0):
     return cfg, cfg["circuit"](), cfg["noise"](), (shots_override or cfg["shots"]), cfg["seed"]
 
 
-def config_dict(key, cfg, shots, n_gpus):
+def config_dict(key, cfg, shots, n_gpus, executor="gpu-batch"):
     desc = {
         "C1": "GHZ10 + depolarizing 1%",
         "C2": "QV16 (16 layers of SU(4) blocks) + depolarizing 1% + 1% readout flip",
@@ -66,7 +66,7 @@ def config_dict(key, cfg, shots, n_gpus):
         "C5": "QV24 + depolarizing 1%",
     }[key]
     return {"workload": f"{key} {cfg['name']}: {desc}", "shots_per_gpu_per_step": shots,
-            "global_shots_per_step": shots * n_gpus, "seed": cfg["seed"], "executor": "gpu-batch",
+            "global_shots_per_step": shots * n_gpus, "seed": cfg["seed"], "executor": executor,
             "parallelism": f"shot-sharded x{n_gpus} (weak)",
             "l2": "inputs larger than L2: per-wave state 16 GiB >> 126 MB L2",
             "arithmetic": "fp64 complex, reference scalar-table rounding (no FMA), bit-exact counts"}
@@ -296,7 +296,8 @@ def run_reference_arm(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference", "config": config_dict(args.config, cfg, k, 1),
+            "impl": "reference",
+            "config": config_dict(args.config, cfg, k, 1, executor="reference run_single_shot (CPU, all host threads)"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": f"{k} shot ids per step on {cores} host threads (reference CPU path)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -356,7 +357,7 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     pass_s = other_s = 0.0
-    pass_launches = launches = passes_per_wave = 0
+    pass_launches = launches = passes_per_wave = shapes = 0
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -364,6 +365,7 @@ def main():
             pass_s += st.pass_seconds
             pass_launches += st.pass_launches
             passes_per_wave = st.fused_passes
+            shapes = st.specialised_shapes
             other_s += st.special_seconds + st.sample_seconds
             launches += nl
         ev1.record(stream)
@@ -421,7 +423,9 @@ def main():
     n_timed_shots = shots * args.steps
     if pass_s > 0:
         achieved = pass_b * n_timed_shots / pass_s / 1e9
-        roof = {"bound": "hbm", "kernel": "tile_pass_kernel" if prog.num_qubits > 13 else "resident_kernel",
+        kname = ("ssb_tile_pass_jit (run-time shape-specialised, %d shapes)" % shapes if shapes else "tile_pass_kernel") \
+            if prog.num_qubits > 13 else "resident_kernel"
+        roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(args.config, n_timed_shots * passes_per_wave / max(pass_launches, 1)),
                 "traffic_source": "profiles/ncu_summary.json (ncu --set full dram__bytes_read+write per shot-pass)",
