@@ -88,6 +88,8 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
   __syncthreads();
 
   const uint32_t lo_part = static_cast<uint32_t>(pdep_positions(threadIdx.x, pd.lq, kt));
+  bool no_relabel = true;
+  for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) no_relabel &= P.items[it_i].sigma == 0xE4;
   // Shape-specialised straight-line executors need every register round full.
   const bool full_rounds = k >= 2 && ((1u << (k - 2)) % (NT * QPT)) == 0;
   // Work units are (shot, tile) pairs in shot-major order; each CTA owns a
@@ -154,7 +156,11 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
     __syncthreads();
     double2* seg = state + (s << n);
     const uint64_t t_begin = u_begin > s * tiles ? u_begin - s * tiles : 0;
-    const uint64_t t_end = u_end < (s + 1) * tiles ? u_end - s * tiles : tiles;
+    uint64_t t_end = u_end < (s + 1) * tiles ? u_end - s * tiles : tiles;
+    // Nothing to apply for this shot (every micro-op compacted away — e.g. a
+    // pass of readout Pauli sites that all drew identity) and no relabeled
+    // segment to store: its tiles are left untouched in HBM.
+    if (!pd.first && pre[nu] == 0 && no_relabel) t_end = t_begin;
     for (uint64_t t = t_begin; t < t_end; ++t) {
       double2* tbase = seg + pdep_positions(t, hpos, n - k);
       if (pd.first) {
