@@ -123,8 +123,43 @@ __device__ __forceinline__ void cta_pauli(double2* st, unsigned nloc, uint32_t x
 // All 2^k outcome probabilities of qubits q (outcome_probability,
 // statevector.cpp:142-164) into probs[] (shared). red: shared scratch of
 // max(2^k * G/512, 1) doubles. Ends with __syncthreads().
+// Sequential sum of |st[insert_zero(g, t) | off]|^2 over g in [g0, g1): the
+// reference's in-block order, 8 elements loaded ahead of the add chain.
+__device__ __forceinline__ double block_norm_sum_1q(const double2* st, unsigned t, uint64_t off, uint64_t g0,
+                                                    uint64_t g1) {
+  double s = 0.0;
+  uint64_t g = g0;
+  for (; g + 8 <= g1; g += 8) {
+    double p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = c_norm(st[insert_zero(g + j, t) | off]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = __dadd_rn(s, p[j]);
+  }
+  for (; g < g1; ++g) s = __dadd_rn(s, c_norm(st[insert_zero(g, t) | off]));
+  return s;
+}
+
 static __device__ __noinline__ void cta_outcome_probs(const double2* st, unsigned n, const uint8_t* q, unsigned k,
                                   double* probs, double* red) {
+  if (k == 1) {  // single-qubit measure / reset (the common case): no index tables
+    const unsigned t = q[0];
+    const uint64_t bit = uint64_t{1} << t, G = uint64_t{1} << (n - 1);
+    if (G <= SUM_BLOCK) {
+      if (threadIdx.x < 2) probs[threadIdx.x] = block_norm_sum_1q(st, t, threadIdx.x ? bit : 0, 0, G);
+      __syncthreads();
+      return;
+    }
+    const uint64_t nb = G / SUM_BLOCK;
+    for (uint64_t x = threadIdx.x; x < 2 * nb; x += NT) {
+      const uint64_t m = x / nb, b = x % nb;
+      red[x] = block_norm_sum_1q(st, t, m ? bit : 0, b * SUM_BLOCK, (b + 1) * SUM_BLOCK);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) probs[threadIdx.x] = pairwise_inplace(red + threadIdx.x * nb, nb);
+    __syncthreads();
+    return;
+  }
   uint8_t sorted[32];
   sort_positions(q, k, sorted);
   const uint64_t G = uint64_t{1} << (n - k), no = uint64_t{1} << k;

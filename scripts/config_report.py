@@ -36,7 +36,9 @@ def main():
         cfg = cc.CONFIGS[key]
         prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
         run = eng.run_branch if mode == "branch" else eng.run_batch
-        run(prog, RunOptions(shots=min(shots, 64), seed=1, **extra))  # warm-up (+ specialisation compile)
+        # Warm-up at the timed size (specialisation compile, engine buffers and
+        # the branch slot pool reach their steady-state sizes), as bench.py does.
+        run(prog, RunOptions(shots=shots, seed=1, **extra))
         t0 = time.perf_counter()
         r = run(prog, RunOptions(shots=shots, seed=1, **extra))
         wall = time.perf_counter() - t0
