@@ -562,6 +562,36 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   };
   DBuf<uint8_t> dcubtmp{&E, "branch.cubtmp"};
 
+  // Size every per-site table once for the run's worst case (live nodes <=
+  // max_slots, keys per node <= the largest site fan-out), so the site loop
+  // never reallocates (each growth would synchronise the device).
+  {
+    uint64_t max_keys = 1;
+    for (uint32_t k = 0; k < h.end; ++k) {
+      const DevOp& o = h.ops[k];
+      if (o.kind == K_PAULI) max_keys = std::max<uint64_t>(max_keys, o.count);
+      else if (o.kind == K_KRAUS) max_keys = std::max<uint64_t>(max_keys, h.channels[o.aux].nmat);
+      else if (o.kind == K_MEASURE || o.kind == K_RESET) max_keys = std::max<uint64_t>(max_keys, uint64_t{1} << o.nq);
+    }
+    const uint64_t nodes_max = max_slots, cells = nodes_max * max_keys;
+    dnodes.get(nodes_max);
+    dlive_a.get(nodes_max);
+    dlive_b.get(nodes_max);
+    dslots.get(nodes_max);
+    dcreg.get(nodes_max);
+    dactive.get(nodes_max);
+    dchildrun.get(cells);
+    dcopysrc.get(cells);
+    dgdst.get(cells);
+    dgoff.get(cells);
+    dsel.get(cells);
+    dgcnt.get(cells);
+    dgval.get(cells);
+    dcounts.get(cells);
+    ddst.get(cells);
+    dcursor.get(cells);
+    dkeys.get(count);
+  }
   // SHOTSIM_B200_BRANCH_HOST_PLAN=1: plan every site on the host (A/B tests).
   const bool device_plan = [] {
     const char* v = std::getenv("SHOTSIM_B200_BRANCH_HOST_PLAN");
