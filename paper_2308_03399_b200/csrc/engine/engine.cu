@@ -427,13 +427,21 @@ void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c) {
   }
 }
 
+// Shared memory of resident_kernel for a resident plan: state | staged
+// matrices | micro-ops | compacted segment | reduction scratch | outcome
+// probabilities | Pauli draws.
 size_t resident_smem(const HostDevProgram& h) {
   const uint64_t A = uint64_t{1} << h.n;
   const uint64_t probs =
       (h.eligible && h.sample_qubits.size() < h.n) ? (uint64_t{1} << h.sample_qubits.size()) + 16 : 16;
   uint32_t sites = 0;
   for (const DevOp& o : h.ops) sites += o.kind == K_PAULI;
-  return A * sizeof(double2) + (resident_red_doubles() + probs) * sizeof(double) + sites;
+  uint64_t staged = 0;
+  if (!h.passes.empty()) {
+    const PassDesc& pd = h.passes[0];
+    staged = uint64_t{pd.mat_count} * sizeof(double2) + 2 * uint64_t{pd.uop_end - pd.uop_begin} * sizeof(Uop);
+  }
+  return A * sizeof(double2) + staged + (resident_red_doubles() + probs) * sizeof(double) + sites;
 }
 
 // Optional per-kernel-class CUDA-event timing (ssb_run_options::profile):
@@ -494,16 +502,17 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
   const unsigned n = prog->dev.n;
   const uint64_t launches0 = E->launches;
   CK(cudaMemsetAsync(E->serial_chunks, 0, sizeof(unsigned long long), E->stream));
-  const size_t rsmem = resident_smem(prog->dev);
+  // The resident plan (and its shared-memory size) for states that may fit.
+  DevProgram* rdp = n <= rc.resident_max ? &device_program(E, prog, 0) : nullptr;
+  const size_t rsmem = rdp ? resident_smem(rdp->host) : ~size_t{0};
   KernelTimer timer;
   timer.on = opts && opts->profile;
   timer.stream = E->stream;
-  if (n <= rc.resident_max && rsmem <= E->smem_optin) {
-    DevProgram& dp = device_program(E, prog, 0);
-    // One-warp CTAs for small states (SHOTSIM_B200_WARP_RESIDENT_MAX: largest n,
-    // default 10).
-    unsigned warp_max = 10;
-    if (const char* v = std::getenv("SHOTSIM_B200_WARP_RESIDENT_MAX"); v && *v) warp_max = std::atoi(v);
+  if (rdp && rsmem <= E->smem_optin) {
+    DevProgram& dp = *rdp;
+    // One-warp CTAs for small states; their plan carries the staged micro-ops
+    // (plan_resident), so the choice is fixed by n.
+    const unsigned warp_max = 10;
     uint64_t grid = 0;
     timer.begin(0);
     if (n <= warp_max) {

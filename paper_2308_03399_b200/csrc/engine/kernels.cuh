@@ -75,6 +75,56 @@ __device__ __forceinline__ bool scan_full(Amp amp, uint64_t count, bool identity
   return last != count;
 }
 
+#ifndef SSB_RESIDENT_STAGED
+#define SSB_RESIDENT_STAGED 0
+#endif
+
+// One register segment of the resident program, staged: compact its micro-ops
+// for this shot now (conditions read the register as it stands): drop failed
+// conditions and identity Pauli draws, resolve drawn Paulis to quad masks;
+// then run it with CX / SWAP as register relabelings and the fast U layouts.
+// Out of line so the resident kernel's own register allocation is unaffected.
+static __device__ __noinline__ void resident_staged_segment(const ProgView& P, const Item& it, double2* st, unsigned n,
+                                                            const Uop* uops, Uop* eops, const double2* smats,
+                                                            uint64_t creg, const uint8_t* psel, uint32_t* seg_count) {
+  if (threadIdx.x < 32) {
+    uint32_t count = 0;
+    for (uint32_t c0 = it.begin; c0 < it.end; c0 += 32) {
+      const uint32_t i = c0 + threadIdx.x;
+      bool keep = false;
+      Uop u{};
+      if (i < it.end) {
+        u = uops[i];
+        keep = true;
+        const DevOp& op = P.ops[u.ref];
+        if ((u.flags & 1) && (creg & op.cond_mask) != op.cond_value) keep = false;
+        if (keep && u.code == UC_PAULI) {
+          const DevTerm tm = P.terms[op.aux + psel[op.site]];
+          if (tm.identity) {
+            keep = false;
+          } else {
+            uint32_t xq = 0, zq = 0;
+            for (unsigned b = 0; b < op.nq; ++b) {
+              const uint32_t qb = (u.qb >> b) & 1u;
+              xq |= ((tm.x >> op.q[b]) & 1u) << qb;
+              zq |= ((tm.z >> op.q[b]) & 1u) << qb;
+            }
+            u.pauli = static_cast<uint8_t>(xq | (zq << 2) | ((tm.num_y & 3u) << 4));
+          }
+        }
+      }
+      const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+      if (keep) eops[count + __popc(ballot & ((1u << threadIdx.x) - 1))] = u;
+      count += __popc(ballot);
+    }
+    if (threadIdx.x == 0) *seg_count = count;
+  }
+  __syncthreads();
+  const uint32_t cnt = *seg_count;
+  if (cnt == 0 && it.sigma == 0xE4) return;
+  run_segment_staged(st, n, it, eops, 0, cnt, smats, P.ops, 0);
+}
+
 // Shared-memory layout of resident_kernel: state | red (513) | probs | Pauli
 // decisions (u8 per site).
 __host__ __device__ constexpr uint64_t resident_red_doubles() { return 513; }
@@ -88,13 +138,20 @@ static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint
   extern __shared__ double2 smem[];
   const unsigned n = P.n;
   const uint64_t A = uint64_t{1} << n;
+  const PassDesc& pd = P.passes[0];
+  const uint32_t nu = pd.uop_end - pd.uop_begin;
   double2* st = smem;
-  double* red = reinterpret_cast<double*>(st + A);
+  double2* smats = st + A;                                   // staged-segment matrices
+  Uop* uops = reinterpret_cast<Uop*>(smats + pd.mat_count);  // the program's micro-ops
+  Uop* eops = uops + nu;                                     // one segment, compacted
+  double* red = reinterpret_cast<double*>(eops + nu);
   double* probs = red + resident_red_doubles();
   uint8_t* psel = reinterpret_cast<uint8_t*>(probs + resident_probs_doubles(P));
   __shared__ uint64_t bc_out;
   __shared__ double bc_p;
-  const PassDesc& pd = P.passes[0];
+  __shared__ uint32_t seg_count;
+  for (uint32_t i = threadIdx.x; i < pd.mat_count; i += NT) smats[i] = P.uop_mats[pd.mat_begin + i];
+  for (uint32_t i = threadIdx.x; i < nu; i += NT) uops[i] = P.uops[pd.uop_begin + i];
 
   for (uint64_t s = blockIdx.x; s < S; s += gridDim.x) {
     const uint64_t shot = shot_of(ids, shot_begin, s);
@@ -109,6 +166,12 @@ static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint
     for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
       const Item it = P.items[it_i];
       if (it.kind == IT_SEGMENT) {
+#if SSB_RESIDENT_STAGED
+        if (nu != 0) {  // staged lowering (2..10-qubit states, one-warp CTAs)
+          resident_staged_segment(P, it, st, n, uops, eops, smats, creg, psel, &seg_count);
+          continue;
+        }
+#endif
         run_segment(st, n, it, P.pass_ops, P.ops, P.mats, P.terms, creg, psel);
         continue;
       }

@@ -5,7 +5,9 @@
 // sequential steps (pick_outcome / terminal scan); with one warp per CTA, a
 // dozen shots run per SM and every barrier is a warp barrier. Same device
 // code, same arithmetic — only the block size differs. The headers are
-// compiled here under a private namespace so the two builds never meet.
+// compiled here under a private namespace so the two builds never meet. This
+// build also runs the resident plan's staged segments (plan_resident lowers
+// 2..10-qubit programs to micro-ops: CX / SWAP relabelings, fast U layouts).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -13,6 +15,7 @@
 #include <string>
 
 #define SSB_NT 32
+#define SSB_RESIDENT_STAGED 1
 #define ssb ssb_w32
 #include "kernels.cuh"
 #undef ssb
