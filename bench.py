@@ -357,7 +357,7 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     pass_s = other_s = 0.0
-    pass_launches = launches = passes_per_wave = shapes = 0
+    pass_launches = launches = passes_per_wave = shapes = skipped = 0
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -366,6 +366,7 @@ def main():
             pass_launches += st.pass_launches
             passes_per_wave = st.fused_passes
             shapes = st.specialised_shapes
+            skipped += st.trunk_skipped
             other_s += st.special_seconds + st.sample_seconds
             launches += nl
         ev1.record(stream)
@@ -413,10 +414,16 @@ def main():
     dp_peak = _fp64_peak(eng)
     dp_shot = dp_ops_per_shot(prog)
     fp64 = None
+    # Shared noiseless trunk: (shot, pass) pairs whose work the trunk did once
+    # for all shots are not executed; the FP64 rate counts executed work only
+    # (skipped pairs weighted as an average pass).
+    shot_passes = shots * args.steps * max(passes_per_wave, 1)
+    executed = max(0.0, 1.0 - skipped / shot_passes) if passes_per_wave else 1.0
     if pass_s > 0:
-        dp_achieved = dp_shot * shots * args.steps / pass_s
+        dp_achieved = dp_shot * shots * args.steps * executed / pass_s
         fp64 = {"bound": "fp64-pipe", "achieved": dp_achieved / 1e12, "peak": dp_peak / 1e12, "unit": "T DP-op/s",
                 "frac": dp_achieved / dp_peak, "dp_ops_per_shot": dp_shot,
+                "executed_shot_pass_frac": executed,
                 "peak_source": "measured live: ssb_fp64_peak (independent DMUL/DADD chains, CUDA events)",
                 "note": "the tile passes are FP64-issue bound: bit-exact parity forbids FMA, so every complex "
                         "product is 4 DMUL + 2 DADD; this is the kernel's true roofline fraction"}
@@ -427,7 +434,7 @@ def main():
             if prog.num_qubits > 13 else "resident_kernel"
         roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config, n_timed_shots * passes_per_wave / max(pass_launches, 1)),
+                "traffic": ncu_traffic(args.config, n_timed_shots * passes_per_wave * executed / max(pass_launches, 1)),
                 "traffic_source": "profiles/ncu_summary.json (ncu --set full dram__bytes_read+write per shot-pass)",
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_shot": pass_b, "alg_bytes_per_launch": pass_b * n_timed_shots / max(

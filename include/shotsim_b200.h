@@ -161,6 +161,9 @@ typedef struct ssb_stats {
   uint64_t sampling_serial_chunks; /* terminal-sampling chunks replayed with the
                                       reference's sequential adds (binade
                                       changes, ties, the deciding chunk) */
+  uint64_t trunk_skipped;    /* streamed: (shot, pass) pairs not run because
+                                the shot's noise draws had not yet diverged
+                                from the shared noiseless trunk */
 } ssb_stats;
 
 SSB_API const char* ssb_last_error(void);

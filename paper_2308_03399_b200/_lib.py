@@ -78,6 +78,7 @@ class StatsC(C.Structure):
         ("pass_seconds", C.c_double), ("pass_launches", C.c_uint64), ("special_seconds", C.c_double),
         ("sample_seconds", C.c_double), ("specialised_shapes", C.c_uint64),
         ("sampling_serial_chunks", C.c_uint64),
+        ("trunk_skipped", C.c_uint64),
     ]
 
 

@@ -131,6 +131,7 @@ class RunResult:
     fused_passes: int = 0
     specialised_shapes: int = 0
     sampling_serial_chunks: int = 0
+    trunk_skipped: int = 0
 
 
 def bitstring(value: int, width: int) -> str:
@@ -200,7 +201,8 @@ class Engine:
                       branch=BranchStats(st.peak_states, st.passes), strategy=name, shots=count,
                       seed=opts.seed, device_seconds=st.device_seconds, wall_seconds=st.wall_seconds,
                       fused_passes=st.fused_passes, specialised_shapes=st.specialised_shapes,
-                      sampling_serial_chunks=st.sampling_serial_chunks)
+                      sampling_serial_chunks=st.sampling_serial_chunks,
+                      trunk_skipped=st.trunk_skipped)
         r._values = values
         return r
 

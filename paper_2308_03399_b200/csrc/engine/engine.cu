@@ -37,6 +37,12 @@ struct DevProgram {
   ProgView view{};
   uint32_t* pauli_site_ops = nullptr;
   uint32_t num_pauli = 0;
+  // Shared noiseless trunk (streamed plans without specials, Kraus or
+  // conditions): per Pauli site the pass that applies it, and a Pauli-draw row
+  // of identity terms (the trunk's own draws).
+  bool trunk_ok = false;
+  uint16_t* site_pass = nullptr;
+  uint8_t* ident_row = nullptr;
   ~DevProgram() {
     for (void* p : allocs) cudaFree(p);
   }
@@ -168,6 +174,34 @@ DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile
   d->pauli_site_ops = upload(*d, sites);
   v.pauli_site_ops = d->pauli_site_ops;
   v.num_pauli = d->num_pauli;
+  if (tile_k && !h.passes.empty() && d->num_pauli && h.passes.size() < 0xFFFF) {
+    bool ok = h.eligible && !h.steps.empty() && h.steps.back().kind == S_SAMPLE;
+    for (const Step& s : h.steps) ok &= s.kind == S_PASS || s.kind == S_SAMPLE;
+    std::vector<uint16_t> sp(d->num_pauli, 0xFFFF);
+    for (size_t p = 0; p < h.passes.size(); ++p) {
+      const size_t e = p + 1 < h.passes.size() ? h.passes[p + 1].po_begin : h.pass_ops.size();
+      for (size_t i = h.passes[p].po_begin; i < e; ++i) {
+        const DevOp& o = h.ops[h.pass_ops[i].op];
+        ok &= !o.has_cond;
+        if (o.kind == K_PAULI) sp[o.site] = static_cast<uint16_t>(p);
+      }
+    }
+    std::vector<uint8_t> ident(d->num_pauli, 0);
+    for (uint32_t s = 0; s < d->num_pauli; ++s) {
+      ok &= sp[s] != 0xFFFF;
+      const DevOp& o = h.ops[sites[s]];
+      for (uint32_t t = 0; t < o.count; ++t)
+        if (h.terms[o.aux + t].identity) {
+          ident[s] = static_cast<uint8_t>(t);
+          break;
+        }
+    }
+    if (ok) {
+      d->trunk_ok = true;
+      d->site_pass = upload(*d, sp);
+      d->ident_row = upload(*d, ident);
+    }
+  }
   auto& ref = *d;
   E->programs.emplace(key, std::move(d));
   return ref;
@@ -552,9 +586,60 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
                                    " qubits needs " + std::to_string(largest * seg) +
                                    " bytes; lower max_batch_size or raise the memory limit");
     const uint64_t tiles = uint64_t{1} << (n - h.tile_k);
-    wave = std::min<uint64_t>(largest, (uint64_t{1} << 31) / tiles);
-    double2* state = static_cast<double2*>(scratch(E, "state", wave * seg));
-    uint8_t* psel = dp.num_pauli ? static_cast<uint8_t*>(scratch(E, "psel", wave * dp.num_pauli)) : nullptr;
+    wave = std::min<uint64_t>(largest, std::max<uint64_t>(1, (uint64_t{1} << 31) / tiles - 1));
+    // Shared noiseless trunk: a shot runs no pass before the first one at which
+    // it draws a non-identity Pauli term; until then its state equals that of
+    // a noiseless trunk (wave slot S, all-identity draws) and is copied from
+    // it when the shot diverges. Most shots of a weakly noisy circuit share a
+    // long prefix with the trunk (arXiv:2308.03399 §III-B, applied to the
+    // batch). Needs one more state slot than the wave.
+    const char* no_trunk = std::getenv("SHOTSIM_B200_NO_TRUNK");
+    const bool trunk = dp.trunk_ok && !(no_trunk && *no_trunk && *no_trunk != '0') &&
+                       (wave + 1) * seg <= limit;
+    const uint64_t slots = wave + (trunk ? 1 : 0);
+    double2* state = static_cast<double2*>(scratch(E, "state", slots * seg));
+    uint8_t* psel = dp.num_pauli ? static_cast<uint8_t*>(scratch(E, "psel", slots * dp.num_pauli)) : nullptr;
+    const uint32_t npass = static_cast<uint32_t>(h.passes.size());
+    // Trunk bookkeeping: per shot its first diverging pass (device kernel,
+    // read back once), then per wave the slots in activation order (trunk
+    // first) and the per-pass activation boundaries.
+    uint32_t* act_dev = nullptr;
+    std::vector<uint64_t> act_off, act_end;  // per wave: offset into act, per-pass end counts
+    std::vector<char> wave_trunk;            // per wave: the trunk pays for itself
+    uint64_t trunk_skipped = 0;
+    if (trunk) {
+      uint16_t* first_dev = static_cast<uint16_t*>(scratch(E, "trunk_first", count * sizeof(uint16_t)));
+      first_divergence_kernel<<<grid_for(count), NT, 0, E->stream>>>(dp.view, dp.pauli_site_ops, dp.site_pass,
+                                                                     dp.num_pauli, seed, shot_begin, count,
+                                                                     static_cast<uint16_t>(npass), first_dev);
+      launched(E);
+      const uint64_t nwaves = (count + wave - 1) / wave;
+      uint16_t* first = static_cast<uint16_t*>(engine_host(E, "trunk_first", count * sizeof(uint16_t)));
+      CK(cudaMemcpyAsync(first, first_dev, count * sizeof(uint16_t), cudaMemcpyDeviceToHost, E->stream));
+      CK(cudaStreamSynchronize(E->stream));
+      const uint64_t nact = count + nwaves;
+      uint32_t* act = static_cast<uint32_t*>(engine_host(E, "trunk_act", nact * sizeof(uint32_t)));
+      act_dev = static_cast<uint32_t*>(scratch(E, "trunk_act", nact * sizeof(uint32_t)));
+      std::vector<uint64_t> cnt(npass + 2);
+      for (uint64_t w0 = 0, off = 0; w0 < count; w0 += wave) {
+        const uint64_t S = std::min(wave, count - w0);
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (uint64_t s = 0; s < S; ++s) ++cnt[first[w0 + s] + 1];
+        for (uint32_t p = 0; p <= npass; ++p) cnt[p + 1] += cnt[p];  // cnt[p]: shots with first < p
+        act_off.push_back(off);
+        for (uint32_t p = 0; p <= npass; ++p) act_end.push_back(1 + cnt[p + 1]);  // trunk + first <= p
+        act[off] = static_cast<uint32_t>(S);
+        for (uint64_t s = 0; s < S; ++s) act[off + 1 + cnt[first[w0 + s]]++] = static_cast<uint32_t>(s);
+        // Worth it when the skipped (shot, pass) pairs exceed the trunk's own
+        // passes plus its copies (a copy moves one state once: ~1/4 of a pass).
+        uint64_t skipped = 0;
+        for (uint32_t p = 0; p < npass; ++p) skipped += S + 1 - act_end[act_end.size() - (npass + 1) + p];
+        const uint64_t copied = S + 1 - act_end[act_end.size() - (npass + 1)];
+        wave_trunk.push_back(skipped > npass + copied / 4);
+        off += S + 1;
+      }
+      CK(cudaMemcpyAsync(act_dev, act, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, E->stream));
+    }
     // Per-shot Kraus choices of the wave (S_KRAUS_DECIDE -> next pass).
     double2* kmat = nullptr;
     uint64_t* kcls = nullptr;
@@ -578,14 +663,27 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
     uint64_t waves = 0, fused = 0;
     for (uint64_t w0 = 0; w0 < count; w0 += wave) {
       const uint64_t S = std::min(wave, count - w0);
-      ++waves;
       SegCtx c{state, S, seed, nullptr, shot_begin + w0, nullptr, values_dev + w0};
       CK(cudaMemsetAsync(c.cregs, 0, S * sizeof(uint64_t), E->stream));
       if (dp.num_pauli) {
         pauli_decide_kernel<<<grid_for(S * dp.num_pauli), NT, 0, E->stream>>>(dp.view, dp.pauli_site_ops, dp.num_pauli,
                                                                              seed, nullptr, c.begin, S, psel);
         launched(E);
+        if (trunk && wave_trunk[waves])
+          CK(cudaMemcpyAsync(psel + S * dp.num_pauli, dp.ident_row, dp.num_pauli, cudaMemcpyDeviceToDevice, E->stream));
       }
+      const bool wtrunk = trunk && wave_trunk[waves];
+      const uint32_t* wact = wtrunk ? act_dev + act_off[waves] : nullptr;
+      const uint64_t* wend = wtrunk ? act_end.data() + waves * (npass + 1) : nullptr;
+      // Activate the shots whose first diverging pass is p: copy the trunk in.
+      auto activate = [&](uint32_t p) {
+        const uint64_t b = p ? wend[p - 1] : 1, e = wend[p];
+        if (e <= b) return;
+        copy_trunk_kernel<<<grid_for(((e - b) << n) / 4), NT, 0, E->stream>>>(state, S, n, wact + b,
+                                                                             static_cast<uint32_t>(e - b));
+        launched(E);
+      };
+      ++waves;
       fused = 0;
       for (const Step& st : h.steps) {
         if (st.kind == S_KRAUS_DECIDE) {
@@ -593,13 +691,20 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
           kraus_decide_wave(E, dp, st.index, c, kmat, kcls, kchosen);
           timer.end(1);
         } else if (st.kind == S_PASS) {
+          // Trunk mode: only the trunk and the shots already diverged run.
+          uint64_t active = S;
+          if (wtrunk) {
+            if (st.index > 0) activate(st.index);
+            active = wend[st.index];
+            trunk_skipped += S + 1 - active;
+          }
           timer.begin(0);
           const unsigned grid =
-              static_cast<unsigned>(std::min<uint64_t>(S * tiles, uint64_t(std::max(per_sm, 1)) * E->num_sms));
+              static_cast<unsigned>(std::min<uint64_t>(active * tiles, uint64_t(std::max(per_sm, 1)) * E->num_sms));
           uint32_t pass_index = st.index, num_pauli = dp.num_pauli;
-          uint64_t* cregs = c.cregs;
-          void* args[] = {&dp.view, &pass_index, &state, const_cast<uint64_t*>(&S), &cregs, &psel, &num_pauli,
-                          &kmat, &kcls};
+          uint64_t* cregs = wtrunk ? nullptr : c.cregs;  // trunk mode: no conditions
+          void* args[] = {&dp.view, &pass_index, &state, &active, &cregs, &psel, &num_pauli,
+                          &kmat, &kcls, const_cast<uint32_t**>(&wact)};
           CK(cudaLaunchKernel(kfn, dim3(grid), dim3(NT), args, tsmem, E->stream));
           launched(E);
           timer.end(0);
@@ -609,6 +714,7 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
           apply_op(E, dp, st.index, c, false);
           timer.end(1);
         } else {
+          if (wtrunk) activate(npass);  // shots that never diverged
           timer.begin(2);
           sample_terminal(E, dp, c);
           timer.end(2);
@@ -620,6 +726,7 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       stats->passes = waves;
       stats->fused_passes = fused;
       stats->specialised_shapes = specialised ? h.shapes.size() : 0;
+      stats->trunk_skipped = trunk_skipped;
     }
   }
   if (stats) {

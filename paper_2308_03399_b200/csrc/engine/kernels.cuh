@@ -272,7 +272,7 @@ static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint
 }
 
 static __global__ void __launch_bounds__(NT, SSB_TILE_MINB) tile_pass_kernel(SSB_TILE_PASS_PARAMS) {
-  tile_pass_body(P, pass_index, state, S, cregs, pauli_sel, num_pauli, kmat, kcls);
+  tile_pass_body(P, pass_index, state, S, cregs, pauli_sel, num_pauli, kmat, kcls, act);
 }
 
 // Per-(shot, Pauli site) term choice for a wave: sel[s][site] (u8).
@@ -283,6 +283,39 @@ static __global__ void pauli_decide_kernel(ProgView P, const uint32_t* site_ops,
   const uint64_t s = idx / num_sites, site = idx % num_sites;
   const DevOp& op = P.ops[site_ops[site]];
   sel[idx] = static_cast<uint8_t>(pick_term(P.terms + op.aux, op.count, keyed_uniform(seed, shot_of(ids, shot_begin, s), op.event)));
+}
+
+// Shared noiseless trunk (streamed executor): the first pass at which shot s
+// draws a non-identity Pauli term (none: no such draw). Sites are in op order,
+// so the first non-identity site decides; the draws are the same keyed stream
+// pauli_decide_kernel reads.
+static __global__ void first_divergence_kernel(ProgView P, const uint32_t* site_ops, const uint16_t* site_pass,
+                                               uint32_t num_sites, uint64_t seed, uint64_t shot_begin, uint64_t count,
+                                               uint16_t none, uint16_t* first) {
+  const uint64_t s = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  if (s >= count) return;
+  uint16_t f = none;
+  for (uint32_t site = 0; site < num_sites; ++site) {
+    const DevOp& op = P.ops[site_ops[site]];
+    const int t = pick_term(P.terms + op.aux, op.count, keyed_uniform(seed, shot_begin + s, op.event));
+    if (!P.terms[op.aux + t].identity) {
+      f = site_pass[site];
+      break;
+    }
+  }
+  first[s] = f;
+}
+
+// Trunk state (wave slot S) -> the listed wave slots, 16-byte coalesced.
+static __global__ void copy_trunk_kernel(double2* state, uint64_t S, unsigned n, const uint32_t* slots,
+                                         uint32_t count) {
+  const uint64_t per = uint64_t{1} << n, total = uint64_t{count} * per;
+  const double2* src = state + (S << n);
+  for (uint64_t idx = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t i = idx >> n, e = idx & (per - 1);
+    state[(uint64_t{slots[i]} << n) + e] = src[e];
+  }
 }
 
 // ---------------------------------------------------------------------------

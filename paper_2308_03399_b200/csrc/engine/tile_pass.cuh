@@ -59,7 +59,8 @@ __host__ __device__ inline uint64_t tile_smem_bytes(unsigned k, uint32_t nuops, 
 // 1/sqrt(p)) and its classes for a pass that starts with a Kraus apply.
 static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_t pass_index, double2* state, uint64_t S,
                                                       const uint64_t* cregs, const uint8_t* pauli_sel,
-                                                      uint32_t num_pauli, const double2* kmat, const uint64_t* kcls) {
+                                                      uint32_t num_pauli, const double2* kmat, const uint64_t* kcls,
+                                                      const uint32_t* act) {
   extern __shared__ double2 tile[];
   const PassDesc& pd = P.passes[pass_index];
   const unsigned n = P.n, k = pd.k;
@@ -98,7 +99,10 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
   // per 16 GiB wave) still spread over every SM.
   const uint64_t units = S * tiles;
   const uint64_t u_begin = units * blockIdx.x / gridDim.x, u_end = units * (blockIdx.x + 1) / gridDim.x;
-  for (uint64_t s = u_begin / tiles; s * tiles < u_end; ++s) {
+  // act: optional list of the wave slots this pass runs (shared-trunk mode:
+  // shots whose randomness has not diverged from the trunk yet are skipped).
+  for (uint64_t si = u_begin / tiles; si * tiles < u_end; ++si) {
+    const uint64_t s = act ? act[si] : si;  // wave slot
     // Per-shot compaction (warp 0, in order): drop failed conditions and
     // identity Pauli draws; resolve each Pauli to quad masks.
     if (threadIdx.x < 32) {
@@ -155,8 +159,8 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
     }
     __syncthreads();
     double2* seg = state + (s << n);
-    const uint64_t t_begin = u_begin > s * tiles ? u_begin - s * tiles : 0;
-    uint64_t t_end = u_end < (s + 1) * tiles ? u_end - s * tiles : tiles;
+    const uint64_t t_begin = u_begin > si * tiles ? u_begin - si * tiles : 0;
+    uint64_t t_end = u_end < (si + 1) * tiles ? u_end - si * tiles : tiles;
     // Nothing to apply for this shot (every micro-op compacted away — e.g. a
     // pass of readout Pauli sites that all drew identity) and no relabeled
     // segment to store: its tiles are left untouched in HBM.
@@ -207,6 +211,6 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
 
 #define SSB_TILE_PASS_PARAMS                                                                            \
   ssb::ProgView P, uint32_t pass_index, double2 *state, uint64_t S, const uint64_t *cregs, const uint8_t *pauli_sel, \
-      uint32_t num_pauli, const double2 *kmat, const uint64_t *kcls
+      uint32_t num_pauli, const double2 *kmat, const uint64_t *kcls, const uint32_t *act
 
 }  // namespace ssb

@@ -249,3 +249,20 @@ def test_exact_parallel_sampling_paths(engine, oracle, monkeypatch):
         r = engine.run_batch(prog, RunOptions(shots=64, seed=5, resident_max_qubits=1))
         assert (values(r) == want).all()
         monkeypatch.delenv("SHOTSIM_B200_SAMPLE_SERIAL")
+
+
+@pytest.mark.parametrize("n,tile,wave", [(8, 3, 0), (12, 10, 37), (14, 12, 0)])
+def test_shared_trunk(engine, oracle, monkeypatch, n, tile, wave):
+    """Shared noiseless trunk: shots run no pass before their first
+    non-identity Pauli draw and copy the trunk state in then. Same values as
+    the oracle and as the plain streamed run, across waves (max_batch_size)."""
+    prog = Program.from_text(cc.quantum_volume(n, depth=5, seed=n), cc.depolarizing_model(0.004))
+    shots = 160
+    want = oracle.run_shots(prog, np.arange(shots), 21, threads=8)
+    kw = dict(shots=shots, seed=21, resident_max_qubits=1, tile_qubits=tile, max_batch_size=wave)
+    r = engine.run_batch(prog, RunOptions(**kw))
+    assert (values(r) == want).all()
+    assert 0 < r.trunk_skipped < shots * r.fused_passes
+    monkeypatch.setenv("SHOTSIM_B200_NO_TRUNK", "1")
+    r2 = engine.run_batch(prog, RunOptions(**kw))
+    assert (values(r2) == want).all() and r2.trunk_skipped == 0
