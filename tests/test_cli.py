@@ -1,6 +1,5 @@
 """CLI drop-in for the reference's `run` / `validate` subcommands
 (shotsim_main.cpp:38-67, 97-139): options, output format and exit codes."""
-import json
 import subprocess
 
 import pytest
@@ -49,7 +48,7 @@ def test_run_c1_counts(c1_files, strategy):
             "--seed", g["seed"])
     assert r.returncode == 0, r.stderr
     got = {k: int(v) for k, v in (line.split() for line in r.stdout.splitlines())}
-    want = counts_from_values(json.loads(g["values"]), 10, True)
+    want = counts_from_values(g["values"], 10, True)
     assert got == want
     assert list(got) == sorted(got)  # std::map order
     assert r.stderr.startswith(f"strategy={strategy} shots={g['shots']} seed={g['seed']} seconds=")
