@@ -120,10 +120,15 @@ def dp_ops_per_shot(program):
     per row, every nonzero term's product plus 2 DADD per complex add
     (row_apply / quad_apply*, exact.cuh). Pure permutations (CX, SWAP) and
     identity gates cost nothing; Pauli sites are sign / register moves."""
+    return sum(dp_ops_per_op(program))
+
+
+def dp_ops_per_op(program):
+    """dp_ops_per_shot split per op of the program (0 for non-gates)."""
     f = program.flat()
     A = 1 << f.num_qubits
     end = f.terminal_measure_begin if f.sampling_eligible else f.num_ops
-    total = 0
+    out = [0] * f.num_ops
     for i in range(end):
         op = f.ops[i]
         if op.kind != 0:
@@ -144,8 +149,8 @@ def dp_ops_per_shot(program):
                     identity = False
             ops += 2 * max(terms - 1, 0)
         if not identity:
-            total += ops * (A >> k)
-    return total
+            out[i] = ops * (A >> k)
+    return out
 
 
 def measured_peak():

@@ -220,6 +220,13 @@ SSB_API int ssb_histogram_device(ssb_engine* engine, const uint64_t* values_devi
  * ssb_last_error(). */
 SSB_API int ssb_program_specialise_check(const ssb_program* program, uint32_t tile_qubits, uint32_t* shapes);
 
+/* Diagnostics: the HBM tile pass (0-based, in execution order) each op of the
+ * program runs in under the streamed plan for `tile_qubits` (0: default);
+ * 0xFFFFFFFF for ops executed outside a pass (measure, reset, Kraus decide,
+ * skipped identities). pass_of_op may be NULL to only get *num_passes. */
+SSB_API int ssb_program_pass_map(const ssb_program* program, uint32_t tile_qubits, uint32_t* pass_of_op,
+                                 uint64_t cap, uint32_t* num_passes);
+
 /* FP64-pipe roofline probe: the sustained rate of rounded DMUL/DADD (no FMA,
  * the engine's arithmetic) over the whole device, in FP64 ops per second,
  * measured with CUDA events (the denominator of bench.py's fp64 roofline). */

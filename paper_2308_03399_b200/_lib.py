@@ -107,6 +107,7 @@ SIGNATURES = {
     "ssb_histogram_device": (C.c_int, [_vp, _vp, _u64, C.c_uint32, _vp]),
     "ssb_fp64_peak": (C.c_int, [_vp, _pd]),
     "ssb_program_specialise_check": (C.c_int, [_vp, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "ssb_program_pass_map": (C.c_int, [_vp, C.c_uint32, C.POINTER(C.c_uint32), _u64, C.POINTER(C.c_uint32)]),
     "ssb_batch_create": (C.c_int, [_vp, _vp, _pu64, _u64, _u64, C.POINTER(_vp)]),
     "ssb_batch_destroy": (None, [_vp]),
     "ssb_batch_apply_op": (C.c_int, [_vp, _u64, _pd]),

@@ -55,6 +55,16 @@ class Program:
         check(load().ssb_program_specialise_check(self._h, tile_qubits, C.byref(n)))
         return n.value
 
+    def pass_map(self, tile_qubits: int = 0) -> np.ndarray:
+        """Diagnostics: the streamed plan's tile pass of every op (-1: outside
+        a pass), for `tile_qubits` local qubits (0: default). Host only."""
+        f = self.flat()
+        out = np.empty(f.num_ops, dtype=np.uint32)
+        n = C.c_uint32(0)
+        check(load().ssb_program_pass_map(self._h, tile_qubits, out.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                          f.num_ops, C.byref(n)))
+        return out.astype(np.int64) - ((out == 0xFFFFFFFF) * (1 << 32))
+
     def dump(self) -> str:
         n = C.c_size_t()
         check(load().ssb_program_dump(self._h, None, 0, C.byref(n)))

@@ -93,6 +93,23 @@ namespace ssb {
 bool specialise_compile_check(const HostDevProgram& h, std::string* log);
 }
 
+extern "C" SSB_API int ssb_program_pass_map(const ssb_program* program, uint32_t tile_qubits, uint32_t* pass_of_op,
+                                           uint64_t cap, uint32_t* num_passes) {
+  return ssb::guard([&] {
+    if (!program || !num_passes) throw std::invalid_argument("null argument");
+    ssb::HostDevProgram h = program->dev;
+    ssb::plan_passes(h, tile_qubits ? std::max(3u, std::min(13u, tile_qubits)) : 12u);
+    *num_passes = static_cast<uint32_t>(h.passes.size());
+    if (!pass_of_op) return;
+    if (cap < h.ops.size()) throw std::invalid_argument("pass_of_op too small");
+    std::fill(pass_of_op, pass_of_op + h.ops.size(), 0xFFFFFFFFu);
+    for (size_t p = 0; p < h.passes.size(); ++p) {
+      const size_t e = p + 1 < h.passes.size() ? h.passes[p + 1].po_begin : h.pass_ops.size();
+      for (size_t i = h.passes[p].po_begin; i < e; ++i) pass_of_op[h.pass_ops[i].op] = static_cast<uint32_t>(p);
+    }
+  });
+}
+
 extern "C" SSB_API int ssb_program_specialise_check(const ssb_program* program, uint32_t tile_qubits,
                                                    uint32_t* shapes) {
   return ssb::guard([&] {

@@ -53,7 +53,10 @@ def main():
             line.update(peak_states=r.branch.peak_states, passes=r.branch.passes)
         if prog.num_qubits > 13:
             dp = bench.dp_ops_per_shot(prog)
-            line.update(dp_ops_per_shot=dp, fp64_frac_whole_run=rate * dp / dp_peak, fp64_peak=dp_peak)
+            # executed work only: (shot, pass) pairs the shared trunk covered are not run
+            executed = 1.0 - r.trunk_skipped / max(1, shots * r.fused_passes)
+            line.update(dp_ops_per_shot=dp, fp64_frac_whole_run=rate * dp * executed / dp_peak, fp64_peak=dp_peak,
+                        trunk_skipped_frac=1.0 - executed)
         g = golden.get(key)
         if g:
             got = [int(run(prog, RunOptions(shots=1, seed=1, **extra), shot_begin=i, shot_count=1)._values[0])
