@@ -88,9 +88,20 @@ std::vector<char> build_cubin(const std::string& shapes, std::string* log_out) {
   };
   const std::string qpt = "-DSSB_QPT=" + knob("SHOTSIM_B200_JIT_QPT", SSB_STR(SSB_JIT_QPT));
   const std::string minb = "-DSSB_TILE_MINB=" + knob("SHOTSIM_B200_JIT_MINB", SSB_STR(SSB_JIT_MINB));
-  const char* opts[] = {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES", qpt.c_str(),
-                        minb.c_str()};
-  const nvrtcResult r = nvrtcCompileProgram(prog, static_cast<int>(sizeof opts / sizeof opts[0]), opts);
+  std::vector<const char*> opts = {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES",
+                                   qpt.c_str(), minb.c_str()};
+  // SHOTSIM_B200_JIT_VERBOSE=1: print ptxas register / spill usage to stderr.
+  const char* verbose = std::getenv("SHOTSIM_B200_JIT_VERBOSE");
+  const bool loud = verbose && *verbose && *verbose != '0';
+  if (loud) opts.push_back("--ptxas-options=-v");
+  const nvrtcResult r = nvrtcCompileProgram(prog, static_cast<int>(opts.size()), opts.data());
+  if (loud && r == NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, log.data());
+    std::fprintf(stderr, "%s\n", log.c_str());
+  }
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);

@@ -172,14 +172,37 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
         for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
           tile[l] = make_double2((origin && (lo_part | hi_off[i]) == 0) ? 1.0 : 0.0, 0.0);
       } else {
-        for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) tile[l] = tbase[lo_part | hi_off[i]];
+        // Asynchronous global -> shared copies (LDGSTS): every 16-byte element
+        // of the thread is in flight at once, with no register round trip
+        // (a register copy loop serialises on the loads).
+        // (No memory clobber: the copies only write this thread's tile slots,
+        // read after cp.async.wait_all below.)
+        // Offsets are read 8 at a time ahead of their copies.
+        const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
+        for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * NT, i0 += 8) {
+          uint32_t off[8];
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * NT < L ? hi_off[i0 + j] : 0u;
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j)
+            if (l0 + j * NT < L)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tile_s + 16 * (l0 + j * NT)),
+                           "l"(tbase + (lo_part | off[j])));
+        }
         // Warm L2 with the next tile of this shot while this one is computed,
         // so its loads return at L2 latency (no registers, no shared memory).
         if (t + 1 < t_end) {
           const double2* nb = seg + pdep_positions(t + 1, hpos, n - k);
-          for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + (lo_part | hi_off[i])));
+          for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * NT, i0 += 8) {
+            uint32_t off[8];
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * NT < L ? hi_off[i0 + j] : 0u;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j)
+              if (l0 + j * NT < L) asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + (lo_part | off[j])));
+          }
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
       }
       __syncthreads();
       for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) {
