@@ -174,7 +174,7 @@ DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile
   d->pauli_site_ops = upload(*d, sites);
   v.pauli_site_ops = d->pauli_site_ops;
   v.num_pauli = d->num_pauli;
-  if (tile_k && !h.passes.empty() && d->num_pauli && h.passes.size() < 0xFFFF) {
+  if (tile_k && !h.passes.empty() && h.passes.size() < 0xFFFF) {
     bool ok = h.eligible && !h.steps.empty() && h.steps.back().kind == S_SAMPLE;
     for (const Step& s : h.steps) ok &= s.kind == S_PASS || s.kind == S_SAMPLE;
     std::vector<uint16_t> sp(d->num_pauli, 0xFFFF);

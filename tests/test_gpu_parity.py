@@ -266,3 +266,15 @@ def test_shared_trunk(engine, oracle, monkeypatch, n, tile, wave):
     monkeypatch.setenv("SHOTSIM_B200_NO_TRUNK", "1")
     r2 = engine.run_batch(prog, RunOptions(**kw))
     assert (values(r2) == want).all() and r2.trunk_skipped == 0
+
+
+def test_shared_trunk_noiseless(engine, oracle, monkeypatch):
+    """Without noise every shot's state is the trunk's: the passes run once per
+    wave and only terminal sampling is per shot."""
+    prog = Program.from_text(cc.quantum_volume(14, depth=4, seed=3), "")
+    want = oracle.run_shots(prog, np.arange(200), 8, threads=8)
+    r = engine.run_batch(prog, RunOptions(shots=200, seed=8))
+    assert (values(r) == want).all()
+    assert r.fused_passes > 0 and r.trunk_skipped == 200 * r.fused_passes
+    monkeypatch.setenv("SHOTSIM_B200_NO_TRUNK", "1")
+    assert (values(engine.run_batch(prog, RunOptions(shots=200, seed=8))) == want).all()
