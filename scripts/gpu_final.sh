@@ -16,5 +16,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/launches_bench.log 2>&1
 python profiles/summarize_launches.py gpurun_out/launches_bench.csv > gpurun_out/launches_bench.txt
 timeout 900 python scripts/config_report.py > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
-tail -2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -1 gpurun_out/bench.err gpurun_out/bench_torchrun.err gpurun_out/bench_ref.err
+tail -n 2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -n 1 gpurun_out/bench.err gpurun_out/bench_torchrun.err gpurun_out/bench_ref.err
 cut -c1-300 gpurun_out/bench.json gpurun_out/bench_torchrun.json gpurun_out/bench_ref.json; cat gpurun_out/launches_bench.txt; cut -c1-250 gpurun_out/configs.jsonl
