@@ -320,10 +320,18 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    # SHOTSIM_BENCH_DIST_BACKEND=gloo (test hook): exercise the N>1 path with
+    # several ranks sharing the visible GPUs (NCCL refuses duplicate GPUs).
+    backend = os.environ.get("SHOTSIM_BENCH_DIST_BACKEND", "nccl")
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2308_03399_b200 import Engine, Program, RunOptions
     cfg, circuit, noise, shots, seed = workload(args.config, args.shots)
