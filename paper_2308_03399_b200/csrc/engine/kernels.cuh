@@ -18,6 +18,7 @@
 #include "tile_pass.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace ssb {
 
@@ -526,11 +527,68 @@ static __global__ void __launch_bounds__(128) g_expval2_kernel(const double2* st
   }
 }
 
+// g_expval2_kernel with the amplitudes staged through shared memory: a CTA of
+// 128 threads owns 128 consecutive 8-group leaves (1024 groups) of one shot,
+// copies their 4 x 1024 amplitudes in with coalesced LDGSTS, then every thread
+// forms its leaf exactly as g_expval2_kernel does. (Leaf-per-thread loads
+// straight from HBM touch a different 128-byte line per lane per load.)
+constexpr unsigned kE2Threads = 128, kE2Groups = 8 * kE2Threads;
+__device__ __forceinline__ uint32_t e2_slot(uint32_t c, uint32_t g) {
+  return c * (kE2Groups + kE2Groups / 8) + g + g / 8;  // one pad slot per leaf: conflict-free rows
+}
+static __global__ void __launch_bounds__(kE2Threads) g_expval2_staged_kernel(const double2* st, uint64_t S, RedSpec R,
+                                                                            const uint8_t* active, double* part,
+                                                                            const uint32_t* slots = nullptr) {
+  extern __shared__ double2 e2[];  // 4 x (1024 + 128) amplitudes
+  const uint64_t ctas_per_shot = R.nb / kE2Threads, total = S * ctas_per_shot;
+  const uint64_t off[4] = {0, uint64_t{1} << R.q[0], uint64_t{1} << R.q[1],
+                           (uint64_t{1} << R.q[0]) | (uint64_t{1} << R.q[1])};
+  const uint32_t e2_s = static_cast<uint32_t>(__cvta_generic_to_shared(e2));
+  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    const uint64_t s = w / ctas_per_shot, g0 = (w % ctas_per_shot) * kE2Groups;
+    if (active && !active[s]) continue;  // CTA-uniform
+    const double2* a = st + (seg_of(slots, s) << R.n);
+    __syncthreads();  // previous item's reads of e2 are done
+    for (uint32_t e = threadIdx.x; e < 4 * kE2Groups; e += kE2Threads) {
+      const uint32_t c = e / kE2Groups, g = e % kE2Groups;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(e2_s + 16 * e2_slot(c, g)),
+                   "l"(a + (expand_sorted(g0 + g, R.sorted, 2) + off[c])));
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const uint64_t b = g0 / 8 + threadIdx.x;  // this thread's leaf
+    for (uint32_t qi = 0; qi < R.nq; ++qi) {
+      double2 m[16];
+      load_matrix<4>(R.mats + 16 * qi, m);
+      const uint64_t cls = R.cls[qi];
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        double2 in[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) in[c] = e2[e2_slot(c, 8 * threadIdx.x + j)];
+        double row = 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) row = __dadd_rn(row, c_norm(row_apply<4>(m, cls, r, in)));
+        acc = __dadd_rn(acc, row);
+      }
+      part[(s * R.nq + qi) * R.nb + b] = acc;
+    }
+  }
+}
+constexpr size_t kE2Smem = 4 * (kE2Groups + kE2Groups / 8) * sizeof(double2);
+
 // Launches the partial reduction for R (the 2q expval has its own kernel).
 inline void launch_reduce(cudaStream_t stream, const double2* st, uint64_t S, const RedSpec& R, const uint8_t* active,
                           double* part, const uint32_t* slots = nullptr) {
   const uint64_t work = reduce_threads(R, S);
-  if (R.mode == R_EXPVAL2) {
+  if (R.mode == R_EXPVAL2 && R.blk == 8 && R.nb % kE2Threads == 0 && !std::getenv("SHOTSIM_B200_EXPVAL2_DIRECT")) {
+    // (the attribute is per device; setting it is cheap)
+    cudaFuncSetAttribute(g_expval2_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kE2Smem));
+    const uint64_t items = S * (R.nb / kE2Threads);
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(items, 148u * 6u)));
+    g_expval2_staged_kernel<<<grid, kE2Threads, kE2Smem, stream>>>(st, S, R, active, part, slots);
+  } else if (R.mode == R_EXPVAL2) {
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((work + 127) / 128, 1u << 30)));
     g_expval2_kernel<<<grid, 128, 0, stream>>>(st, S, R, active, part, slots);
   } else {
