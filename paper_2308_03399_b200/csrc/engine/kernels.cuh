@@ -578,6 +578,52 @@ static __global__ void __launch_bounds__(kE2Threads) g_expval2_staged_kernel(con
 }
 constexpr size_t kE2Smem = 4 * (kE2Groups + kE2Groups / 8) * sizeof(double2);
 
+// R_EXPVAL1 partials staged the same way: a CTA of 128 threads owns 128
+// consecutive 512-pair blocks of one (shot, matrix); each round copies 16
+// pairs of every block in (16 lanes read 256 contiguous bytes), then each
+// thread continues its block's sequential sum over those 16 pairs.
+constexpr unsigned kE1Threads = 128, kE1Pairs = 16;
+__device__ __forceinline__ uint32_t e1_slot(uint32_t j, uint32_t h, uint32_t p) {
+  return j * (2 * kE1Pairs + 1) + h * kE1Pairs + p;  // one pad slot per block: conflict-free
+}
+static __global__ void __launch_bounds__(kE1Threads) g_expval1_staged_kernel(const double2* st, uint64_t S, RedSpec R,
+                                                                            const uint8_t* active, double* part,
+                                                                            const uint32_t* slots = nullptr) {
+  extern __shared__ double2 e1[];  // 128 x (2 x 16 + 1) amplitudes
+  const uint64_t ctas_per = R.nb / kE1Threads, total = S * R.nq * ctas_per;
+  const unsigned t = R.q[0];
+  const uint64_t bit = uint64_t{1} << t;
+  const uint32_t e1_s = static_cast<uint32_t>(__cvta_generic_to_shared(e1));
+  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    const uint64_t grp = w % ctas_per, qs = w / ctas_per, qi = qs % R.nq, s = qs / R.nq;
+    if (active && !active[s]) continue;  // CTA-uniform
+    const double2* a = st + (seg_of(slots, s) << R.n);
+    double2 m[4];
+    load_matrix<2>(R.mats + 16 * qi, m);
+    const uint64_t cls = R.cls[qi];
+    const uint64_t first = grp * kE1Threads * R.blk;  // first pair of the CTA's first block
+    double acc = 0.0;
+    for (uint64_t r = 0; r < R.blk; r += kE1Pairs) {
+      __syncthreads();  // previous round's reads are done
+      for (uint32_t e = threadIdx.x; e < kE1Threads * 2 * kE1Pairs; e += kE1Threads) {
+        const uint32_t j = e / (2 * kE1Pairs), h = (e / kE1Pairs) & 1, p = e % kE1Pairs;
+        const uint64_t i0 = insert_zero(first + j * R.blk + r + p, t) | (h ? bit : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(e1_s + 16 * e1_slot(j, h, p)), "l"(a + i0));
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+#pragma unroll 4
+      for (uint32_t p = 0; p < kE1Pairs; ++p) {
+        const double2 in[2] = {e1[e1_slot(threadIdx.x, 0, p)], e1[e1_slot(threadIdx.x, 1, p)]};
+        acc = __dadd_rn(acc, c_norm(row_apply<2>(m, cls, 0, in)));
+        acc = __dadd_rn(acc, c_norm(row_apply<2>(m, cls, 1, in)));
+      }
+    }
+    part[(s * R.nq + qi) * R.nb + grp * kE1Threads + threadIdx.x] = acc;
+  }
+}
+constexpr size_t kE1Smem = kE1Threads * (2 * kE1Pairs + 1) * sizeof(double2);
+
 // Launches the partial reduction for R (the 2q expval has its own kernel).
 inline void launch_reduce(cudaStream_t stream, const double2* st, uint64_t S, const RedSpec& R, const uint8_t* active,
                           double* part, const uint32_t* slots = nullptr) {
@@ -588,6 +634,12 @@ inline void launch_reduce(cudaStream_t stream, const double2* st, uint64_t S, co
     const uint64_t items = S * (R.nb / kE2Threads);
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(items, 148u * 6u)));
     g_expval2_staged_kernel<<<grid, kE2Threads, kE2Smem, stream>>>(st, S, R, active, part, slots);
+  } else if (R.mode == R_EXPVAL1 && R.blk % kE1Pairs == 0 && R.nb % kE1Threads == 0 &&
+             !std::getenv("SHOTSIM_B200_EXPVAL1_DIRECT")) {
+    cudaFuncSetAttribute(g_expval1_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kE1Smem));
+    const uint64_t items = S * R.nq * (R.nb / kE1Threads);
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(items, 148u * 12u)));
+    g_expval1_staged_kernel<<<grid, kE1Threads, kE1Smem, stream>>>(st, S, R, active, part, slots);
   } else if (R.mode == R_EXPVAL2) {
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((work + 127) / 128, 1u << 30)));
     g_expval2_kernel<<<grid, 128, 0, stream>>>(st, S, R, active, part, slots);

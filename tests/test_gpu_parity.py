@@ -71,9 +71,9 @@ def test_more_random_programs_vs_oracle(engine, oracle):
 
 @pytest.mark.parametrize("n,tile", [(6, 3), (8, 5), (10, 10), (12, 11), (12, 12)])
 def test_kraus_thermal_all_paths(engine, oracle, n, tile):
-    """Kraus sites through the resident kernel, the streamed passes (apply in
-    the next pass; at n >= 11 / tile >= 11 matrix 0's partials come from the
-    preceding pass's tiles) and the branch executor."""
+    """Kraus sites through the resident kernel, the streamed passes (decide
+    step between passes, apply as the next pass's first micro-op) and the
+    branch executor."""
     prog = Program.from_text(cc.random_layers(n, depth=4, seed=n), cc.thermal_noise(0.05, 0.1))
     want = oracle.run_shots(prog, np.arange(200), 3)
     for kw in ({}, dict(resident_max_qubits=1, tile_qubits=tile)):
@@ -278,3 +278,16 @@ def test_shared_trunk_noiseless(engine, oracle, monkeypatch):
     assert r.fused_passes > 0 and r.trunk_skipped == 200 * r.fused_passes
     monkeypatch.setenv("SHOTSIM_B200_NO_TRUNK", "1")
     assert (values(engine.run_batch(prog, RunOptions(shots=200, seed=8))) == want).all()
+
+
+@pytest.mark.parametrize("direct", [False, True])
+def test_kraus_probabilities_large_states(engine, oracle, monkeypatch, direct):
+    """1q / 2q Kraus probabilities at n = 17: the shared-memory staged
+    reductions (coalesced LDGSTS) and the direct per-thread kernels give the
+    reference's blocked sums, hence the same choices."""
+    if direct:
+        monkeypatch.setenv("SHOTSIM_B200_EXPVAL1_DIRECT", "1")
+        monkeypatch.setenv("SHOTSIM_B200_EXPVAL2_DIRECT", "1")
+    prog = Program.from_text(cc.random_layers(17, depth=3, seed=17), cc.thermal_noise(0.05, 0.1))
+    want = oracle.run_shots(prog, np.arange(32), 5, threads=8)
+    assert (values(engine.run_batch(prog, RunOptions(shots=32, seed=5))) == want).all()
