@@ -232,6 +232,25 @@ SSB_API int ssb_program_pass_map(const ssb_program* program, uint32_t tile_qubit
  * measured with CUDA events (the denominator of bench.py's fp64 roofline). */
 SSB_API int ssb_fp64_peak(ssb_engine* engine, double* ops_per_second);
 
+/* ---- exact density-matrix reference (density.hpp:12-68, n <= 10) ---- */
+/* exact_creg_distribution (density.cpp:291-306): the exact distribution of
+ * final classical-register values, evolved on the device. Entries are in
+ * ascending key order. keys/probs NULL: only *count is set (size query);
+ * otherwise capacity must be >= the entry count (SSB_ERR_CAPACITY if not).
+ * Errors as the reference: n outside 1..10 or > 2 intermediate measure sites
+ * -> SSB_ERR_CAPACITY; a conditional intermediate measure -> INVALID_ARGUMENT. */
+SSB_API int ssb_exact_creg_distribution(ssb_engine* engine, const ssb_program* program, uint64_t* keys,
+                                        double* probs, uint64_t capacity, uint64_t* count);
+/* exact_distribution (density.cpp:280-289): outcome distribution over the
+ * listed qubits (qubits[0] = bit 0); out holds 2^num_qubits doubles. */
+SSB_API int ssb_exact_distribution(ssb_engine* engine, const ssb_program* program, const uint32_t* qubits,
+                                   uint32_t num_qubits, double* out);
+/* tvd_vs_exact (density.cpp:308-315) against the Counts that
+ * counts_from_values(values, num_clbits, has_measure) builds (result.cpp:40-48)
+ * from the executors' per-shot register values. Host arithmetic. */
+SSB_API int ssb_tvd_vs_exact(const uint64_t* values, uint64_t shots, uint32_t num_clbits, uint32_t has_measure,
+                             const uint64_t* keys, const double* probs, uint64_t count, double* tvd);
+
 /* ---- operator-level entry points (BatchState, exec_batch.hpp:22-84) ---- */
 /* A device-resident batch over arbitrary shot ids, initialised to |0...0>. */
 SSB_API int ssb_batch_create(ssb_engine* engine, const ssb_program* program,

@@ -260,6 +260,12 @@ using ExecutorFn = RunResult (*)(const NoisyCircuit&, const RunOptions&);
 ExecutorFn executor_by_name(std::string_view name);
 uint64_t default_mem_limit_bytes();
 
+// The reference's statistical checker (density.hpp:56-68), evolved on device 0
+// (n <= 10; CapacityError / std::invalid_argument as the reference).
+std::vector<double> exact_distribution(const NoisyCircuit& program, std::span<const unsigned> qubits);
+std::map<uint64_t, double> exact_creg_distribution(const NoisyCircuit& program);
+double tvd_vs_exact(const Counts& counts, uint64_t shots, const std::map<uint64_t, double>& exact);
+
 // Flat (C ABI) view of an instrumented program; storage owned by the holder.
 struct FlatProgram {
   ssb_flat_program view{};

@@ -118,6 +118,8 @@ class Reference:
         lib.ref_run_ids.argtypes = [C.c_char_p, C.c_char_p, _pu64, C.c_uint64, C.c_uint64, C.c_uint, _pu64, _pd]
         lib.ref_batch_segments.argtypes = [C.c_char_p, C.c_char_p, _pu64, C.c_uint64, C.c_uint64, _pd, _pu64, _pu64]
         lib.ref_program_dump.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
+        lib.ref_exact_creg_distribution.argtypes = [C.c_char_p, C.c_char_p, _pu64, _pd, C.c_uint64, _pu64]
+        lib.ref_exact_distribution.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_uint), C.c_uint, _pd]
         self.lib = lib
         self.select_kernels("scalar")  # canonical arithmetic order
 
@@ -176,3 +178,21 @@ class Reference:
         buf = C.create_string_buffer(n.value + 1)
         self._check(self.lib.ref_program_dump(circuit.encode(), noise.encode(), buf, n.value + 1, None))
         return buf.value.decode()
+
+    def exact_creg_distribution(self, circuit, noise):
+        """exact_creg_distribution (density.cpp:291-306): {creg value: probability}."""
+        n = C.c_uint64()
+        self._check(self.lib.ref_exact_creg_distribution(circuit.encode(), noise.encode(), None, None, 0, C.byref(n)))
+        keys = np.empty(n.value, dtype=np.uint64)
+        probs = np.empty(n.value, dtype=np.float64)
+        self._check(self.lib.ref_exact_creg_distribution(circuit.encode(), noise.encode(), keys.ctypes.data_as(_pu64),
+                                                         probs.ctypes.data_as(_pd), n.value, C.byref(n)))
+        return keys, probs
+
+    def exact_distribution(self, circuit, noise, qubits):
+        """exact_distribution (density.cpp:280-289) over `qubits` (qubits[0] = bit 0)."""
+        q = (C.c_uint * len(qubits))(*qubits)
+        out = np.empty(1 << len(qubits), dtype=np.float64)
+        self._check(self.lib.ref_exact_distribution(circuit.encode(), noise.encode(), q, len(qubits),
+                                                    out.ctypes.data_as(_pd)))
+        return out

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <map>
 #include <numeric>
 #include <sstream>
 #include <string>
@@ -25,6 +26,7 @@
 #include <json.hpp>
 
 #include "shotsim/circuit_io.hpp"
+#include "shotsim/density.hpp"
 #include "shotsim/exec.hpp"
 #include "shotsim/exec_batch.hpp"
 #include "shotsim/exec_branch.hpp"
@@ -240,6 +242,35 @@ int ref_program_dump(const char* circuit_text, const char* noise, char* out, siz
       std::memcpy(out, s.data(), n);
       out[n] = '\0';
     }
+  });
+}
+
+// The reference's exact density-matrix evolver (density.cpp:280-306): the
+// statistical checker SURVEY.md §8(f) rank 4 asks the GPU evolver to match.
+// keys/probs NULL: size query only.
+int ref_exact_creg_distribution(const char* circuit_text, const char* noise, uint64_t* keys, double* probs,
+                                uint64_t cap, uint64_t* count) {
+  return guarded([&] {
+    const NoisyCircuit p = build(circuit_text, noise);
+    const std::map<uint64_t, double> d = exact_creg_distribution(p);
+    *count = d.size();
+    if (!keys) return;
+    if (cap < d.size()) throw std::invalid_argument("capacity too small");
+    uint64_t i = 0;
+    for (const auto& [k, v] : d) {
+      keys[i] = k;
+      probs[i] = v;
+      ++i;
+    }
+  });
+}
+
+int ref_exact_distribution(const char* circuit_text, const char* noise, const unsigned* qubits, unsigned count,
+                           double* out) {
+  return guarded([&] {
+    const NoisyCircuit p = build(circuit_text, noise);
+    const std::vector<double> d = exact_distribution(p, std::span<const unsigned>(qubits, count));
+    std::copy(d.begin(), d.end(), out);
   });
 }
 

@@ -8,10 +8,10 @@ The product is the C++/CUDA library ``lib/libshotsim_b200.so`` (C ABI in
 from ._lib import (CapacityError, ConfigError, CudaUnavailable, DegenerateDistribution, LIB_PATH,
                    ShotsimError)
 from .api import (BatchState, Engine, Program, RunOptions, RunResult, bitstring, counts_checksum_of_values,
-                  counts_from_values, executor_by_name)
+                  counts_from_values, executor_by_name, tvd_vs_exact)
 
 __all__ = [
     "BatchState", "Engine", "Program", "RunOptions", "RunResult", "bitstring", "counts_from_values",
-    "counts_checksum_of_values", "executor_by_name", "CapacityError", "ConfigError", "CudaUnavailable",
+    "counts_checksum_of_values", "executor_by_name", "tvd_vs_exact", "CapacityError", "ConfigError", "CudaUnavailable",
     "DegenerateDistribution", "ShotsimError", "LIB_PATH",
 ]

@@ -239,6 +239,37 @@ class Engine:
                                           C.c_void_p(hist_ptr)))
 
 
+    # ---- exact density-matrix reference (density.hpp:56-68), n <= 10 ----
+    def exact_creg_distribution(self, program: Program) -> Dict[int, float]:
+        """exact_creg_distribution (density.cpp:291-306), evolved on this device."""
+        n = C.c_uint64()
+        check(load().ssb_exact_creg_distribution(self._h, program.handle, None, None, 0, C.byref(n)))
+        keys = np.empty(n.value, dtype=np.uint64)
+        probs = np.empty(n.value, dtype=np.float64)
+        check(load().ssb_exact_creg_distribution(self._h, program.handle, keys.ctypes.data_as(_lib._pu64),
+                                                 probs.ctypes.data_as(_lib._pd), n.value, C.byref(n)))
+        return {int(k): float(p) for k, p in zip(keys, probs)}
+
+    def exact_distribution(self, program: Program, qubits: Sequence[int]) -> np.ndarray:
+        """exact_distribution (density.cpp:280-289) over `qubits` (qubits[0] = bit 0)."""
+        q = (C.c_uint32 * max(1, len(qubits)))(*qubits)
+        out = np.empty(1 << len(qubits), dtype=np.float64)
+        check(load().ssb_exact_distribution(self._h, program.handle, q, len(qubits), out.ctypes.data_as(_lib._pd)))
+        return out
+
+
+def tvd_vs_exact(values: np.ndarray, num_clbits: int, has_measure: bool, exact: Dict[int, float]) -> float:
+    """tvd_vs_exact (density.cpp:308-315) of per-shot register values against an exact distribution."""
+    v = np.ascontiguousarray(values, dtype=np.uint64)
+    keys = np.array(sorted(exact), dtype=np.uint64)
+    probs = np.array([exact[int(k)] for k in keys], dtype=np.float64)
+    out = C.c_double()
+    check(load().ssb_tvd_vs_exact(v.ctypes.data_as(_lib._pu64), v.size, num_clbits, int(has_measure),
+                                  keys.ctypes.data_as(_lib._pu64), probs.ctypes.data_as(_lib._pd), keys.size,
+                                  C.byref(out)))
+    return out.value
+
+
 def _fp64_peak(engine) -> float:
     out = C.c_double(0.0)
     check(load().ssb_fp64_peak(engine._h, C.byref(out)))

@@ -1,5 +1,6 @@
 // C ABI, host half: program lowering, dumps and result folding.
 #include <cstring>
+#include <map>
 
 #include "capi_internal.hpp"
 
@@ -84,6 +85,18 @@ SSB_API int ssb_counts_checksum(const uint64_t* values, uint64_t count, uint32_t
         shotsim::counts_from_values(std::span<const uint64_t>(values, count), num_clbits, has_measure != 0);
     if (checksum_out) *checksum_out = shotsim::counts_checksum(c);
     if (num_keys_out) *num_keys_out = c.size();
+  });
+}
+
+SSB_API int ssb_tvd_vs_exact(const uint64_t* values, uint64_t shots, uint32_t num_clbits, uint32_t has_measure,
+                             const uint64_t* keys, const double* probs, uint64_t count, double* tvd) {
+  return ssb::guard([&] {
+    if (!tvd || (shots && !values) || (count && (!keys || !probs))) throw std::invalid_argument("null argument");
+    const shotsim::Counts counts =
+        shotsim::counts_from_values(std::span<const uint64_t>(values, shots), num_clbits, has_measure != 0);
+    std::map<uint64_t, double> exact;
+    for (uint64_t i = 0; i < count; ++i) exact[keys[i]] = probs[i];
+    *tvd = shotsim::tvd_vs_exact(counts, shots, exact);  // density.cpp:308-315 (host/executors.cpp)
   });
 }
 

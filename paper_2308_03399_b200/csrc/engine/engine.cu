@@ -748,6 +748,12 @@ struct DeviceGuard {
 void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h, uint64_t shot_begin,
                        uint64_t count, uint64_t seed, const ssb_run_options* opts, uint64_t* values_dev,
                        ssb_stats* stats, uint64_t mem_limit_bytes);
+
+// density.cu: the exact density-matrix reference.
+std::map<uint64_t, double> exact_creg_distribution_device(const ssb_flat_program& F, cudaStream_t stream,
+                                                          uint64_t* launches, int num_sms);
+std::vector<double> exact_distribution_device(const ssb_flat_program& F, const uint32_t* qubits, unsigned count,
+                                              cudaStream_t stream, uint64_t* launches, int num_sms);
 }  // namespace ssb
 
 using namespace ssb;
@@ -891,6 +897,37 @@ SSB_API int ssb_fp64_peak(ssb_engine* E, double* ops_per_second) {
       best = std::min(best, ms);
     }
     *ops_per_second = double(grid) * kThreads * kIters * fp64_probe_ops_per_iter() / (best * 1e-3);
+  });
+}
+
+// ---- exact density-matrix reference (density.cu) ---------------------------
+SSB_API int ssb_exact_creg_distribution(ssb_engine* E, const ssb_program* prog, uint64_t* keys, double* probs,
+                                        uint64_t capacity, uint64_t* count) {
+  return guard([&] {
+    if (!E || !prog || !count) throw std::invalid_argument("null argument");
+    if ((keys == nullptr) != (probs == nullptr)) throw std::invalid_argument("keys and probs must both be set");
+    DeviceGuard g(E->device);
+    const auto dist = exact_creg_distribution_device(prog->flat.view, E->stream, &E->launches, E->num_sms);
+    *count = dist.size();
+    if (!keys) return;
+    if (capacity < dist.size()) throw shotsim::CapacityError("exact distribution has more entries than capacity");
+    uint64_t i = 0;
+    for (const auto& [k, p] : dist) {
+      keys[i] = k;
+      probs[i] = p;
+      ++i;
+    }
+  });
+}
+
+SSB_API int ssb_exact_distribution(ssb_engine* E, const ssb_program* prog, const uint32_t* qubits,
+                                   uint32_t num_qubits, double* out) {
+  return guard([&] {
+    if (!E || !prog || !out || (num_qubits && !qubits)) throw std::invalid_argument("null argument");
+    DeviceGuard g(E->device);
+    const auto dist = exact_distribution_device(prog->flat.view, qubits, num_qubits, E->stream, &E->launches,
+                                                E->num_sms);
+    std::copy(dist.begin(), dist.end(), out);
   });
 }
 

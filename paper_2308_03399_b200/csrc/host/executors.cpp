@@ -5,6 +5,7 @@
 // per device, per-shard values concatenated and folded into Counts on the
 // host (merge_counts is commutative, result.cpp:15-21).
 #include <chrono>
+#include <cmath>
 #include <cstdlib>
 #include <memory>
 #include <thread>
@@ -105,6 +106,75 @@ ExecutorFn executor_by_name(std::string_view name) {
   if (name == "gpu-batch") return &run_gpu_batch;
   if (name == "gpu-branch") return &run_gpu_branch;
   throw ConfigError("unknown strategy: " + std::string(name));
+}
+
+namespace {
+
+// Device 0 engine + flattened program for the density-matrix checker.
+template <class F>
+void with_engine(const NoisyCircuit& program, F&& f) {
+  FlatProgram flat;
+  flatten(program, flat);
+  ssb_program* prog = nullptr;
+  if (int rc = ssb_program_from_flat(&flat.view, &prog)) rethrow(rc);
+  std::unique_ptr<ssb_program, void (*)(ssb_program*)> hold(prog, ssb_program_destroy);
+  ssb_engine* E = nullptr;
+  if (int rc = ssb_engine_create(0, &E)) rethrow(rc);
+  std::unique_ptr<ssb_engine, void (*)(ssb_engine*)> hold_e(E, ssb_engine_destroy);
+  if (int rc = f(E, prog)) rethrow(rc);
+}
+
+}  // namespace
+
+std::vector<double> exact_distribution(const NoisyCircuit& program, std::span<const unsigned> qubits) {
+  if (qubits.size() > 63) throw std::invalid_argument("too many qubits");
+  std::vector<uint32_t> q(qubits.begin(), qubits.end());
+  std::vector<double> out(uint64_t{1} << q.size());
+  with_engine(program, [&](ssb_engine* E, ssb_program* p) {
+    return ssb_exact_distribution(E, p, q.data(), static_cast<uint32_t>(q.size()), out.data());
+  });
+  return out;
+}
+
+std::map<uint64_t, double> exact_creg_distribution(const NoisyCircuit& program) {
+  std::vector<uint64_t> keys;
+  std::vector<double> probs;
+  with_engine(program, [&](ssb_engine* E, ssb_program* p) {
+    uint64_t n = 0;
+    if (int rc = ssb_exact_creg_distribution(E, p, nullptr, nullptr, 0, &n)) return rc;
+    keys.resize(n);
+    probs.resize(n);
+    return ssb_exact_creg_distribution(E, p, keys.data(), probs.data(), n, &n);
+  });
+  std::map<uint64_t, double> out;
+  for (size_t i = 0; i < keys.size(); ++i) out.emplace(keys[i], probs[i]);
+  return out;
+}
+
+// density.cpp:308-315 over Counts directly (the C ABI takes per-shot values).
+double tvd_vs_exact(const Counts& counts, uint64_t shots, const std::map<uint64_t, double>& exact) {
+  std::map<uint64_t, double> empirical;
+  for (const auto& [key, n] : counts) {
+    const uint64_t v = key.empty() ? 0 : std::stoull(key, nullptr, 2);
+    empirical[v] += static_cast<double>(n) / static_cast<double>(shots);
+  }
+  double l1 = 0.0;
+  auto ie = empirical.begin();
+  auto ix = exact.begin();
+  while (ie != empirical.end() || ix != exact.end()) {
+    if (ix == exact.end() || (ie != empirical.end() && ie->first < ix->first)) {
+      l1 += std::abs(ie->second);
+      ++ie;
+    } else if (ie == empirical.end() || ix->first < ie->first) {
+      l1 += std::abs(ix->second);
+      ++ix;
+    } else {
+      l1 += std::abs(ie->second - ix->second);
+      ++ie;
+      ++ix;
+    }
+  }
+  return 0.5 * l1;
 }
 
 uint64_t default_mem_limit_bytes() {

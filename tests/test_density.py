@@ -1,0 +1,104 @@
+"""Exact density-matrix reference on the device.
+
+Parity target: the reference's own exact_creg_distribution / exact_distribution
+(proj/src/density.cpp:280-306), pinned as tests/golden/density_exact.json by
+tests/golden/make_density_golden.py. Tolerance (floating point, SURVEY §8 /
+north_star): |gpu - ref| <= 1e-10 * |ref| + 1e-15 per probability; keys exact.
+The statistical gate is the reference's: executors within TVD 0.02 of the
+exact distribution (acceptance_main.cpp:154-170, test_density.cpp:178-192).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+REL, ABS = 1e-10, 1e-15
+CASES = golden("density_exact.json")["cases"]
+ERRORS = golden("density_exact.json")["errors"]
+
+
+def _by_name(name):
+    return next(c for c in CASES if c["name"] == name)
+
+
+# ---- CPU: fixture pins (reference known answers) and host arithmetic ------------
+def test_fixture_known_answers():
+    """test_density.cpp:106-172 examples, as recorded from the reference."""
+    assert np.allclose(_by_name("qft3_noiseless")["marginal"], 0.125, rtol=1e-9)
+    assert np.allclose(_by_name("h_flip")["marginal"], [0.5, 0.5], rtol=1e-12)
+    assert np.allclose(_by_name("x_flip")["marginal"], [0.01, 0.99], rtol=1e-12)
+    inter = _by_name("intermediate")
+    assert inter["keys"] == [0b00, 0b11] and np.allclose(inter["probs"], [0.5, 0.5], rtol=1e-12)
+    reset = _by_name("reset")
+    assert reset["keys"] == [0] and abs(reset["probs"][0] - 1.0) < 1e-12
+    for c in CASES:
+        assert abs(sum(c["probs"]) - 1.0) < 1e-9, c["name"]
+
+
+def test_fixture_matches_reference_library():
+    """Re-derive a few fixtures from oracle/_ref (skipped where it is absent)."""
+    from oracle.oracle import REF_SO, Reference
+    if not REF_SO.exists():
+        pytest.skip("oracle/_ref not built")
+    ref = Reference()
+    for name in ("qft3_depol", "dyn6_depol", "rnd5_thermal"):
+        c = _by_name(name)
+        keys, probs = ref.exact_creg_distribution(c["circuit"], c["noise"])
+        assert [int(k) for k in keys] == c["keys"]
+        assert [float(p) for p in probs] == c["probs"]
+
+
+def test_tvd_host_arithmetic():
+    """ssb_tvd_vs_exact (host half of the C ABI) = half the L1 distance."""
+    from paper_2308_03399_b200 import tvd_vs_exact
+    rng = np.random.default_rng(3)
+    values = rng.integers(0, 8, size=5000).astype(np.uint64)
+    exact = {0: 0.1, 1: 0.2, 2: 0.3, 5: 0.4, 9: 0.0}
+    emp = np.bincount(values.astype(np.int64), minlength=10) / values.size
+    want = 0.5 * sum(abs(emp[k] - exact.get(k, 0.0)) for k in range(10))
+    assert abs(tvd_vs_exact(values, 4, True, exact) - want) < 1e-12
+    assert tvd_vs_exact(np.array([], dtype=np.uint64), 4, True, {}) == 0.0
+
+
+# ---- GPU: the device evolver against the reference --------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_exact_distribution_parity(engine, case):
+    from paper_2308_03399_b200 import Program
+    p = Program.from_text(case["circuit"], case["noise"])
+    got = engine.exact_creg_distribution(p)
+    assert sorted(got) == case["keys"]
+    for k, want in zip(case["keys"], case["probs"]):
+        assert abs(got[k] - want) <= REL * abs(want) + ABS, (case["name"], k, got[k], want)
+    if "qubits" in case:
+        m = engine.exact_distribution(p, case["qubits"])
+        want = np.array(case["marginal"])
+        assert np.all(np.abs(m - want) <= REL * np.abs(want) + ABS), case["name"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("err", ERRORS, ids=[e["name"] for e in ERRORS])
+def test_exact_distribution_errors(engine, err):
+    from paper_2308_03399_b200 import CapacityError, Program
+    p = Program.from_text(err["circuit"], err["noise"])
+    exc = CapacityError if err["error"] == "CapacityError" else ValueError
+    with pytest.raises(exc):
+        engine.exact_creg_distribution(p)
+
+
+@pytest.mark.gpu
+def test_executors_within_tvd_of_exact(engine):
+    """acceptance_main.cpp:154-170: qft 2..6 + depolarizing 1%, 50000 shots,
+    seed 5, both GPU executors within TVD 0.02 of the exact distribution."""
+    from paper_2308_03399_b200 import Program, RunOptions, tvd_vs_exact
+    worst = 0.0
+    for n in range(2, 7):
+        c = _by_name("qft%d_depol" % n)
+        p = Program.from_text(c["circuit"], c["noise"])
+        exact = engine.exact_creg_distribution(p)
+        f = p.flat()
+        for run in (engine.run_batch, engine.run_branch):
+            r = run(p, RunOptions(shots=50000, seed=5))
+            worst = max(worst, tvd_vs_exact(r._values, f.num_clbits, bool(f.has_measure), exact))
+    assert worst <= 0.02, worst
