@@ -102,3 +102,22 @@ def test_executors_within_tvd_of_exact(engine):
             r = run(p, RunOptions(shots=50000, seed=5))
             worst = max(worst, tvd_vs_exact(r._values, f.num_clbits, bool(f.has_measure), exact))
     assert worst <= 0.02, worst
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["ghz10_depol", "dyn6_depol", "rnd5_thermal", "qft4_depol_kraus", "qv8_readout"])
+def test_executors_match_exact_on_fixtures(engine, name):
+    """The same statistical gate on the golden programs that exercise every op
+    kind (Kraus channels, resets, conditions, intermediate measures, n = 10),
+    with the exact distribution taken from the reference's fixture, 4e5 shots."""
+    from paper_2308_03399_b200 import Program, RunOptions, tvd_vs_exact
+    c = _by_name(name)
+    p = Program.from_text(c["circuit"], c["noise"])
+    exact = dict(zip(c["keys"], c["probs"]))
+    f = p.flat()
+    # QV is the batch path's workload; its 256-way noisy fan-out makes the
+    # branch run slow without adding coverage, so it runs batch only.
+    runs = (engine.run_batch,) if name == "qv8_readout" else (engine.run_batch, engine.run_branch)
+    for run in runs:
+        r = run(p, RunOptions(shots=400000, seed=9))
+        assert tvd_vs_exact(r._values, f.num_clbits, bool(f.has_measure), exact) <= 0.02, (name, run.__name__)
