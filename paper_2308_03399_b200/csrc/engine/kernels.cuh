@@ -527,6 +527,31 @@ static __global__ void __launch_bounds__(128) g_expval2_kernel(const double2* st
   }
 }
 
+// Runs body(w) for this CTA's grid-stride items w (blockIdx.x + k*gridDim.x <
+// total) whose shot (w / per_shot) is active, in ascending k. The active flags
+// of blockDim.x items are read in parallel and ballotted into shared memory,
+// so a launch with few pending shots (later Kraus matrices) does not walk
+// every inactive item through a dependent global load. CTA-uniform; body may
+// use __syncthreads. blockDim.x: a multiple of 32, <= 256.
+template <class F>
+__device__ __forceinline__ void for_active_items(uint64_t total, uint64_t per_shot, const uint8_t* active, F&& body) {
+  __shared__ uint32_t act_bits[8];
+  const uint32_t nt = blockDim.x;
+  for (uint64_t base = 0;; base += nt) {
+    const uint64_t w0 = blockIdx.x + base * gridDim.x;
+    if (w0 >= total) break;
+    const uint64_t w = w0 + uint64_t{threadIdx.x} * gridDim.x;
+    const bool on = w < total && (!active || active[w / per_shot]);
+    __syncthreads();  // the previous round's readers of act_bits are done
+    const uint32_t b = __ballot_sync(0xffffffffu, on);
+    if ((threadIdx.x & 31) == 0) act_bits[threadIdx.x >> 5] = b;
+    __syncthreads();
+    for (uint32_t wi = 0; wi < nt / 32; ++wi) {
+      for (uint32_t m = act_bits[wi]; m; m &= m - 1) body(w0 + uint64_t{wi * 32 + __ffs(m) - 1} * gridDim.x);
+    }
+  }
+}
+
 // g_expval2_kernel with the amplitudes staged through shared memory: a CTA of
 // 128 threads owns 128 consecutive 8-group leaves (1024 groups) of one shot,
 // copies their 4 x 1024 amplitudes in with coalesced LDGSTS, then every thread
@@ -544,9 +569,8 @@ static __global__ void __launch_bounds__(kE2Threads) g_expval2_staged_kernel(con
   const uint64_t off[4] = {0, uint64_t{1} << R.q[0], uint64_t{1} << R.q[1],
                            (uint64_t{1} << R.q[0]) | (uint64_t{1} << R.q[1])};
   const uint32_t e2_s = static_cast<uint32_t>(__cvta_generic_to_shared(e2));
-  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
+  for_active_items(total, ctas_per_shot, active, [&](uint64_t w) {
     const uint64_t s = w / ctas_per_shot, g0 = (w % ctas_per_shot) * kE2Groups;
-    if (active && !active[s]) continue;  // CTA-uniform
     const double2* a = st + (seg_of(slots, s) << R.n);
     __syncthreads();  // previous item's reads of e2 are done
     for (uint32_t e = threadIdx.x; e < 4 * kE2Groups; e += kE2Threads) {
@@ -574,9 +598,59 @@ static __global__ void __launch_bounds__(kE2Threads) g_expval2_staged_kernel(con
       }
       part[(s * R.nq + qi) * R.nb + b] = acc;
     }
-  }
+  });
 }
 constexpr size_t kE2Smem = 4 * (kE2Groups + kE2Groups / 8) * sizeof(double2);
+
+// Same staging, but the compute is spread over 2x the threads: each of 256
+// threads forms the row sums of 4 groups (group 256*i + t), and lane 8j of
+// each warp chains the 8 row sums of its leaf, taken from lanes 8j..8j+7 by
+// shuffles, in group order — the same DADD sequence as the per-leaf kernel
+// (expval_generic, statevector.cpp:56-80), so results are bit-identical.
+// More resident warps per SM (and shorter dependent chains per thread) let
+// the LDGSTS copies of one CTA overlap the arithmetic of the others.
+constexpr unsigned kE2Block = 256;
+static __global__ void __launch_bounds__(kE2Block) g_expval2_split_kernel(const double2* st, uint64_t S, RedSpec R,
+                                                                         const uint8_t* active, double* part,
+                                                                         const uint32_t* slots = nullptr) {
+  extern __shared__ double2 e2[];  // 4 x (1024 + 128) amplitudes
+  const uint64_t ctas_per_shot = R.nb / kE2Threads, total = S * ctas_per_shot;
+  const uint64_t off[4] = {0, uint64_t{1} << R.q[0], uint64_t{1} << R.q[1],
+                           (uint64_t{1} << R.q[0]) | (uint64_t{1} << R.q[1])};
+  const uint32_t e2_s = static_cast<uint32_t>(__cvta_generic_to_shared(e2));
+  const uint32_t lane = threadIdx.x & 31, leader = lane & ~7u;
+  for_active_items(total, ctas_per_shot, active, [&](uint64_t w) {
+    const uint64_t s = w / ctas_per_shot, g0 = (w % ctas_per_shot) * kE2Groups;
+    const double2* a = st + (seg_of(slots, s) << R.n);
+    __syncthreads();  // previous item's reads of e2 are done
+    for (uint32_t e = threadIdx.x; e < 4 * kE2Groups; e += kE2Block) {
+      const uint32_t c = e / kE2Groups, g = e % kE2Groups;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(e2_s + 16 * e2_slot(c, g)),
+                   "l"(a + (expand_sorted(g0 + g, R.sorted, 2) + off[c])));
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (uint32_t qi = 0; qi < R.nq; ++qi) {
+      double2 m[16];
+      load_matrix<4>(R.mats + 16 * qi, m);
+      const uint64_t cls = R.cls[qi];
+#pragma unroll
+      for (uint32_t i = 0; i < kE2Groups / kE2Block; ++i) {
+        const uint32_t g = kE2Block * i + threadIdx.x;
+        double2 in[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) in[c] = e2[e2_slot(c, g)];
+        double row = 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) row = __dadd_rn(row, c_norm(row_apply<4>(m, cls, r, in)));
+        double acc = 0.0;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, row, leader + j));
+        if (lane == leader) part[(s * R.nq + qi) * R.nb + (g0 + g) / 8] = acc;
+      }
+    }
+  });
+}
 
 // R_EXPVAL1 partials staged the same way: a CTA of 128 threads owns 128
 // consecutive 512-pair blocks of one (shot, matrix); each round copies 16
@@ -594,7 +668,7 @@ static __global__ void __launch_bounds__(kE1Threads) g_expval1_staged_kernel(con
   const unsigned t = R.q[0];
   const uint64_t bit = uint64_t{1} << t;
   const uint32_t e1_s = static_cast<uint32_t>(__cvta_generic_to_shared(e1));
-  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {
+  for (uint64_t w = blockIdx.x; w < total; w += gridDim.x) {  // grid ~ items: no active-item walk needed
     const uint64_t grp = w % ctas_per, qs = w / ctas_per, qi = qs % R.nq, s = qs / R.nq;
     if (active && !active[s]) continue;  // CTA-uniform
     const double2* a = st + (seg_of(slots, s) << R.n);
@@ -630,10 +704,15 @@ inline void launch_reduce(cudaStream_t stream, const double2* st, uint64_t S, co
   const uint64_t work = reduce_threads(R, S);
   if (R.mode == R_EXPVAL2 && R.blk == 8 && R.nb % kE2Threads == 0 && !std::getenv("SHOTSIM_B200_EXPVAL2_DIRECT")) {
     // (the attribute is per device; setting it is cheap)
-    cudaFuncSetAttribute(g_expval2_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kE2Smem));
     const uint64_t items = S * (R.nb / kE2Threads);
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(items, 148u * 6u)));
-    g_expval2_staged_kernel<<<grid, kE2Threads, kE2Smem, stream>>>(st, S, R, active, part, slots);
+    if (std::getenv("SHOTSIM_B200_EXPVAL2_LEAF")) {  // A/B: one thread per leaf
+      cudaFuncSetAttribute(g_expval2_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kE2Smem));
+      g_expval2_staged_kernel<<<grid, kE2Threads, kE2Smem, stream>>>(st, S, R, active, part, slots);
+    } else {
+      cudaFuncSetAttribute(g_expval2_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kE2Smem));
+      g_expval2_split_kernel<<<grid, kE2Block, kE2Smem, stream>>>(st, S, R, active, part, slots);
+    }
   } else if (R.mode == R_EXPVAL1 && R.blk % kE1Pairs == 0 && R.nb % kE1Threads == 0 &&
              !std::getenv("SHOTSIM_B200_EXPVAL1_DIRECT")) {
     cudaFuncSetAttribute(g_expval1_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kE1Smem));
