@@ -623,10 +623,14 @@ static __global__ void __launch_bounds__(kE2Block) g_expval2_split_kernel(const 
     const uint64_t s = w / ctas_per_shot, g0 = (w % ctas_per_shot) * kE2Groups;
     const double2* a = st + (seg_of(slots, s) << R.n);
     __syncthreads();  // previous item's reads of e2 are done
-    for (uint32_t e = threadIdx.x; e < 4 * kE2Groups; e += kE2Block) {
-      const uint32_t c = e / kE2Groups, g = e % kE2Groups;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(e2_s + 16 * e2_slot(c, g)),
-                   "l"(a + (expand_sorted(g0 + g, R.sorted, 2) + off[c])));
+    // One group index expansion feeds the group's 4 amplitudes (for each c the
+    // warp's copies are still consecutive groups: coalesced as before).
+#pragma unroll
+    for (uint32_t g = threadIdx.x; g < kE2Groups; g += kE2Block) {
+      const double2* base = a + expand_sorted(g0 + g, R.sorted, 2);
+#pragma unroll
+      for (uint32_t c = 0; c < 4; ++c)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(e2_s + 16 * e2_slot(c, g)), "l"(base + off[c]));
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
