@@ -121,3 +121,29 @@ def test_executors_match_exact_on_fixtures(engine, name):
     for run in runs:
         r = run(p, RunOptions(shots=400000, seed=9))
         assert tvd_vs_exact(r._values, f.num_clbits, bool(f.has_measure), exact) <= 0.02, (name, run.__name__)
+
+
+@pytest.mark.gpu
+def test_cpp_api(tmp_path):
+    """The C++ drop-in (include/shotsim_b200.hpp): exact_creg_distribution,
+    exact_distribution and tvd_vs_exact over Counts, compiled against the
+    in-tree library like a reference-side caller would be."""
+    import subprocess
+    from conftest import ROOT
+    exe = tmp_path / "density_api"
+    lib = ROOT / "paper_2308_03399_b200" / "lib"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"), str(ROOT / "tests" / "cpp" / "density_api.cpp"),
+                    "-o", str(exe), "-L", str(lib), "-lshotsim_b200", f"-Wl,-rpath,{lib}"], check=True, timeout=300)
+    c = _by_name("rnd5_thermal")
+    (tmp_path / "c.txt").write_text(c["circuit"])
+    (tmp_path / "n.json").write_text(c["noise"])
+    out = subprocess.run([str(exe), str(tmp_path / "c.txt"), str(tmp_path / "n.json")], capture_output=True, text=True,
+                         timeout=300, check=True).stdout.splitlines()
+    rows = [l.split() for l in out if l[0].isdigit()]
+    assert [int(k) for k, _ in rows] == c["keys"]
+    for (_, p), want in zip(rows, c["probs"]):
+        assert abs(float.fromhex(p) - want) <= REL * abs(want) + ABS
+    marg = next(l for l in out if l.startswith("marginal0")).split()[1:]
+    assert abs(sum(float.fromhex(x) for x in marg) - 1.0) < 1e-9
+    assert float(next(l for l in out if l.startswith("tvd")).split()[1]) <= 0.02
+    assert "capacity error" in out
