@@ -251,8 +251,8 @@ struct Evolver {
     else if (k == 2) dm_conj_sum<2><<<grid(blocks), 256, 0, stream>>>(rho, mats, a);
     else throw std::invalid_argument("density evolver supports 1- and 2-qubit operators");
     launched();
-    // `mats` is reused by the next op: keep the host vector alive until copied.
-    CKD(cudaStreamSynchronize(stream));
+    // No sync: the pageable H2D copy has staged `m` when it returns, and the
+    // next op's copy into `mats` is stream-ordered after this kernel.
   }
 
   std::vector<double2> matrix(uint32_t index, unsigned k) const {
