@@ -147,3 +147,25 @@ def test_cpp_api(tmp_path):
     assert abs(sum(float.fromhex(x) for x in marg) - 1.0) < 1e-9
     assert float(next(l for l in out if l.startswith("tvd")).split()[1]) <= 0.02
     assert "capacity error" in out
+
+
+@pytest.mark.gpu
+def test_c_abi_argument_errors(engine):
+    """C ABI contract of the checker: size query, capacity, bad qubits."""
+    import ctypes as C
+    from paper_2308_03399_b200 import CapacityError, Program, _lib
+    c = _by_name("qft3_depol")
+    p = Program.from_text(c["circuit"], c["noise"])
+    lib = _lib.load()
+    n = C.c_uint64()
+    assert lib.ssb_exact_creg_distribution(engine.handle, p.handle, None, None, 0, C.byref(n)) == 0
+    assert n.value == len(c["keys"])
+    keys = (C.c_uint64 * 2)()
+    probs = (C.c_double * 2)()
+    rc = lib.ssb_exact_creg_distribution(engine.handle, p.handle, keys, probs, 2, C.byref(n))
+    assert rc == _lib.SSB_ERR_CAPACITY
+    with pytest.raises(ValueError):
+        engine.exact_distribution(p, [5])
+    big = Program.from_text(_by_name("ghz10_depol")["circuit"].replace("qubits 10", "qubits 11"), "")
+    with pytest.raises(CapacityError):
+        engine.exact_distribution(big, [0])
