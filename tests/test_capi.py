@@ -56,3 +56,14 @@ def test_shape_specialisation_compiles_without_gpu(key, tile):
     cfg = cc.CONFIGS[key]
     prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
     assert prog.specialise_check(tile) > 0
+
+
+@pytest.mark.gpu
+def test_integration_stub_runs_verbatim():
+    """INTEGRATION.md §2's ctypes stub is executed as written (scripts/stub_check.py)."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    r = subprocess.run([sys.executable, str(ROOT / "scripts" / "stub_check.py")], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "stub ok" in r.stdout, r.stderr[-2000:]
