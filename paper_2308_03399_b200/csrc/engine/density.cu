@@ -45,7 +45,7 @@ namespace ssb {
 
 namespace {
 
-constexpr unsigned kMaxKraus = 16;  // matrices per channel held in constant-size args
+constexpr unsigned kInitialKraus = 16;  // matrix slots allocated up front (grown on demand)
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -206,7 +206,8 @@ struct Evolver {
   uint64_t d;
   std::vector<void*> allocs;
   double2* scratch = nullptr;
-  double2* mats = nullptr;  // up to kMaxKraus 4x4 matrices
+  double2* mats = nullptr;  // Kraus / unitary matrices of the current op
+  size_t mats_cap = 0;      // in double2
 
   Evolver(const ssb_flat_program& f, cudaStream_t s, uint64_t* l, int sms)
       : F(f), stream(s), launches(l), num_sms(sms), n(f.num_qubits), d(1ull << f.num_qubits) {}
@@ -243,8 +244,14 @@ struct Evolver {
     for (unsigned i = 0; i < k; ++i) a.q[i] = a.sorted[i] = qubits[i];
     std::sort(a.sorted, a.sorted + k);
     const unsigned side = 1u << k;
-    if (count > kMaxKraus || m.size() != size_t(count) * side * side)
-      throw std::invalid_argument("density evolver: channel too large");
+    if (m.size() != size_t(count) * side * side) throw std::invalid_argument("density evolver: bad channel");
+    if (m.size() > mats_cap) {  // channels of any length (the reference has no cap)
+      void* p = nullptr;
+      CKD(cudaMalloc(&p, m.size() * sizeof(double2)));
+      allocs.push_back(p);  // the old slot table is freed with the rest
+      mats = static_cast<double2*>(p);
+      mats_cap = m.size();
+    }
     CKD(cudaMemcpyAsync(mats, m.data(), m.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
     const uint64_t blocks = 1ull << (2 * (n - k));
     if (k == 1) dm_conj_sum<1><<<grid(blocks), 256, 0, stream>>>(rho, mats, a);
@@ -296,9 +303,10 @@ struct Evolver {
     scratch = alloc_rho();
     {
       void* p = nullptr;
-      CKD(cudaMalloc(&p, kMaxKraus * 16 * sizeof(double2)));
+      CKD(cudaMalloc(&p, kInitialKraus * 16 * sizeof(double2)));
       allocs.push_back(p);
       mats = static_cast<double2*>(p);
+      mats_cap = kInitialKraus * 16;
     }
     std::vector<Traj> trajs(1);
     trajs[0].rho = alloc_rho();

@@ -44,6 +44,12 @@ def cases():
     out.append(("rnd5_thermal", cc.random_layers(5, 4, 77), cc.thermal_noise(0.05, 0.1), [0, 4]))
     out.append(("ghz10_depol", cc.ghz(10), depol, [9, 0]))
     out.append(("qv8_readout", cc.quantum_volume(8, 3, 11), cc.qv_noise(0.02, 0.03), None))
+    # A 2q channel longer than 16 matrices: the thermal tensor product with
+    # every matrix split in two halves (18 matrices, still complete).
+    rules = json.loads(cc.thermal_noise(0.05, 0.1))["rules"]
+    h = 0.5 ** 0.5
+    rules[1]["channel"]["matrices"] = [[[h * x, h * y] for x, y in m] for m in rules[1]["channel"]["matrices"] for _ in (0, 1)]
+    out.append(("rnd4_kraus18", cc.random_layers(4, 3, 5), json.dumps({"rules": rules}), [1, 2]))
     return out
 
 
