@@ -105,7 +105,8 @@ def test_executors_within_tvd_of_exact(engine):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["ghz10_depol", "dyn6_depol", "rnd5_thermal", "qft4_depol_kraus", "qv8_readout"])
+@pytest.mark.parametrize("name", ["ghz10_depol", "dyn6_depol", "rnd5_thermal", "qft4_depol_kraus", "qv8_readout",
+                                  "rnd4_kraus18"])
 def test_executors_match_exact_on_fixtures(engine, name):
     """The same statistical gate on the golden programs that exercise every op
     kind (Kraus channels, resets, conditions, intermediate measures, n = 10),
