@@ -291,3 +291,21 @@ def test_kraus_probabilities_large_states(engine, oracle, monkeypatch, direct):
     prog = Program.from_text(cc.random_layers(17, depth=3, seed=17), cc.thermal_noise(0.05, 0.1))
     want = oracle.run_shots(prog, np.arange(32), 5, threads=8)
     assert (values(engine.run_batch(prog, RunOptions(shots=32, seed=5))) == want).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,tile", [(6, 3), (8, 5)])
+def test_kraus_long_channel_all_paths(engine, oracle, n, tile):
+    """A 2q Kraus channel of 18 matrices (thermal tensor product, every matrix
+    split in halves; tests/golden/make_density_golden.py): longer than any
+    built-in channel, bit-exact on every path."""
+    import json
+    rules = json.loads(cc.thermal_noise(0.05, 0.1))["rules"]
+    h = 0.5 ** 0.5
+    rules[1]["channel"]["matrices"] = [[[h * x, h * y] for x, y in m] for m in rules[1]["channel"]["matrices"]
+                                       for _ in (0, 1)]
+    prog = Program.from_text(cc.random_layers(n, depth=4, seed=n), json.dumps({"rules": rules}))
+    want = oracle.run_shots(prog, np.arange(200), 3)
+    for kw in ({}, dict(resident_max_qubits=1, tile_qubits=tile)):
+        assert (values(engine.run_batch(prog, RunOptions(shots=200, seed=3, **kw))) == want).all()
+    assert (values(engine.run_branch(prog, RunOptions(shots=200, seed=3, branch_budget=16))) == want).all()
