@@ -40,7 +40,7 @@ extern "C" {
 #define SSB_API
 #endif
 
-#define SSB_ABI_VERSION 1
+#define SSB_ABI_VERSION 2
 
 typedef enum ssb_status {
   SSB_OK = 0,
@@ -135,13 +135,36 @@ typedef struct ssb_batch ssb_batch;
 typedef struct ssb_run_options {
   uint64_t max_batch_size;   /* 0: derive from mem_limit_bytes                 */
   uint64_t branch_budget;    /* gpu-branch: max live states (>= 1)             */
-  uint64_t mem_limit_bytes;  /* 0: SHOTSIM_MEM_LIMIT_BYTES or 90% of free HBM  */
-  uint32_t check_norms;      /* reserved (debug norm checks)                   */
-  uint32_t collect_leaf_stats;
+  uint64_t mem_limit_bytes;  /* 0: SHOTSIM_MEM_LIMIT_BYTES or 80% of free HBM  */
+  uint32_t check_norms;      /* gpu-batch: |norm^2 - 1| <= 1e-10 after every op
+                                (exec_batch.cpp:217-224), else SSB_ERR_RUNTIME;
+                                runs the op-at-a-time kernels (debug/tests) */
+  uint32_t collect_leaf_stats; /* gpu-branch: shots per leaf into leaf_shots */
   uint32_t resident_max_qubits; /* n <= this: whole program SM-resident (0: 13) */
   uint32_t tile_qubits;      /* streamed mode: local qubits per HBM tile (0: 12) */
   uint32_t profile;          /* 1: per-kernel-class CUDA-event times in stats   */
   uint32_t interpret_only;   /* 1: never use the shape-specialised tile kernel  */
+  /* ---- ABI 2 ---- */
+  uint32_t fused_matrices;   /* gpu-batch, streamed sizes: 1 = multiply each
+                                run of gates + Pauli sites on <= 2 qubits into
+                                one 4x4 per shot (FMA arithmetic; amplitudes
+                                within 1e-10 of the reference) and guard every
+                                amplitude-dependent decision: a shot whose draw
+                                lies within the rounding bound of a boundary is
+                                replayed exactly on the device, so counts stay
+                                bit-exact. Programs the fused planner does not
+                                cover run exactly (stats->fused_blocks = 0). */
+  uint32_t reserved0;
+  uint64_t* leaf_shots;      /* collect_leaf_stats: HOST array receiving
+                                BranchStats::leaf_shots (exec_branch.cpp:280),
+                                leaf order of the reference; NULL: count only */
+  uint64_t leaf_shots_capacity;
+  double* states_out;        /* DEBUG (parity tests): HOST array of
+                                shot_count * 2^n complex (re, im) doubles that
+                                receives, per shot, the state terminal sampling
+                                reads (or the final state when the program is
+                                not sampling-eligible) — BatchState::segment
+                                (exec_batch.hpp:31-32) of every executor path */
 } ssb_run_options;
 
 typedef struct ssb_stats {
@@ -164,6 +187,12 @@ typedef struct ssb_stats {
   uint64_t trunk_skipped;    /* streamed: (shot, pass) pairs not run because
                                 the shot's noise draws had not yet diverged
                                 from the shared noiseless trunk */
+  /* ---- ABI 2 ---- */
+  uint64_t num_leaves;       /* gpu-branch: leaves over all passes */
+  uint64_t fused_blocks;     /* fused_matrices: 4x4 blocks per shot (0: exact) */
+  uint64_t guard_flagged;    /* fused_matrices: shots replayed exactly because
+                                a decision fell inside the guard band */
+  double guard_delta;        /* fused_matrices: largest guard half-width used */
 } ssb_stats;
 
 SSB_API const char* ssb_last_error(void);

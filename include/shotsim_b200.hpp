@@ -243,13 +243,16 @@ struct RunResult {
 struct RunOptions {
   uint64_t shots = 1;
   uint64_t seed = 0;
-  unsigned workers = 1;          // GPUs (devices 0..workers-1), shot-sharded
+  unsigned workers = 1;          // shot shards (contiguous id ranges); shard g runs on
+                                 // device g % device_count — a performance hint only:
+                                 // results never depend on it (exec.hpp:24-27)
   uint64_t max_batch_size = 0;
   uint64_t branch_budget = 64;
   uint64_t mem_limit_bytes = 0;
   bool record_shot_values = false;
   bool check_norms = false;
   bool collect_leaf_stats = false;
+  bool fused_matrices = false;   // ssb_run_options::fused_matrices (gpu-batch)
 };
 
 RunResult run_gpu_batch(const NoisyCircuit& program, const RunOptions& options);

@@ -68,6 +68,10 @@ class RunOptionsC(C.Structure):
         ("check_norms", C.c_uint32), ("collect_leaf_stats", C.c_uint32),
         ("resident_max_qubits", C.c_uint32), ("tile_qubits", C.c_uint32),
         ("profile", C.c_uint32), ("interpret_only", C.c_uint32),
+        # ABI 2
+        ("fused_matrices", C.c_uint32), ("reserved0", C.c_uint32),
+        ("leaf_shots", C.POINTER(C.c_uint64)), ("leaf_shots_capacity", C.c_uint64),
+        ("states_out", C.POINTER(C.c_double)),
     ]
 
 
@@ -79,6 +83,9 @@ class StatsC(C.Structure):
         ("sample_seconds", C.c_double), ("specialised_shapes", C.c_uint64),
         ("sampling_serial_chunks", C.c_uint64),
         ("trunk_skipped", C.c_uint64),
+        # ABI 2
+        ("num_leaves", C.c_uint64), ("fused_blocks", C.c_uint64), ("guard_flagged", C.c_uint64),
+        ("guard_delta", C.c_double),
     ]
 
 

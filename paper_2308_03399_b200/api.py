@@ -112,18 +112,21 @@ class RunOptions:
     tile_qubits: int = 0
     profile: bool = False         # per-kernel-class CUDA-event timing in the stats
     interpret_only: bool = False  # never use the run-time shape-specialised tile kernel
+    fused_matrices: bool = False  # 4x4 block fusion + guard band (ssb_run_options::fused_matrices)
+    export_states: bool = False   # debug: RunResult.states = each shot's pre-sampling state
 
     def to_c(self) -> _lib.RunOptionsC:
         return _lib.RunOptionsC(self.max_batch_size, self.branch_budget, self.mem_limit_bytes,
                                 int(self.check_norms), int(self.collect_leaf_stats),
                                 self.resident_max_qubits, self.tile_qubits, int(self.profile),
-                                int(self.interpret_only))
+                                int(self.interpret_only), int(self.fused_matrices), 0)
 
 
 @dataclass
 class BranchStats:
     peak_states: int = 0
     passes: int = 0
+    leaf_shots: List[int] = field(default_factory=list)
 
 
 @dataclass
@@ -142,6 +145,10 @@ class RunResult:
     specialised_shapes: int = 0
     sampling_serial_chunks: int = 0
     trunk_skipped: int = 0
+    fused_blocks: int = 0
+    guard_flagged: int = 0
+    guard_delta: float = 0.0
+    states: Optional[np.ndarray] = None
 
 
 def bitstring(value: int, width: int) -> str:
@@ -202,17 +209,32 @@ class Engine:
         values = np.empty(count, dtype=np.uint64)
         st = _lib.StatsC()
         co = opts.to_c()
+        f = program.flat()
+        states = None
+        if opts.export_states:
+            states = np.empty((count, 1 << f.num_qubits), dtype=np.complex128)
+            co.states_out = states.ctypes.data_as(_lib._pd)
+        leaves = np.empty(0, dtype=np.uint64)
+        if opts.collect_leaf_stats:
+            leaves = np.empty(4096, dtype=np.uint64)
+            co.leaf_shots, co.leaf_shots_capacity = leaves.ctypes.data_as(_lib._pu64), leaves.size
         check(fn(self._h, program.handle, shot_begin, count, opts.seed, C.byref(co),
                  values.ctypes.data_as(_lib._pu64), C.byref(st)))
-        f = program.flat()
+        if opts.collect_leaf_stats and st.num_leaves > leaves.size:  # rerun with room for every leaf
+            leaves = np.empty(st.num_leaves, dtype=np.uint64)
+            co.leaf_shots, co.leaf_shots_capacity = leaves.ctypes.data_as(_lib._pu64), leaves.size
+            check(fn(self._h, program.handle, shot_begin, count, opts.seed, C.byref(co),
+                     values.ctypes.data_as(_lib._pu64), C.byref(st)))
         r = RunResult(counts=counts_from_values(values, f.num_clbits, bool(f.has_measure)),
                       shot_values=values if opts.record_shot_values else None,
                       dispatch_count=st.dispatch_count, peak_states=st.peak_states,
-                      branch=BranchStats(st.peak_states, st.passes), strategy=name, shots=count,
+                      branch=BranchStats(st.peak_states, st.passes,
+                                         [int(x) for x in leaves[:st.num_leaves]]), strategy=name, shots=count,
                       seed=opts.seed, device_seconds=st.device_seconds, wall_seconds=st.wall_seconds,
                       fused_passes=st.fused_passes, specialised_shapes=st.specialised_shapes,
                       sampling_serial_chunks=st.sampling_serial_chunks,
-                      trunk_skipped=st.trunk_skipped)
+                      trunk_skipped=st.trunk_skipped, fused_blocks=st.fused_blocks,
+                      guard_flagged=st.guard_flagged, guard_delta=st.guard_delta, states=states)
         r._values = values
         return r
 

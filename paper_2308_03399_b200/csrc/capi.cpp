@@ -56,7 +56,11 @@ SSB_API int ssb_program_from_flat(const ssb_flat_program* flat, ssb_program** ou
   });
 }
 
-SSB_API void ssb_program_destroy(ssb_program* program) { delete program; }
+SSB_API void ssb_program_destroy(ssb_program* program) {
+  if (!program) return;
+  ssb::evict_program(program->uid);
+  delete program;
+}
 
 SSB_API int ssb_program_flat(const ssb_program* program, ssb_flat_program* out) {
   return ssb::guard([&] {

@@ -26,6 +26,8 @@ struct CudaError : std::runtime_error {
 
 void set_last_error(const std::string& msg);
 uint64_t next_program_uid();
+// engine.cu: drop every engine's device copies of program `uid`.
+void evict_program(uint64_t uid);
 
 // Maps the reference's exception types onto ssb_status (shotsim_b200.h).
 template <class F>

@@ -207,40 +207,34 @@ __global__ void b_apply(ProgView P, DevOp op, double2* pool, const ChildOp* kids
   }
 }
 
-// Leaf cumulative over all sampled outcomes (groups = 1 case) — one thread
-// per leaf, the reference's sequential order; last[] = last nonzero outcome.
+// Leaf cumulative over all sampled outcomes (groups = 1 case): one WARP per
+// leaf builds the reference's sequential cumulative (exec_branch.cpp:267-276
+// -> pick_outcome's order) bit-exactly with the warp-parallel exact scan
+// (exact_scan.cuh); last[] = last nonzero outcome (count: none).
 __global__ void b_leaf_cum_full(ProgView P, const double2* pool, const DevNode* leaves, uint64_t nl, double* cum,
                                 uint64_t* last) {
-  const uint64_t l = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
-  if (l >= nl) return;
+  const uint64_t l = (uint64_t{blockIdx.x} * blockDim.x + threadIdx.x) / 32;
+  if (l >= nl) return;  // whole warps exit together
   const unsigned n = P.n;
   const double2* a = pool + (uint64_t{leaves[l].slot} << n);
   const uint64_t count = uint64_t{1} << P.nsample;
-  double c = 0.0;
-  uint64_t lz = count;
   double* out = cum + l * count;
-  for (uint64_t m = 0; m < count; ++m) {
-    const double p = c_norm(a[P.sample_identity ? m : scatter_bits(m, P.sample_qubits, P.nsample)]);
-    c = __dadd_rn(c, p);
-    out[m] = c;
-    if (p > 0.0) lz = m;
-  }
-  last[l] = lz;
+  const bool ident = P.sample_identity;
+  const ExactPick r = warp_exact_scan(
+      [&](uint64_t m) { return c_norm(a[ident ? m : scatter_bits(m, P.sample_qubits, P.nsample)]); }, count, -1.0,
+      [&](uint64_t m, double v) { out[m] = v; });
+  if ((threadIdx.x & 31) == 0) last[l] = r.any_nonzero ? r.outcome : count;
 }
 
 // Same from precomputed probabilities (k < n sampled qubits).
 __global__ void b_leaf_cum_probs(const double* probs, uint64_t nl, uint64_t count, double* cum, uint64_t* last) {
-  const uint64_t l = uint64_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  const uint64_t l = (uint64_t{blockIdx.x} * blockDim.x + threadIdx.x) / 32;
   if (l >= nl) return;
-  double c = 0.0;
-  uint64_t lz = count;
-  for (uint64_t m = 0; m < count; ++m) {
-    const double p = probs[l * count + m];
-    c = __dadd_rn(c, p);
-    cum[l * count + m] = c;
-    if (p > 0.0) lz = m;
-  }
-  last[l] = lz;
+  const double* pr = probs + l * count;
+  double* out = cum + l * count;
+  const ExactPick r = warp_exact_scan([&](uint64_t m) { return pr[m]; }, count, -1.0,
+                                      [&](uint64_t m, double v) { out[m] = v; });
+  if ((threadIdx.x & 31) == 0) last[l] = r.any_nonzero ? r.outcome : count;
 }
 
 __global__ void b_leaf_values(ProgView P, const DevNode* leaves, uint64_t nl, const uint64_t* shots, uint64_t total,
@@ -632,7 +626,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
     using T = std::remove_pointer_t<decltype(type_tag)>;
     return static_cast<T*>(E.host(E.ctx, name, std::max<size_t>(count, 1) * sizeof(T)));
   };
-  uint64_t peak = 0, passes = 0;
+  uint64_t peak = 0, passes = 0, num_leaves = 0;
   // Planner work arrays, reused across sites (no per-site allocation).
   struct Cand {
     uint64_t parent;
@@ -1023,6 +1017,21 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       hl[x] = {live[x].slot, 1, live[x].off, live[x].len, live[x].creg};
       total += live[x].len;
     }
+    if (opts && opts->collect_leaf_stats) {  // BranchStats::leaf_shots (exec_branch.cpp:280)
+      for (uint64_t x = 0; x < nl; ++x, ++num_leaves)
+        if (opts->leaf_shots && num_leaves < opts->leaf_shots_capacity) opts->leaf_shots[num_leaves] = live[x].len;
+    }
+    if (opts && opts->states_out && total > 0) {
+      // Debug export: every shot's leaf state (what its terminal sampling reads).
+      std::vector<uint64_t> hshots(total);
+      CKB(cudaMemcpyAsync(hshots.data(), cur_shots, total * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      CKB(cudaStreamSynchronize(s));
+      for (uint64_t x = 0; x < nl; ++x)
+        for (uint64_t p = live[x].off; p < live[x].off + live[x].len; ++p)
+          CKB(cudaMemcpyAsync(opts->states_out + 2 * ((hshots[p] - shot_begin) << n), pool + (uint64_t{live[x].slot} << n),
+                              A * sizeof(double2), cudaMemcpyDeviceToHost, s));
+      CKB(cudaStreamSynchronize(s));
+    }
     if (nl > 0 && total > 0) {
       DevNode* leaves = dnodes.get(nl);
       CKB(cudaMemcpyAsync(leaves, hl.data(), nl * sizeof(DevNode), cudaMemcpyHostToDevice, s));
@@ -1033,7 +1042,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
         cum = dcum.get(nl * cnt);
         last = dlast.get(nl);
         if (P.nsample == n) {
-          b_leaf_cum_full<<<gridn(nl, 64), 64, 0, s>>>(P, pool, leaves, nl, cum, last);
+          b_leaf_cum_full<<<gridn(nl * 32, 128), 128, 0, s>>>(P, pool, leaves, nl, cum, last);
           launched();
         } else {
           RedSpec R{};
@@ -1056,7 +1065,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
           launched();
           g_finish_kernel<<<static_cast<unsigned>(std::min<uint64_t>(nl * R.nq, 1u << 20)), NT, 0, s>>>(nl, R.nq, R.nb, 0, nullptr, part, probs);
           launched();
-          b_leaf_cum_probs<<<gridn(nl, 64), 64, 0, s>>>(probs, nl, cnt, cum, last);
+          b_leaf_cum_probs<<<gridn(nl * 32, 128), 128, 0, s>>>(probs, nl, cnt, cum, last);
           launched();
           CKB(cudaStreamSynchronize(s));
         }
@@ -1072,6 +1081,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
   if (stats) {
     stats->peak_states = peak;
     stats->passes = passes;
+    stats->num_leaves = num_leaves;
     stats->dispatch_count = *E.launches - launches0;
   }
 }

@@ -9,6 +9,8 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -25,7 +27,7 @@ namespace ssb {
 
 // resident_warp.cu: the resident kernel with one-warp CTAs (small states).
 int launch_resident_warp(const void* view, uint64_t seed, uint64_t shot_begin, uint64_t count, uint64_t* values,
-                         int* err, cudaStream_t stream, size_t smem, int num_sms);
+                         int* err, cudaStream_t stream, size_t smem, int num_sms, void* exp);
 
 // specialise.cpp: the shape-specialised tile-pass kernel for a plan, or null.
 const void* specialised_tile_kernel(const HostDevProgram& h);
@@ -58,6 +60,10 @@ struct ssb_engine {
   size_t smem_optin = 0;
   int* err = nullptr;
   unsigned long long* serial_chunks = nullptr;  // sampling chunks replayed sequentially
+  unsigned* bad_op = nullptr;                   // check_norms: first op whose norm drifted
+  // Device copies of programs, keyed by (program uid, plan). Entries are
+  // evicted when their ssb_program is destroyed (ssb::evict_program).
+  std::mutex programs_mu;
   std::map<std::pair<uint64_t, unsigned>, std::unique_ptr<ssb::DevProgram>> programs;
   std::map<std::string, std::pair<void*, size_t>> scratch;
   std::map<std::string, std::pair<void*, size_t>> host_scratch;  // pinned
@@ -137,8 +143,13 @@ T* upload(DevProgram& d, const std::vector<T>& v) {
 }
 
 // tile_k == 0 selects the resident plan (whole program in one pass, k = n).
+// Live engines, so that destroying a program evicts its device copies.
+std::mutex g_engines_mu;
+std::set<ssb_engine*> g_engines;
+
 DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile_k) {
   const auto key = std::make_pair(prog->uid, tile_k);
+  std::lock_guard<std::mutex> lk(E->programs_mu);
   auto it = E->programs.find(key);
   if (it != E->programs.end()) return *it->second;
   auto d = std::make_unique<DevProgram>();
@@ -224,6 +235,14 @@ void check_device_error(ssb_engine* E) {
   if (h == DEV_DEGENERATE) {
     CK(cudaMemsetAsync(E->err, 0, sizeof(int), E->stream));
     throw shotsim::DegenerateDistribution("measured distribution sums to zero or branch has zero probability");
+  }
+  if (h == DEV_NORM) {  // exec_batch.cpp:217-224
+    unsigned op = 0;
+    CK(cudaMemcpyAsync(&op, E->bad_op, sizeof op, cudaMemcpyDeviceToHost, E->stream));
+    CK(cudaMemsetAsync(E->err, 0, sizeof(int), E->stream));
+    CK(cudaMemsetAsync(E->bad_op, 0xFF, sizeof(unsigned), E->stream));
+    CK(cudaStreamSynchronize(E->stream));
+    throw std::runtime_error("batch segment norm drifted after op " + std::to_string(op));
   }
 }
 
@@ -528,6 +547,59 @@ RunConfig config_of(const ssb_run_options* o) {
   return rc;
 }
 
+// Debug export (ssb_run_options::states_out): wave slots [0, S) -> host.
+void export_states(ssb_engine* E, const ssb_run_options* opts, const double2* state, uint64_t w0, uint64_t S,
+                   unsigned n) {
+  if (!opts || !opts->states_out) return;
+  CK(cudaMemcpyAsync(opts->states_out + 2 * (w0 << n), state, (S << n) * sizeof(double2), cudaMemcpyDeviceToHost,
+                     E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+}
+
+uint64_t wave_for(const ssb_run_options* opts, uint64_t count, uint64_t seg, uint64_t limit) {
+  const uint64_t wave = opts && opts->max_batch_size
+                            ? opts->max_batch_size
+                            : std::max<uint64_t>(1, std::min<uint64_t>(limit, uint64_t{16} << 30) / seg);
+  const uint64_t largest = std::min(wave, count);
+  if (largest * seg > limit)
+    throw shotsim::CapacityError("batch of " + std::to_string(largest) + " shots needs " +
+                                 std::to_string(largest * seg) +
+                                 " bytes; lower max_batch_size or raise the memory limit");
+  return largest;
+}
+
+// check_norms (exec_batch.cpp:200-227): BatchState::run op at a time with the
+// norm of every segment checked after every non-barrier op. A debug mode: the
+// per-op kernels instead of the fused passes, same arithmetic and decisions.
+void run_batch_checked(ssb_engine* E, const ssb_program* prog, uint64_t shot_begin, uint64_t count, uint64_t seed,
+                       const ssb_run_options* opts, uint64_t* values_dev, ssb_stats* stats) {
+  DevProgram& dp = device_program(E, prog, kTileDefault);
+  const unsigned n = dp.host.n;
+  const uint64_t seg = (uint64_t{1} << n) * sizeof(double2);
+  const uint64_t wave = wave_for(opts, count, seg, mem_limit(opts));
+  double2* state = static_cast<double2*>(scratch(E, "state", wave * seg));
+  uint64_t waves = 0;
+  for (uint64_t w0 = 0; w0 < count; w0 += wave, ++waves) {
+    const uint64_t S = std::min(wave, count - w0);
+    g_init_kernel<<<grid_for(S << n), NT, 0, E->stream>>>(state, S, n, values_dev + w0);
+    launched(E);
+    const SegCtx c{state, S, seed, nullptr, shot_begin + w0, nullptr, values_dev + w0};
+    for (uint32_t i = 0; i < dp.host.end; ++i) {
+      apply_op(E, dp, i, c, false);
+      if (dp.host.ops[i].kind == K_BARRIER) continue;
+      g_norm_check_kernel<<<static_cast<unsigned>(std::min<uint64_t>(S, 1u << 20)), NT, 0, E->stream>>>(
+          state, S, n, i, E->err, E->bad_op);
+      launched(E);
+    }
+    export_states(E, opts, state, w0, S, n);
+    if (dp.host.eligible) sample_terminal(E, dp, c);
+  }
+  if (stats) {
+    stats->peak_states = wave;
+    stats->passes = waves;
+  }
+}
+
 // gpu-batch over shot ids [shot_begin, shot_begin+count) (or explicit ids).
 void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begin, uint64_t count, uint64_t seed,
                       const ssb_run_options* opts, uint64_t* values_dev, ssb_stats* stats) {
@@ -536,6 +608,14 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
   const unsigned n = prog->dev.n;
   const uint64_t launches0 = E->launches;
   CK(cudaMemsetAsync(E->serial_chunks, 0, sizeof(unsigned long long), E->stream));
+  if (opts && opts->check_norms) {
+    run_batch_checked(E, prog, shot_begin, count, seed, opts, values_dev, stats);
+    if (stats) stats->dispatch_count = E->launches - launches0;
+    return;
+  }
+  double2* exp_dev = (opts && opts->states_out)
+                         ? static_cast<double2*>(scratch(E, "export", (count << n) * sizeof(double2)))
+                         : nullptr;
   // The resident plan (and its shared-memory size) for states that may fit.
   DevProgram* rdp = n <= rc.resident_max ? &device_program(E, prog, 0) : nullptr;
   const size_t rsmem = rdp ? resident_smem(rdp->host) : ~size_t{0};
@@ -551,7 +631,7 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
     timer.begin(0);
     if (n <= warp_max) {
       const int g = launch_resident_warp(&dp.view, seed, shot_begin, count, values_dev, E->err, E->stream, rsmem,
-                                         E->num_sms);
+                                         E->num_sms, exp_dev);
       if (g < 0) throw CudaError("resident (warp) launch failed");
       grid = static_cast<uint64_t>(g);
       launched(E);
@@ -561,10 +641,11 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, resident_kernel, NT, rsmem));
       grid = std::min<uint64_t>(count, static_cast<uint64_t>(std::max(1, per_sm)) * E->num_sms);
       resident_kernel<<<static_cast<unsigned>(grid), NT, rsmem, E->stream>>>(dp.view, seed, nullptr, shot_begin, count,
-                                                                             values_dev, E->err);
+                                                                             values_dev, E->err, exp_dev);
       launched(E);
     }
     timer.end(0);
+    if (exp_dev) export_states(E, opts, exp_dev, 0, count, n);
     if (stats) {
       stats->peak_states = std::min<uint64_t>(count, grid);
       stats->passes = 1;
@@ -715,11 +796,13 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
           timer.end(1);
         } else {
           if (wtrunk) activate(npass);  // shots that never diverged
+          export_states(E, opts, state, w0, S, n);
           timer.begin(2);
           sample_terminal(E, dp, c);
           timer.end(2);
         }
       }
+      if (!h.eligible) export_states(E, opts, state, w0, S, n);
     }
     if (stats) {
       stats->peak_states = std::min(wave, count);
@@ -756,6 +839,30 @@ std::vector<double> exact_distribution_device(const ssb_flat_program& F, const u
                                               cudaStream_t stream, uint64_t* launches, int num_sms);
 }  // namespace ssb
 
+namespace ssb {
+// Called by ssb_program_destroy: frees every engine's device copies of the
+// program (the caller guarantees no run with it is in flight, as the
+// reference's executors borrow the program for the duration of a run).
+void evict_program(uint64_t uid) {
+  std::lock_guard<std::mutex> lk(g_engines_mu);
+  for (ssb_engine* E : g_engines) {
+    std::lock_guard<std::mutex> plk(E->programs_mu);
+    for (auto it = E->programs.begin(); it != E->programs.end();) {
+      if (it->first.first == uid) {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(E->device);
+        cudaStreamSynchronize(E->stream);
+        it = E->programs.erase(it);
+        if (prev >= 0) cudaSetDevice(prev);
+      } else {
+        ++it;
+      }
+    }
+  }
+}
+}  // namespace ssb
+
 using namespace ssb;
 
 extern "C" {
@@ -770,8 +877,9 @@ SSB_API int ssb_engine_create(int device, ssb_engine** out) {
     DeviceGuard g(device);
     cudaDeviceProp prop{};
     CK(cudaGetDeviceProperties(&prop, device));
-    if (prop.major < 10) throw CudaError("shotsim_b200 is built for sm_100a (Blackwell); device is sm_" +
-                                         std::to_string(prop.major) + std::to_string(prop.minor));
+    if (prop.major != 10 || prop.minor != 0)
+      throw CudaError("shotsim_b200 is built for sm_100a (B200) only; device is sm_" + std::to_string(prop.major) +
+                      std::to_string(prop.minor));
     auto E = std::make_unique<ssb_engine>();
     E->device = device;
     E->num_sms = prop.multiProcessorCount;
@@ -783,12 +891,20 @@ SSB_API int ssb_engine_create(int device, ssb_engine** out) {
     CK(cudaMemset(E->err, 0, sizeof(int)));
     CK(cudaMalloc(&E->serial_chunks, sizeof(unsigned long long)));
     CK(cudaMemset(E->serial_chunks, 0, sizeof(unsigned long long)));
+    CK(cudaMalloc(&E->bad_op, sizeof(unsigned)));
+    CK(cudaMemset(E->bad_op, 0xFF, sizeof(unsigned)));
+    std::lock_guard<std::mutex> lk(g_engines_mu);
+    g_engines.insert(E.get());
     *out = E.release();
   });
 }
 
 SSB_API void ssb_engine_destroy(ssb_engine* E) {
   if (!E) return;
+  {
+    std::lock_guard<std::mutex> lk(g_engines_mu);
+    g_engines.erase(E);
+  }
   cudaSetDevice(E->device);
   cudaStreamSynchronize(E->stream);
   E->programs.clear();
@@ -796,6 +912,7 @@ SSB_API void ssb_engine_destroy(ssb_engine* E) {
   for (auto& [name, slot] : E->host_scratch) cudaFreeHost(slot.first);
   cudaFree(E->err);
   cudaFree(E->serial_chunks);
+  cudaFree(E->bad_op);
   cudaEventDestroy(E->ev0);
   cudaEventDestroy(E->ev1);
   cudaStreamDestroy(E->stream);

@@ -16,6 +16,7 @@
 #pragma once
 
 #include "tile_pass.cuh"
+#include "exact_scan.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -134,8 +135,11 @@ __host__ __device__ inline uint64_t resident_probs_doubles(const ProgView& P) {
 }
 
 // ---------------------------------------------------------------------------
+// exp (debug, may be null): receives each shot's state as terminal sampling
+// reads it (or the final state), BatchState::segment (exec_batch.hpp:31-32).
 static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint64_t seed, const uint64_t* ids,
-                                                         uint64_t shot_begin, uint64_t S, uint64_t* values, int* err) {
+                                                         uint64_t shot_begin, uint64_t S, uint64_t* values, int* err,
+                                                         double2* exp) {
   extern __shared__ double2 smem[];
   const unsigned n = P.n;
   const uint64_t A = uint64_t{1} << n;
@@ -246,22 +250,32 @@ static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint
         __syncthreads();
       }
     }
+    if (exp) {
+      for (uint64_t j = threadIdx.x; j < A; j += NT) exp[(s << n) + j] = st[j];
+    }
     if (P.eligible) {
       const unsigned k = P.nsample;
       const double u = keyed_uniform(seed, shot, P.num_events);
+      // pick_outcome (statevector.cpp:185-197) by warp 0 with the exact
+      // warp-parallel sequential sum (exact_scan.cuh).
       if (k == n) {
-        if (threadIdx.x == 0) {
-          uint64_t o = 0;
-          if (!scan_full([&](uint64_t idx) { return st[idx]; }, A, P.sample_identity, P.sample_qubits, k, u, &o))
-            raise(err, DEV_DEGENERATE);
-          bc_out = o;
+        if (threadIdx.x < 32) {
+          const bool ident = P.sample_identity;
+          const ExactPick r = warp_exact_scan(
+              [&](uint64_t m) { return c_norm(st[ident ? m : scatter_bits(m, P.sample_qubits, k)]); }, A, u, NoSum{});
+          if (threadIdx.x == 0) {
+            if (!r.any_nonzero) raise(err, DEV_DEGENERATE);
+            bc_out = r.outcome;
+          }
         }
       } else {
         cta_outcome_probs(st, n, P.sample_qubits, k, probs, red);
-        if (threadIdx.x == 0) {
-          uint64_t o = 0;
-          if (!pick_outcome(probs, uint64_t{1} << k, u, &o)) raise(err, DEV_DEGENERATE);
-          bc_out = o;
+        if (threadIdx.x < 32) {
+          const ExactPick r = warp_exact_scan([&](uint64_t m) { return probs[m]; }, uint64_t{1} << k, u, NoSum{});
+          if (threadIdx.x == 0) {
+            if (!r.any_nonzero) raise(err, DEV_DEGENERATE);
+            bc_out = r.outcome;
+          }
         }
       }
       __syncthreads();
@@ -1144,6 +1158,33 @@ static __global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, do
 #pragma unroll
   for (int j = 0; j < 8; ++j) s = __dadd_rn(s, x[j]);
   if (s == 12345.678) *sink = s;  // keep the chains alive
+}
+
+// check_norms (exec_batch.cpp:217-224): |sum |a|^2 - 1| <= 1e-10 per segment
+// after op `op_index`; the first failing op (smallest index) is kept. One CTA
+// per shot; the order of the sum is irrelevant at this tolerance.
+static __global__ void __launch_bounds__(NT) g_norm_check_kernel(const double2* st, uint64_t S, unsigned n,
+                                                                 uint32_t op_index, int* err, unsigned* bad_op) {
+  __shared__ double part[NT / 32];
+  const uint64_t A = uint64_t{1} << n;
+  for (uint64_t s = blockIdx.x; s < S; s += gridDim.x) {
+    const double2* a = st + (s << n);
+    double acc = 0.0;
+    for (uint64_t j = threadIdx.x; j < A; j += NT) acc += c_norm(a[j]);
+#pragma unroll
+    for (int off = 16; off > 0; off /= 2) acc += __shfl_down_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < NT / 32; ++i) t += part[i];
+      if (!(fabs(t - 1.0) <= 1e-10)) {
+        atomicCAS(err, 0, DEV_NORM);
+        atomicMin(bad_op, op_index);
+      }
+    }
+    __syncthreads();
+  }
 }
 
 static __global__ void g_histogram_kernel(const uint64_t* values, uint64_t count, uint32_t bits, unsigned long long* hist) {

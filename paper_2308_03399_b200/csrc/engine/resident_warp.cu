@@ -24,7 +24,7 @@ namespace ssb {
 
 // view: a ProgView (identical layout in both builds).
 int launch_resident_warp(const void* view, uint64_t seed, uint64_t shot_begin, uint64_t count, uint64_t* values,
-                         int* err, cudaStream_t stream, size_t smem, int num_sms) {
+                         int* err, cudaStream_t stream, size_t smem, int num_sms, void* exp) {
   const auto& P = *static_cast<const ssb_w32::ProgView*>(view);
   if (cudaFuncSetAttribute(ssb_w32::resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
@@ -35,7 +35,8 @@ int launch_resident_warp(const void* view, uint64_t seed, uint64_t shot_begin, u
     return -1;
   const uint64_t grid = std::min<uint64_t>(count, static_cast<uint64_t>(std::max(1, per_sm)) * num_sms);
   ssb_w32::resident_kernel<<<static_cast<unsigned>(grid), ssb_w32::NT, smem, stream>>>(P, seed, nullptr, shot_begin,
-                                                                                       count, values, err);
+                                                                                       count, values, err,
+                                                                                       static_cast<double2*>(exp));
   return cudaGetLastError() == cudaSuccess ? static_cast<int>(grid) : -1;
 }
 

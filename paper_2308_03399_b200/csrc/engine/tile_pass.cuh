@@ -6,7 +6,7 @@
 
 namespace ssb {
 
-enum DevError : int { DEV_OK = 0, DEV_DEGENERATE = 1 };
+enum DevError : int { DEV_OK = 0, DEV_DEGENERATE = 1, DEV_NORM = 2 };
 
 struct ProgView {
   const DevOp* ops;

@@ -1,14 +1,21 @@
 // C++ executors with the reference's ExecutorFn contract (exec.hpp:24-35):
 // "gpu-batch" / "gpu-branch" run the instrumented program on sm_100a through
-// the C ABI. RunOptions::workers selects how many GPUs (devices
-// 0..workers-1) share the shots: contiguous shot-id shards, one host thread
-// per device, per-shard values concatenated and folded into Counts on the
-// host (merge_counts is commutative, result.cpp:15-21).
+// the C ABI. RunOptions::workers keeps the reference's meaning of a
+// parallelism hint (exec.hpp:24-27: results never depend on it): the shots
+// split into min(workers, shots) contiguous shot-id shards and shard g runs on
+// device g % device_count, one host thread per device running its shards in
+// order on a pooled engine (engines — and their device buffers and programs
+// cache — persist across calls). Per-shard values are concatenated and folded
+// into Counts on the host (merge_counts is commutative, result.cpp:15-21).
 #include <chrono>
 #include <cmath>
+#include <map>
 #include <cstdlib>
 #include <memory>
+#include <mutex>
 #include <thread>
+
+#include <cuda_runtime.h>
 
 #include "../capi_internal.hpp"
 
@@ -30,6 +37,33 @@ namespace {
 using RunFn = int (*)(ssb_engine*, const ssb_program*, uint64_t, uint64_t, uint64_t, const ssb_run_options*,
                       uint64_t*, ssb_stats*);
 
+// One engine per device, created on first use and kept for the process
+// (re-creating an engine per call would re-allocate its state buffers — up to
+// 16 GiB — and re-upload programs every run). Each device's engine is used by
+// one thread at a time.
+struct PooledEngine {
+  std::mutex mu;
+  ssb_engine* engine = nullptr;
+};
+
+PooledEngine& pooled_engine(int device) {
+  static std::mutex pool_mu;
+  static std::map<int, std::unique_ptr<PooledEngine>> pool;  // never freed: lives until exit
+  std::lock_guard<std::mutex> lk(pool_mu);
+  auto& slot = pool[device];
+  if (!slot) slot = std::make_unique<PooledEngine>();
+  return *slot;
+}
+
+int device_count() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 RunResult run_sharded(const NoisyCircuit& program, const RunOptions& o, RunFn fn, const char* name) {
   if (o.shots < 1) throw std::invalid_argument("shots must be >= 1");
   if (o.workers < 1) throw std::invalid_argument("workers must be >= 1");
@@ -47,32 +81,51 @@ RunResult run_sharded(const NoisyCircuit& program, const RunOptions& o, RunFn fn
   ro.mem_limit_bytes = o.mem_limit_bytes;
   ro.check_norms = o.check_norms;
   ro.collect_leaf_stats = o.collect_leaf_stats;
+  ro.fused_matrices = o.fused_matrices;
 
-  const unsigned G = static_cast<unsigned>(std::min<uint64_t>(o.workers, o.shots));
+  const int ndev = device_count();
+  if (ndev == 0) throw std::runtime_error("CUDA: no CUDA device available (shotsim_b200 has no CPU execution path)");
+  const uint64_t G = std::min<uint64_t>(o.workers, o.shots);  // shards
   std::vector<uint64_t> values(o.shots);
+  std::vector<uint64_t> shard_begin(G + 1, 0);
+  for (uint64_t g = 0; g < G; ++g) shard_begin[g + 1] = shard_begin[g] + o.shots / G + (g < o.shots % G ? 1 : 0);
   std::vector<ssb_stats> stats(G);
-  std::vector<int> rcs(G, 0);
-  std::vector<std::string> errs(G);
+  std::vector<std::vector<uint64_t>> leaves(G);
+  const unsigned D = static_cast<unsigned>(std::min<uint64_t>(G, static_cast<uint64_t>(ndev)));  // devices used
+  std::vector<int> rcs(D, 0);
+  std::vector<std::string> errs(D);
   std::vector<std::thread> pool;
-  uint64_t begin = 0;
-  for (unsigned g = 0; g < G; ++g) {
-    const uint64_t len = o.shots / G + (g < o.shots % G ? 1 : 0);
-    pool.emplace_back([&, g, begin, len] {
-      ssb_engine* E = nullptr;
-      rcs[g] = ssb_engine_create(static_cast<int>(g), &E);
-      if (rcs[g] == 0) {
-        rcs[g] = fn(E, prog, begin, len, o.seed, &ro, values.data() + begin, &stats[g]);
-        ssb_engine_destroy(E);
+  for (unsigned d = 0; d < D; ++d) {
+    pool.emplace_back([&, d] {
+      PooledEngine& pe = pooled_engine(static_cast<int>(d));
+      std::lock_guard<std::mutex> lk(pe.mu);
+      if (!pe.engine) rcs[d] = ssb_engine_create(static_cast<int>(d), &pe.engine);
+      for (uint64_t g = d; rcs[d] == 0 && g < G; g += D) {
+        ssb_run_options so = ro;
+        std::vector<uint64_t>& lv = leaves[g];
+        if (o.collect_leaf_stats) {
+          lv.resize(1024);
+          so.leaf_shots = lv.data();
+          so.leaf_shots_capacity = lv.size();
+        }
+        const uint64_t b = shard_begin[g], len = shard_begin[g + 1] - b;
+        rcs[d] = fn(pe.engine, prog, b, len, o.seed, &so, values.data() + b, &stats[g]);
+        if (rcs[d] == 0 && o.collect_leaf_stats && stats[g].num_leaves > lv.size()) {  // too small: rerun sized
+          lv.resize(stats[g].num_leaves);
+          so.leaf_shots = lv.data();
+          so.leaf_shots_capacity = lv.size();
+          rcs[d] = fn(pe.engine, prog, b, len, o.seed, &so, values.data() + b, &stats[g]);
+        }
+        if (rcs[d] == 0 && o.collect_leaf_stats) lv.resize(stats[g].num_leaves);
       }
-      if (rcs[g]) errs[g] = ssb_last_error();
+      if (rcs[d]) errs[d] = ssb_last_error();
     });
-    begin += len;
   }
   for (auto& t : pool) t.join();
-  for (unsigned g = 0; g < G; ++g)
-    if (rcs[g]) {
-      ssb::set_last_error(errs[g]);
-      rethrow(rcs[g]);
+  for (unsigned d = 0; d < D; ++d)
+    if (rcs[d]) {
+      ssb::set_last_error(errs[d]);
+      rethrow(rcs[d]);
     }
 
   RunResult r;
@@ -80,11 +133,17 @@ RunResult run_sharded(const NoisyCircuit& program, const RunOptions& o, RunFn fn
   r.shots = o.shots;
   r.seed = o.seed;
   r.workers = o.workers;
-  for (const ssb_stats& s : stats) {
+  // Shards on one device run one after another: peak = the largest shard's
+  // peak per device, summed over the devices running concurrently.
+  std::vector<uint64_t> dev_peak(D, 0);
+  for (uint64_t g = 0; g < G; ++g) {
+    const ssb_stats& s = stats[g];
     r.dispatch_count += s.dispatch_count;
-    r.peak_states += s.peak_states;
+    dev_peak[g % D] = std::max(dev_peak[g % D], s.peak_states);
     r.branch.passes = std::max(r.branch.passes, s.passes);
+    r.branch.leaf_shots.insert(r.branch.leaf_shots.end(), leaves[g].begin(), leaves[g].end());
   }
+  for (uint64_t p : dev_peak) r.peak_states += p;
   r.branch.peak_states = r.peak_states;
   r.counts = counts_from_values(values, program.num_clbits, program.has_measure);
   if (o.record_shot_values) r.shot_values = std::move(values);
@@ -118,10 +177,11 @@ void with_engine(const NoisyCircuit& program, F&& f) {
   ssb_program* prog = nullptr;
   if (int rc = ssb_program_from_flat(&flat.view, &prog)) rethrow(rc);
   std::unique_ptr<ssb_program, void (*)(ssb_program*)> hold(prog, ssb_program_destroy);
-  ssb_engine* E = nullptr;
-  if (int rc = ssb_engine_create(0, &E)) rethrow(rc);
-  std::unique_ptr<ssb_engine, void (*)(ssb_engine*)> hold_e(E, ssb_engine_destroy);
-  if (int rc = f(E, prog)) rethrow(rc);
+  PooledEngine& pe = pooled_engine(0);
+  std::lock_guard<std::mutex> lk(pe.mu);
+  if (!pe.engine)
+    if (int rc = ssb_engine_create(0, &pe.engine)) rethrow(rc);
+  if (int rc = f(pe.engine, prog)) rethrow(rc);
 }
 
 }  // namespace

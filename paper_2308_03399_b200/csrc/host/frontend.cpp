@@ -835,7 +835,24 @@ NoisyCircuit unflatten(const ssb_flat_program& v) {
   p.has_measure = v.has_measure != 0;
   p.sampling_eligible = v.sampling_eligible != 0;
   p.terminal_measure_begin = v.terminal_measure_begin;
-  auto read_matrix = [&v](uint32_t idx, unsigned k) {
+  // Every count and index is validated BEFORE it is used to read a caller
+  // buffer: a matrix slot holds at most a 4x4 (SSB_MATRIX_STRIDE doubles), so
+  // matrices are 1- or 2-qubit; term / channel / matrix ranges must lie
+  // inside their arrays; arrays with a nonzero count must be non-null.
+  auto need = [](bool ok, const char* what) {
+    if (!ok) throw std::invalid_argument(std::string("malformed flat program: ") + what);
+  };
+  need(v.num_qubits >= 1 && v.num_qubits <= 30, "num_qubits outside 1..30");
+  need(v.num_clbits <= 64, "num_clbits > 64");
+  need(!v.num_ops || v.ops, "null ops");
+  need(!v.num_terms || v.terms, "null terms");
+  need(!v.num_channels || v.channels, "null channels");
+  need(!v.num_matrices || v.matrices, "null matrices");
+  need(!v.num_sample_qubits || v.sample_qubits, "null sample_qubits");
+  need(!v.num_sample_writes || (v.sample_write_clbit && v.sample_write_pos), "null sample_writes");
+  need(v.terminal_measure_begin <= v.num_ops, "terminal_measure_begin > num_ops");
+  auto read_matrix = [&v, &need](uint32_t idx, unsigned k) {
+    need(k == 1 || k == 2, "matrix arity outside 1..2");
     if (idx >= v.num_matrices) throw std::invalid_argument("matrix index out of range");
     GateMatrix m{k, {}};
     const double* src = v.matrices + size_t(idx) * SSB_MATRIX_STRIDE;
@@ -845,6 +862,9 @@ NoisyCircuit unflatten(const ssb_flat_program& v) {
   for (uint64_t c = 0; c < v.num_channels; ++c) {
     KrausError k;
     k.arity = v.channels[c].arity;
+    need(k.arity == 1 || k.arity == 2, "channel arity outside 1..2");
+    need(uint64_t{v.channels[c].matrix_begin} + v.channels[c].num_matrices <= v.num_matrices,
+         "channel matrices out of range");
     for (uint32_t i = 0; i < v.channels[c].num_matrices; ++i)
       k.matrices.push_back(read_matrix(v.channels[c].matrix_begin + i, k.arity));
     p.kraus_channels.push_back(std::move(k));
@@ -853,6 +873,9 @@ NoisyCircuit unflatten(const ssb_flat_program& v) {
     const ssb_flat_op& o = v.ops[i];
     if (o.kind > SSB_OP_BARRIER || o.num_qubits > SSB_MAX_OP_QUBITS)
       throw std::invalid_argument("malformed flat op");
+    for (uint32_t b = 0; b < o.num_qubits; ++b) need(o.qubits[b] < v.num_qubits, "op qubit out of range");
+    if (o.kind == SSB_OP_PAULI)
+      need(o.term_count >= 1 && uint64_t{o.term_begin} + o.term_count <= v.num_terms, "op terms out of range");
     ProgramOp op;
     op.kind = static_cast<ProgramOp::Kind>(o.kind);
     op.qubits.assign(o.qubits, o.qubits + o.num_qubits);
@@ -877,6 +900,7 @@ NoisyCircuit unflatten(const ssb_flat_program& v) {
     }
     p.ops.push_back(std::move(op));
   }
+  need(v.num_sample_qubits <= v.num_qubits, "too many sample qubits");
   p.sample_qubits.assign(v.sample_qubits, v.sample_qubits + v.num_sample_qubits);
   for (uint32_t i = 0; i < v.num_sample_writes; ++i)
     p.sample_writes.emplace_back(v.sample_write_clbit[i], v.sample_write_pos[i]);

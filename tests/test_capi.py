@@ -26,7 +26,7 @@ def test_header_symbols_exported():
 
 
 def test_abi_version():
-    assert _lib.load().ssb_abi_version() == 1
+    assert _lib.load().ssb_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_gpu():

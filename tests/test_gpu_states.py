@@ -1,0 +1,80 @@
+"""Amplitude-level parity of every executor path against the reference's own
+BatchState states (oracle/_ref, ref_batch_segments over exec_batch.cpp:200-227;
+the state terminal sampling reads, or the final state when the program is not
+sampling-eligible), exported through ssb_run_options::states_out:
+
+* the SM-resident program kernel (n <= 13),
+* the HBM tile passes — run-time shape-specialised and interpreter builds,
+* the shot-branching executor (each shot's leaf state).
+
+Exact paths must be bit-identical (np.array_equal; only the sign of an exact
+zero may differ) and within north_star's 1e-10 relative bound; the fused-
+matrix mode (4x4 block products, FMA) must be within 1e-10 relative.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2308_03399_b200 import Program, RunOptions, circuits as cc
+
+pytestmark = pytest.mark.gpu
+
+IDS = 6
+
+
+def programs(n):
+    return {
+        "qv_pauli": (cc.quantum_volume(n, depth=4, seed=n), cc.qv_noise()),
+        "layers_kraus": (cc.random_layers(n, depth=3, seed=n), cc.thermal_noise(0.05, 0.1)),
+        "dynamic": (cc.dynamic(n, rounds=2), cc.depolarizing_model(0.03)),
+    }
+
+
+@pytest.fixture(scope="module")
+def ref():
+    from oracle.oracle import Reference
+    return Reference()
+
+
+def rel_err(got, want):
+    return np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300)
+
+
+PATHS = {
+    "resident": (lambda n: n <= 13, dict()),
+    "tile_jit": (lambda n: True, dict(resident_max_qubits=1, tile_qubits=10)),
+    "tile_interp": (lambda n: True, dict(resident_max_qubits=1, tile_qubits=10, interpret_only=True)),
+    "tile_default": (lambda n: n > 13, dict()),
+    "branch": (lambda n: True, None),
+}
+
+
+@pytest.mark.parametrize("n", [12, 14, 16])
+@pytest.mark.parametrize("path", list(PATHS))
+def test_states_equal_reference(engine, ref, n, path):
+    ok, kw = PATHS[path]
+    if not ok(n):
+        pytest.skip("path not used at this size")
+    for name, (circ, noise) in programs(n).items():
+        if n == 16 and name != "qv_pauli" and path != "tile_default":
+            continue  # keep the reference's CPU side short; the qv case covers every path at 16
+        want, wregs, _ = ref.batch_segments(circ, noise, list(range(IDS)), 11, n)
+        prog = Program.from_text(circ, noise)
+        if kw is None:
+            r = engine.run_branch(prog, RunOptions(shots=IDS, seed=11, branch_budget=64, export_states=True))
+        else:
+            r = engine.run_batch(prog, RunOptions(shots=IDS, seed=11, export_states=True, **kw))
+        assert np.array_equal(r.states, want), (path, name, n, max(rel_err(g, w) for g, w in zip(r.states, want)))
+        assert max(rel_err(g, w) for g, w in zip(r.states, want)) <= 1e-10
+
+
+@pytest.mark.parametrize("n", [14, 16])
+def test_fused_states_within_bound(engine, ref, n):
+    """fused_matrices: amplitudes within 1e-10 relative of the reference."""
+    circ, noise = programs(n)["qv_pauli"]
+    want, _, _ = ref.batch_segments(circ, noise, list(range(IDS)), 11, n)
+    r = engine.run_batch(Program.from_text(circ, noise),
+                         RunOptions(shots=IDS, seed=11, export_states=True, fused_matrices=True))
+    assert r.fused_blocks > 0
+    errs = [rel_err(g, w) for g, w in zip(r.states, want)]
+    assert max(errs) <= 1e-10, errs
