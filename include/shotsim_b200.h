@@ -256,6 +256,21 @@ SSB_API int ssb_program_specialise_check(const ssb_program* program, uint32_t ti
 SSB_API int ssb_program_pass_map(const ssb_program* program, uint32_t tile_qubits, uint32_t* pass_of_op,
                                  uint64_t cap, uint32_t* num_passes);
 
+/* Diagnostics of the fused-matrix plan (ssb_run_options::fused_matrices) for
+ * `tile_qubits` local qubits (0: default); host only. ok = 0: the program is
+ * outside the fused planner's scope and runs exactly (reason in
+ * ssb_last_error() is NOT set; the run is simply exact). */
+typedef struct ssb_fused_info {
+  uint32_t ok;
+  uint32_t passes;           /* HBM tile passes per shot                     */
+  uint32_t blocks;           /* fused 4x4 blocks per shot                    */
+  uint32_t groups;           /* register groups (<= 4 qubits) over all passes */
+  uint32_t max_pass_blocks;
+  uint32_t reserved;
+  double err_bound;          /* bound on ||psi_fused - psi_reference||_2      */
+} ssb_fused_info;
+SSB_API int ssb_program_fused_info(const ssb_program* program, uint32_t tile_qubits, ssb_fused_info* out);
+
 /* FP64-pipe roofline probe: the sustained rate of rounded DMUL/DADD (no FMA,
  * the engine's arithmetic) over the whole device, in FP64 ops per second,
  * measured with CUDA events (the denominator of bench.py's fp64 roofline). */

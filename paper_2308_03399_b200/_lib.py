@@ -89,6 +89,11 @@ class StatsC(C.Structure):
     ]
 
 
+class FusedInfoC(C.Structure):
+    _fields_ = [("ok", C.c_uint32), ("passes", C.c_uint32), ("blocks", C.c_uint32), ("groups", C.c_uint32),
+                ("max_pass_blocks", C.c_uint32), ("reserved", C.c_uint32), ("err_bound", C.c_double)]
+
+
 _vp = C.c_void_p
 _u64 = C.c_uint64
 _pu64 = C.POINTER(C.c_uint64)
@@ -117,6 +122,7 @@ SIGNATURES = {
     "ssb_exact_distribution": (C.c_int, [_vp, _vp, C.POINTER(C.c_uint32), C.c_uint32, _pd]),
     "ssb_tvd_vs_exact": (C.c_int, [_pu64, _u64, C.c_uint32, C.c_uint32, _pu64, _pd, _u64, _pd]),
     "ssb_program_specialise_check": (C.c_int, [_vp, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "ssb_program_fused_info": (C.c_int, [_vp, C.c_uint32, C.POINTER(FusedInfoC)]),
     "ssb_program_pass_map": (C.c_int, [_vp, C.c_uint32, C.POINTER(C.c_uint32), _u64, C.POINTER(C.c_uint32)]),
     "ssb_batch_create": (C.c_int, [_vp, _vp, _pu64, _u64, _u64, C.POINTER(_vp)]),
     "ssb_batch_destroy": (None, [_vp]),

@@ -65,6 +65,12 @@ class Program:
                                           f.num_ops, C.byref(n)))
         return out.astype(np.int64) - ((out == 0xFFFFFFFF) * (1 << 32))
 
+    def fused_info(self, tile_qubits: int = 0) -> dict:
+        """Diagnostics of the fused-matrix plan (host only)."""
+        i = _lib.FusedInfoC()
+        check(load().ssb_program_fused_info(self._h, tile_qubits, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in _lib.FusedInfoC._fields_ if f != "reserved"}
+
     def dump(self) -> str:
         n = C.c_size_t()
         check(load().ssb_program_dump(self._h, None, 0, C.byref(n)))

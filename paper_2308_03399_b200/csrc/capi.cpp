@@ -3,6 +3,7 @@
 #include <map>
 
 #include "capi_internal.hpp"
+#include "engine/fused.hpp"
 
 namespace ssb {
 
@@ -136,5 +137,19 @@ extern "C" SSB_API int ssb_program_specialise_check(const ssb_program* program, 
     *shapes = static_cast<uint32_t>(h.shapes.size());
     std::string log;
     if (!ssb::specialise_compile_check(h, &log)) throw ssb::CudaError("shape specialisation failed: " + log);
+  });
+}
+
+extern "C" SSB_API int ssb_program_fused_info(const ssb_program* program, uint32_t tile_qubits, ssb_fused_info* out) {
+  return ssb::guard([&] {
+    if (!program || !out) throw std::invalid_argument("null argument");
+    const ssb::FusedPlan f = ssb::plan_fused(program->dev, tile_qubits ? std::max(8u, std::min(13u, tile_qubits)) : 12u);
+    *out = ssb_fused_info{};
+    out->ok = f.ok;
+    out->passes = static_cast<uint32_t>(f.passes.size());
+    out->blocks = f.num_blocks;
+    out->groups = static_cast<uint32_t>(f.groups.size());
+    out->max_pass_blocks = f.max_pass_blocks;
+    out->err_bound = f.err_bound;
   });
 }

@@ -221,7 +221,7 @@ __global__ void b_leaf_cum_full(ProgView P, const double2* pool, const DevNode* 
   double* out = cum + l * count;
   const bool ident = P.sample_identity;
   const ExactPick r = warp_exact_scan(
-      [&](uint64_t m) { return c_norm(a[ident ? m : scatter_bits(m, P.sample_qubits, P.nsample)]); }, count, -1.0,
+      [&](uint64_t m) { return c_norm(a[ident ? m : scatter_bits(m, P.sample_qubits, P.nsample)]); }, count, HUGE_VAL,
       [&](uint64_t m, double v) { out[m] = v; });
   if ((threadIdx.x & 31) == 0) last[l] = r.any_nonzero ? r.outcome : count;
 }
@@ -232,7 +232,7 @@ __global__ void b_leaf_cum_probs(const double* probs, uint64_t nl, uint64_t coun
   if (l >= nl) return;
   const double* pr = probs + l * count;
   double* out = cum + l * count;
-  const ExactPick r = warp_exact_scan([&](uint64_t m) { return pr[m]; }, count, -1.0,
+  const ExactPick r = warp_exact_scan([&](uint64_t m) { return pr[m]; }, count, HUGE_VAL,
                                       [&](uint64_t m, double v) { out[m] = v; });
   if ((threadIdx.x & 31) == 0) last[l] = r.any_nonzero ? r.outcome : count;
 }

@@ -146,4 +146,39 @@ struct Step {
   uint32_t index;      // pass index, or op index for S_SPECIAL
 };
 
+// ---- Fused-matrix mode (ssb_run_options::fused_matrices; fused.cpp) -------
+// Runs of gates + Pauli sites on at most two qubits are multiplied into one
+// 4x4 "block" per shot; a shot that drew non-identity Pauli terms inside a
+// block applies Q_L ... Q_1 M instead of M, with Q_j = V_j P_t V_j^dagger
+// (V_j: the block's gates after site j), all precomputed on the host.
+struct FPass {
+  uint32_t grp_begin, grp_end;     // register groups of this pass (application order)
+  uint32_t blk_begin, blk_end;     // their blocks (group order)
+  uint32_t lmask;                  // local qubit set (k qubits, low 3 included)
+  uint8_t k, first;                // first: synthesise |0...0> instead of loading
+  uint8_t pad[2];
+  uint8_t lq[32];                  // local position -> qubit
+};
+
+// A register group: consecutive blocks of a pass whose qubits lie in four
+// local positions; each thread holds the group's 16 amplitudes of one "hexad"
+// in registers while every block of the group is applied.
+struct FGroup {
+  uint8_t g[4];                    // local positions, ascending (group bit i <-> g[i])
+  uint32_t blk_begin, blk_end;
+};
+
+struct FBlock {
+  uint8_t p0, p1;                  // local positions of matrix bit 0 / bit 1
+  uint8_t gb0, gb1;                // their group bits
+  uint32_t mat;                    // base matrix (16 double2, row-major 4x4)
+  uint32_t site_begin, site_end;   // its Pauli sites (FSite range)
+};
+
+struct FSite {
+  uint32_t site;                   // Pauli-site ordinal (decision table column)
+  uint32_t qbase;                  // qidx[qbase + term]: Q matrix, or kNoQ (identity term)
+};
+constexpr uint32_t kNoQ = 0xFFFFFFFFu;
+
 }  // namespace ssb

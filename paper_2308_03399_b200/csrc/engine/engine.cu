@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../capi_internal.hpp"
+#include "fused.cuh"
 #include "kernels.cuh"
 
 namespace ssb {
@@ -45,6 +46,11 @@ struct DevProgram {
   bool trunk_ok = false;
   uint16_t* site_pass = nullptr;
   uint8_t* ident_row = nullptr;
+  // Fused-matrix plan (fused.cpp), built on first use of fused_matrices.
+  bool fused_tried = false;
+  FusedPlan fplan;
+  FusedView fview{};
+  size_t fsmem = 0;
   ~DevProgram() {
     for (void* p : allocs) cudaFree(p);
   }
@@ -449,7 +455,16 @@ void kraus_decide_wave(ssb_engine* E, DevProgram& dp, uint32_t op_index, const S
   }
 }
 
-void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c) {
+// Guard band of the fused-matrix mode (sample_exact_kernel): shots whose
+// draw lies within the rounding bound of a cumulative boundary are listed.
+struct SampleGuard {
+  double err = 0.0;              // bound on ||psi_fused - psi_reference||_2; 0: exact run
+  unsigned* count = nullptr;     // device counter
+  uint64_t* ids = nullptr;       // device list (shot ids), capacity cap
+  uint64_t cap = 0;
+};
+
+void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c, const SampleGuard& g = SampleGuard{}) {
   const unsigned n = dp.host.n;
   const ProgView& P = dp.view;
   if (P.nsample == n && n >= 12) {
@@ -457,11 +472,13 @@ void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c) {
     for (uint64_t off = 0; off < c.S; off += (1u << 30)) {
       const SegCtx cc = c.sub(off, std::min<uint64_t>(1u << 30, c.S - off), n);
       sample_exact_kernel<<<static_cast<unsigned>(cc.S), SAMPLE_NT, 0, E->stream>>>(
-          P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs, E->serial_chunks, E->err, sample_force_serial());
+          P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs, E->serial_chunks, E->err, sample_force_serial(),
+          g.err, g.count, g.ids, g.cap);
       launched(E);
     }
     return;
   }
+  if (g.err > 0.0) throw std::logic_error("fused_matrices needs the full-register sampler");
   if (P.nsample == n) {
     g_sample_scan_kernel<<<grid_for(c.S, 128), 128, 0, E->stream>>>(P, c.state, c.S, c.seed, c.ids, c.begin, c.cregs,
                                                                     E->err);
@@ -600,6 +617,118 @@ void run_batch_checked(ssb_engine* E, const ssb_program* prog, uint64_t shot_beg
   }
 }
 
+void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begin, uint64_t count, uint64_t seed,
+                      const ssb_run_options* opts, uint64_t* values_dev, ssb_stats* stats);
+
+// Fused-matrix plan of a streamed program (fused.cpp), uploaded once.
+bool fused_ready(ssb_engine* E, DevProgram& dp) {
+  if (dp.fused_tried) return dp.fplan.ok;
+  dp.fused_tried = true;
+  FusedPlan& f = dp.fplan;
+  f = plan_fused(dp.host, dp.host.tile_k);
+  if (f.ok && f.k < 8) {
+    f.ok = false;
+    f.why = "tile smaller than 8 qubits";
+  }
+  if (f.ok && dp.host.eligible && dp.host.n < 12) {
+    f.ok = false;
+    f.why = "fewer than 12 qubits (terminal sampler)";
+  }
+  if (!f.ok) return false;
+  dp.fsmem = fused_smem_bytes(f.k, std::max(1u, f.max_pass_blocks), std::max(1u, f.max_pass_sites));
+  if (dp.fsmem > E->smem_optin) {
+    f.ok = false;
+    f.why = "pass staging exceeds shared memory";
+    return false;
+  }
+  FusedView& v = dp.fview;
+  v.passes = upload(dp, f.passes);
+  v.groups = upload(dp, f.groups);
+  v.blocks = upload(dp, f.blocks);
+  v.sites = upload(dp, f.sites);
+  v.qidx = upload(dp, f.qidx);
+  v.mats = reinterpret_cast<const double2*>(upload(dp, f.mats));
+  v.n = dp.host.n;
+  return true;
+}
+
+// Test hook: SHOTSIM_B200_GUARD_SCALE=x widens the guard band x-fold (forces
+// exact replays so their path is exercised).
+double guard_scale() {
+  const char* v = std::getenv("SHOTSIM_B200_GUARD_SCALE");
+  return v && *v ? std::max(1.0, std::strtod(v, nullptr)) : 1.0;
+}
+
+// gpu-batch in fused-matrix mode (fused.cuh): per wave the Pauli decisions,
+// one fused_pass_kernel per planned pass and the guarded exact sampler; then
+// every flagged shot is re-run through the exact executor into its slot.
+void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t shot_begin, uint64_t count,
+               uint64_t seed, const ssb_run_options* opts, uint64_t* values_dev, ssb_stats* stats, KernelTimer& timer) {
+  const FusedPlan& f = dp.fplan;
+  const unsigned n = dp.host.n;
+  const uint64_t seg = (uint64_t{1} << n) * sizeof(double2);
+  const uint64_t tiles = uint64_t{1} << (n - f.k);
+  uint64_t wave = wave_for(opts, count, seg, mem_limit(opts));
+  wave = std::min<uint64_t>(wave, std::max<uint64_t>(1, (uint64_t{1} << 31) / tiles - 1));
+  double2* state = static_cast<double2*>(scratch(E, "state", wave * seg));
+  uint8_t* psel = dp.num_pauli ? static_cast<uint8_t*>(scratch(E, "psel", wave * dp.num_pauli)) : nullptr;
+  unsigned* gcount = static_cast<unsigned*>(scratch(E, "guard_count", sizeof(unsigned)));
+  uint64_t* gids = static_cast<uint64_t*>(scratch(E, "guard_ids", count * sizeof(uint64_t)));
+  CK(cudaMemsetAsync(gcount, 0, sizeof(unsigned), E->stream));
+  const SampleGuard guard{f.err_bound * guard_scale(), gcount, gids, count};
+  CK(cudaFuncSetAttribute(fused_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dp.fsmem)));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_pass_kernel, NT, dp.fsmem));
+  uint64_t waves = 0;
+  for (uint64_t w0 = 0; w0 < count; w0 += wave, ++waves) {
+    const uint64_t S = std::min(wave, count - w0);
+    const SegCtx c{state, S, seed, nullptr, shot_begin + w0, nullptr, values_dev + w0};
+    CK(cudaMemsetAsync(c.cregs, 0, S * sizeof(uint64_t), E->stream));
+    if (dp.num_pauli) {
+      pauli_decide_kernel<<<grid_for(S * dp.num_pauli), NT, 0, E->stream>>>(dp.view, dp.pauli_site_ops, dp.num_pauli,
+                                                                           seed, nullptr, c.begin, S, psel);
+      launched(E);
+    }
+    const unsigned grid =
+        static_cast<unsigned>(std::min<uint64_t>(S * tiles, uint64_t(std::max(per_sm, 1)) * E->num_sms));
+    for (uint32_t p = 0; p < f.passes.size(); ++p) {
+      timer.begin(0);
+      fused_pass_kernel<<<grid, NT, dp.fsmem, E->stream>>>(dp.fview, p, state, S, psel, dp.num_pauli,
+                                                          std::max(1u, f.max_pass_blocks),
+                                                          std::max(1u, f.max_pass_sites));
+      launched(E);
+      timer.end(0);
+    }
+    export_states(E, opts, state, w0, S, n);
+    if (dp.host.eligible) {
+      timer.begin(2);
+      sample_terminal(E, dp, c, guard);
+      timer.end(2);
+    }
+  }
+  unsigned flagged = 0;
+  CK(cudaMemcpyAsync(&flagged, gcount, sizeof flagged, cudaMemcpyDeviceToHost, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  if (flagged) {  // exact replays (the reference's arithmetic) of the guarded shots
+    std::vector<uint64_t> ids(std::min<uint64_t>(flagged, count));
+    CK(cudaMemcpy(ids.data(), gids, ids.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    ssb_run_options exact = opts ? *opts : ssb_run_options{};
+    exact.fused_matrices = 0;
+    exact.states_out = nullptr;
+    exact.profile = 0;
+    exact.max_batch_size = 0;
+    for (uint64_t id : ids) run_batch_device(E, prog, id, 1, seed, &exact, values_dev + (id - shot_begin), nullptr);
+  }
+  if (stats) {
+    stats->peak_states = wave;
+    stats->passes = waves;
+    stats->fused_passes = f.passes.size();
+    stats->fused_blocks = f.num_blocks;
+    stats->guard_flagged = flagged;
+    stats->guard_delta = 2.02 * guard.err + (2.0 * double(uint64_t{1} << n) + 16.0) * 0x1p-53;
+  }
+}
+
 // gpu-batch over shot ids [shot_begin, shot_begin+count) (or explicit ids).
 void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begin, uint64_t count, uint64_t seed,
                       const ssb_run_options* opts, uint64_t* values_dev, ssb_stats* stats) {
@@ -607,7 +736,6 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
   const RunConfig rc = config_of(opts);
   const unsigned n = prog->dev.n;
   const uint64_t launches0 = E->launches;
-  CK(cudaMemsetAsync(E->serial_chunks, 0, sizeof(unsigned long long), E->stream));
   if (opts && opts->check_norms) {
     run_batch_checked(E, prog, shot_begin, count, seed, opts, values_dev, stats);
     if (stats) stats->dispatch_count = E->launches - launches0;
@@ -653,6 +781,18 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
     }
   } else {
     DevProgram& dp = device_program(E, prog, rc.tile_k);
+    if (opts && opts->fused_matrices && fused_ready(E, dp)) {
+      run_fused(E, prog, dp, shot_begin, count, seed, opts, values_dev, stats, timer);
+      if (stats) {
+        stats->dispatch_count = E->launches - launches0;
+        unsigned long long hits = 0;
+        CK(cudaMemcpyAsync(&hits, E->serial_chunks, sizeof hits, cudaMemcpyDeviceToHost, E->stream));
+        CK(cudaStreamSynchronize(E->stream));
+        stats->sampling_serial_chunks = hits;
+      }
+      timer.collect(stats);
+      return;
+    }
     const HostDevProgram& h = dp.host;
     const uint64_t seg = (uint64_t{1} << n) * sizeof(double2);
     const uint64_t limit = mem_limit(opts);
@@ -927,6 +1067,7 @@ SSB_API int ssb_run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_
   return guard([&] {
     if (!E || !prog || !values_out_device) throw std::invalid_argument("null argument");
     DeviceGuard g(E->device);
+    CK(cudaMemsetAsync(E->serial_chunks, 0, sizeof(unsigned long long), E->stream));
     run_batch_device(E, prog, shot_begin, shot_count, seed, options, values_out_device, stats);
   });
 }
@@ -939,6 +1080,7 @@ SSB_API int ssb_run_batch(ssb_engine* E, const ssb_program* prog, uint64_t shot_
     DeviceGuard g(E->device);
     const auto t0 = std::chrono::steady_clock::now();
     uint64_t* dv = static_cast<uint64_t*>(scratch(E, "values", shot_count * sizeof(uint64_t)));
+    CK(cudaMemsetAsync(E->serial_chunks, 0, sizeof(unsigned long long), E->stream));
     CK(cudaEventRecord(E->ev0, E->stream));
     run_batch_device(E, prog, shot_begin, shot_count, seed, options, dv, stats);
     CK(cudaMemcpyAsync(values_out, dv, shot_count * sizeof(uint64_t), cudaMemcpyDeviceToHost, E->stream));

@@ -30,11 +30,10 @@ struct ExactPick {
 // All 32 lanes of a warp call this with the same arguments. prob(m) returns
 // p_m (m < count); on_sum(m, S_m), when not null-like, receives every running
 // sum in order of m (only called by the lane owning m; used to build a
-// leaf's cumulative table). u < 0 scans the whole range (no early exit).
+// leaf's cumulative table). u = +inf scans the whole range (no early exit).
 template <class Prob, class OnSum>
 __device__ __forceinline__ ExactPick warp_exact_scan(Prob prob, uint64_t count, double u, OnSum on_sum) {
   const unsigned lane = threadIdx.x & 31;
-  const unsigned below = (1u << lane) - 1;
   double S = 0.0;
   long long last_nz = -1;
   ExactPick r{0, 0.0, 0.0, false, false};

@@ -1,0 +1,306 @@
+// Fused-matrix planner (fused.hpp): blocks, their products and folded Pauli
+// factors, the HBM tile-pass schedule over the block DAG and the rounding
+// bound behind the sampler's guard band.
+#include "fused.hpp"
+
+#include <algorithm>
+#include <array>
+#include <bit>
+#include <cmath>
+#include <complex>
+#include <limits>
+
+namespace ssb {
+
+namespace {
+
+using cld = std::complex<long double>;
+using M4 = std::array<cld, 16>;  // row-major: (r, c) at r * 4 + c
+
+M4 eye4() {
+  M4 m{};
+  for (int i = 0; i < 4; ++i) m[i * 5] = 1.0L;
+  return m;
+}
+
+M4 mul(const M4& a, const M4& b) {
+  M4 c{};
+  for (int r = 0; r < 4; ++r)
+    for (int col = 0; col < 4; ++col) {
+      cld s = 0.0L;
+      for (int k = 0; k < 4; ++k) s += a[r * 4 + k] * b[k * 4 + col];
+      c[r * 4 + col] = s;
+    }
+  return c;
+}
+
+M4 dagger(const M4& a) {
+  M4 c{};
+  for (int r = 0; r < 4; ++r)
+    for (int col = 0; col < 4; ++col) c[r * 4 + col] = std::conj(a[col * 4 + r]);
+  return c;
+}
+
+struct Elem {
+  bool pauli;
+  uint32_t op;
+};
+
+struct Blk {
+  unsigned q0, q1;  // matrix bit 0 / bit 1 qubits (q0 < q1)
+  std::vector<Elem> elems;
+};
+
+// Block-basis bit of qubit q.
+unsigned bit_of(const Blk& b, unsigned q) { return q == b.q0 ? 0u : 1u; }
+
+// Gate op embedded in the block basis (program.hpp: qubits[0] = low matrix axis).
+M4 embed_gate(const HostDevProgram& h, const DevOp& o, const Blk& b) {
+  const double* g = &h.mats[size_t{o.aux} * 32];
+  const unsigned d = 1u << o.nq;
+  auto G = [&](unsigned r, unsigned c) { return cld(g[2 * (r * d + c)], g[2 * (r * d + c) + 1]); };
+  auto gidx = [&](unsigned r) {
+    unsigned x = 0;
+    for (unsigned j = 0; j < o.nq; ++j) x |= ((r >> bit_of(b, o.q[j])) & 1u) << j;
+    return x;
+  };
+  // Block bits not touched by the gate must match between row and column.
+  unsigned touched = 0;
+  for (unsigned j = 0; j < o.nq; ++j) touched |= 1u << bit_of(b, o.q[j]);
+  M4 m{};
+  for (unsigned r = 0; r < 4; ++r)
+    for (unsigned c = 0; c < 4; ++c)
+      if (((r ^ c) & ~touched & 3u) == 0) m[r * 4 + c] = G(gidx(r), gidx(c));
+  return m;
+}
+
+// Pauli term (destination-sign form, kernels_scalar.cpp:58-81):
+// new[i] = (-i)^num_y (-1)^popcount(i & z) old[i ^ x], restricted to the block.
+M4 embed_pauli(const DevTerm& t, const Blk& b) {
+  unsigned xb = 0, zb = 0;
+  for (unsigned q : {b.q0, b.q1}) {
+    xb |= ((t.x >> q) & 1u) << bit_of(b, q);
+    zb |= ((t.z >> q) & 1u) << bit_of(b, q);
+  }
+  static const cld phase[4] = {cld(1, 0), cld(0, -1), cld(-1, 0), cld(0, 1)};
+  const cld ph = phase[t.num_y & 3u];
+  M4 m{};
+  for (unsigned r = 0; r < 4; ++r) m[r * 4 + (r ^ xb)] = (std::popcount(r & zb) & 1) ? -ph : ph;
+  return m;
+}
+
+uint32_t push(FusedPlan& f, const M4& m) {
+  const uint32_t idx = static_cast<uint32_t>(f.mats.size() / 32);
+  for (const cld& e : m) {
+    f.mats.push_back(static_cast<double>(e.real()));
+    f.mats.push_back(static_cast<double>(e.imag()));
+  }
+  return idx;
+}
+
+}  // namespace
+
+FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
+  FusedPlan f;
+  const unsigned n = h.n;
+  if (n < 3) {
+    f.why = "fewer than 3 qubits";
+    return f;
+  }
+  if (h.eligible && h.sample_qubits.size() != n) {
+    f.why = "terminal sampling over a subset of the qubits";
+    return f;
+  }
+  for (uint32_t i = 0; i < h.end; ++i) {
+    const DevOp& o = h.ops[i];
+    const bool ok = o.kind == K_BARRIER || ((o.kind == K_GATE || o.kind == K_PAULI) && !o.has_cond && o.nq <= 2);
+    if (!ok) {
+      f.why = "op " + std::to_string(i) + " is not an unconditioned gate / Pauli site on <= 2 qubits";
+      return f;
+    }
+  }
+
+  // ---- blocks (greedy: an op joins the last block on its qubits when that
+  // block is the last one touching each of them; 1q ops wait for the next 2q
+  // block on their qubit) ----
+  std::vector<Blk> blks;
+  std::vector<int> frontier(n, -1);
+  std::vector<std::vector<Elem>> pending(n);
+  uint64_t exact_gates = 0;
+  for (uint32_t i = 0; i < h.end; ++i) {
+    const DevOp& o = h.ops[i];
+    if (o.kind == K_BARRIER) continue;
+    if (o.kind == K_GATE) {
+      if (o.skip) continue;  // exact identity: no factor
+      ++exact_gates;
+    }
+    const Elem e{o.kind == K_PAULI, i};
+    if (o.nq == 1) {
+      const unsigned q = o.q[0];
+      if (frontier[q] >= 0) blks[frontier[q]].elems.push_back(e);
+      else pending[q].push_back(e);
+      continue;
+    }
+    const unsigned a = o.q[0], c = o.q[1];
+    if (frontier[a] >= 0 && frontier[a] == frontier[c]) {
+      blks[frontier[a]].elems.push_back(e);
+      continue;
+    }
+    Blk b{std::min(a, c), std::max(a, c), {}};
+    for (unsigned q : {a, c}) {
+      b.elems.insert(b.elems.end(), pending[q].begin(), pending[q].end());
+      pending[q].clear();
+    }
+    b.elems.push_back(e);
+    frontier[a] = frontier[c] = static_cast<int>(blks.size());
+    blks.push_back(std::move(b));
+  }
+  for (unsigned q = 0; q < n; ++q)
+    if (!pending[q].empty()) {  // a qubit no 2q op ever touches: I (x) G on a partner
+      const unsigned partner = q == 0 ? 1 : 0;
+      Blk b{std::min(q, partner), std::max(q, partner), std::move(pending[q])};
+      blks.push_back(std::move(b));
+    }
+
+  // ---- products, folded Pauli factors ----
+  std::vector<uint32_t> base(blks.size());
+  std::vector<std::pair<uint32_t, uint32_t>> site_range(blks.size());
+  double work = 16.0 * static_cast<double>(exact_gates);  // reference's own rounding
+  for (size_t bi = 0; bi < blks.size(); ++bi) {
+    const Blk& b = blks[bi];
+    // suffix[j] = product of the gates after element j (V_j), built backwards.
+    std::vector<M4> after(b.elems.size());
+    M4 acc = eye4();
+    for (size_t j = b.elems.size(); j-- > 0;) {
+      after[j] = acc;
+      const Elem& e = b.elems[j];
+      if (!e.pauli) acc = mul(acc, embed_gate(h, h.ops[e.op], b));
+    }
+    base[bi] = push(f, acc);  // acc = G_k ... G_1
+    site_range[bi].first = static_cast<uint32_t>(f.sites.size());
+    for (size_t j = 0; j < b.elems.size(); ++j) {
+      const Elem& e = b.elems[j];
+      if (!e.pauli) continue;
+      const DevOp& o = h.ops[e.op];
+      FSite s{o.site, static_cast<uint32_t>(f.qidx.size())};
+      const M4 vd = dagger(after[j]);
+      for (uint32_t t = 0; t < o.count; ++t) {
+        const DevTerm& term = h.terms[o.aux + t];
+        f.qidx.push_back(term.identity ? kNoQ : push(f, mul(mul(after[j], embed_pauli(term, b)), vd)));
+      }
+      f.sites.push_back(s);
+    }
+    site_range[bi].second = static_cast<uint32_t>(f.sites.size());
+    // fused rounding: the product's representation + the apply, and per
+    // drawn site one more factor (product or extra apply)
+    work += 16.0 + 16.0 * (site_range[bi].second - site_range[bi].first);
+  }
+  // Margin x4 over the per-operation constants (complex 2x2 / 4x4 products
+  // with and without FMA stay below 16 unit roundoffs of the state norm).
+  f.err_bound = 4.0 * work * std::ldexp(1.0, -53);
+
+  // ---- HBM tile passes over the block DAG ----
+  const unsigned k = std::min(tile_k, n);
+  f.k = k;
+  const uint32_t low = (1u << std::min(3u, k - 2)) - 1;
+  const uint32_t all = n >= 32 ? ~0u : (1u << n) - 1;
+  std::vector<uint32_t> remaining(blks.size());
+  for (uint32_t i = 0; i < remaining.size(); ++i) remaining[i] = i;
+  bool first = true;
+  while (first || !remaining.empty()) {
+    uint32_t L = low, blocked = 0;
+    std::vector<uint32_t> taken, rest;
+    for (size_t r = 0; r < remaining.size(); ++r) {
+      const uint32_t b = remaining[r];
+      const uint32_t qm = (1u << blks[b].q0) | (1u << blks[b].q1);
+      if (!(qm & blocked) && static_cast<unsigned>(std::popcount(L | qm)) <= k && taken.size() < kFusedMaxPassBlocks) {
+        L |= qm;
+        taken.push_back(b);
+      } else {
+        blocked |= qm;
+        rest.push_back(b);
+      }
+      if (blocked == all) {
+        rest.insert(rest.end(), remaining.begin() + static_cast<long>(r) + 1, remaining.end());
+        break;
+      }
+    }
+    remaining.swap(rest);
+    for (unsigned q = 0; q < n && static_cast<unsigned>(std::popcount(L)) < k; ++q) L |= 1u << q;
+    FPass pd{};
+    pd.lmask = L;
+    pd.k = static_cast<uint8_t>(k);
+    pd.first = first;
+    first = false;
+    uint8_t pos[32] = {};
+    for (unsigned q = 0, j = 0; q < n; ++q)
+      if (L >> q & 1) {
+        pd.lq[j] = static_cast<uint8_t>(q);
+        pos[q] = static_cast<uint8_t>(j++);
+      }
+    // Register groups: repeatedly open a group with the first block whose
+    // predecessors in the pass are applied, then add every ready block whose
+    // qubits keep the group within four local positions (blocks sharing a
+    // qubit keep their order; disjoint ones commute).
+    pd.grp_begin = static_cast<uint32_t>(f.groups.size());
+    pd.blk_begin = static_cast<uint32_t>(f.blocks.size());
+    std::vector<char> placed(taken.size(), 0);
+    size_t nplaced = 0;
+    uint32_t sites_in_pass = 0;
+    while (nplaced < taken.size()) {
+      uint32_t gm = 0;  // group qubit mask
+      FGroup g{};
+      g.blk_begin = static_cast<uint32_t>(f.blocks.size());
+      bool grew = true;
+      while (grew) {
+        grew = false;
+        uint32_t pending_q = 0;  // qubits of earlier unplaced blocks (order constraint)
+        for (size_t t = 0; t < taken.size(); ++t) {
+          if (placed[t]) continue;
+          const uint32_t b = taken[t];
+          const uint32_t qm = (1u << blks[b].q0) | (1u << blks[b].q1);
+          if (!(qm & pending_q) && std::popcount(gm | qm) <= 4) {
+            gm |= qm;
+            placed[t] = 1;
+            ++nplaced;
+            grew = true;
+            FBlock fb{};
+            fb.p0 = pos[blks[b].q0];
+            fb.p1 = pos[blks[b].q1];
+            fb.mat = base[b];
+            fb.site_begin = site_range[b].first;
+            fb.site_end = site_range[b].second;
+            sites_in_pass += fb.site_end - fb.site_begin;
+            f.blocks.push_back(fb);
+          } else {
+            pending_q |= qm;
+          }
+        }
+      }
+      // Pad to four local positions (any unused ones) and assign group bits.
+      uint32_t lm = 0;
+      for (unsigned q = 0; q < n; ++q)
+        if (gm >> q & 1) lm |= 1u << pos[q];
+      for (unsigned j = 0; j < k && std::popcount(lm) < 4; ++j) lm |= 1u << j;
+      for (unsigned j = 0, i = 0; j < k; ++j)
+        if (lm >> j & 1) g.g[i++] = static_cast<uint8_t>(j);
+      g.blk_end = static_cast<uint32_t>(f.blocks.size());
+      for (uint32_t b = g.blk_begin; b < g.blk_end; ++b)
+        for (uint8_t i = 0; i < 4; ++i) {
+          if (g.g[i] == f.blocks[b].p0) f.blocks[b].gb0 = i;
+          if (g.g[i] == f.blocks[b].p1) f.blocks[b].gb1 = i;
+        }
+      f.groups.push_back(g);
+    }
+    pd.grp_end = static_cast<uint32_t>(f.groups.size());
+    pd.blk_end = static_cast<uint32_t>(f.blocks.size());
+    f.max_pass_blocks = std::max<uint32_t>(f.max_pass_blocks, pd.blk_end - pd.blk_begin);
+    f.max_pass_sites = std::max<uint32_t>(f.max_pass_sites, sites_in_pass);
+    f.passes.push_back(pd);
+  }
+  f.num_blocks = static_cast<uint32_t>(blks.size());
+  f.ok = true;
+  return f;
+}
+
+}  // namespace ssb

@@ -1013,7 +1013,9 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
                                                                         uint64_t seed, const uint64_t* ids,
                                                                         uint64_t begin, uint64_t* cregs,
                                                                         unsigned long long* serial_chunks, int* err,
-                                                                        int force_serial) {
+                                                                        int force_serial, double guard_err,
+                                                                        unsigned* guard_count, uint64_t* guard_ids,
+                                                                        uint64_t guard_cap) {
   __shared__ double pbuf[SAMPLE_CHUNK];
   __shared__ long long wsum[SAMPLE_NT / 32];
   __shared__ int wflag[SAMPLE_NT / 32];
@@ -1021,6 +1023,7 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
   __shared__ int decided;
   __shared__ uint64_t outcome;
   __shared__ double Ssh;
+  __shared__ double s_prev, s_at;  // boundaries of the decision (guard band)
   const uint64_t s = blockIdx.x;
   if (s >= S) return;
   const unsigned n = P.n, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1092,10 +1095,13 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
         double Sx = Scur;
         const uint32_t cnt = A - c0 < SAMPLE_CHUNK ? static_cast<uint32_t>(A - c0) : SAMPLE_CHUNK;
         for (uint32_t j = 0; j < cnt; ++j) {
+          const double Sp = Sx;
           Sx = __dadd_rn(Sx, pbuf[j]);
           if (u < Sx) {
             outcome = c0 + j;
             decided = 1;
+            s_prev = Sp;
+            s_at = Sx;
             break;
           }
         }
@@ -1118,7 +1124,21 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) cregs[s] = apply_sample_outcome(P, cregs[s], outcome);
+  if (threadIdx.x == 0) {
+    cregs[s] = apply_sample_outcome(P, cregs[s], outcome);
+    if (guard_err > 0.0) {
+      // Fused-matrix amplitudes: |S'_m - S_m| <= 2 err (sum of |p' - p|) + the
+      // two sequential sums' rounding ((m + 1) u each) + p's own rounding.
+      // A draw outside [S'_{m-1} + D, S'_m - D] decides the reference's m too;
+      // inside it (or on the no-crossing fallback) the shot is replayed exactly.
+      const double D = 2.02 * guard_err + (2.0 * static_cast<double>(outcome) + 16.0) * 0x1p-53;
+      const bool flag = !decided || !(u - s_prev >= D) || !(s_at - u > D);
+      if (flag) {
+        const unsigned i = atomicAdd(guard_count, 1u);
+        if (i < guard_cap) guard_ids[i] = shot_of(ids, begin, s);
+      }
+    }
+  }
 }
 
 // Terminal sampling over k < n qubits: pick over precomputed probabilities.

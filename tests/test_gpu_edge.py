@@ -18,44 +18,48 @@ from paper_2308_03399_b200._lib import DegenerateDistribution, ShotsimError
 
 pytestmark = pytest.mark.gpu
 
-MEAS2 = "qubits 2\nclbits 2\nx q0\nmeasure q0,q1 -> c0,c1\n"
+MEAS1 = "qubits 1\nclbits 1\nx q0\nmeasure q0 -> c0\n"
 
 
 def _measure_with(engine, amps, u):
-    """One 2-qubit measure op applied with draw u to a segment set to amps."""
-    prog = Program.from_text(MEAS2)
-    ops = prog.ops()
-    mi = next(i for i, o in enumerate(ops) if o.kind == 3)
+    """The measure op (1 qubit, the reference's only measure arity) applied
+    with draw u to a segment set to amps (possibly unnormalised)."""
+    prog = Program.from_text(MEAS1)
+    mi = next(i for i, o in enumerate(prog.ops()) if o.kind == 3)
     b = BatchState(engine, prog, [0], 0)
     b.write_segment(0, np.asarray(amps, dtype=np.complex128))
     b.apply_op(mi, [u])
     return int(b.cregs()[0]), b.segments()[0]
 
 
-# probabilities {0.25, 0, 0.5, 0.25}: |0.5|^2, 0, |0.5+0.5i|^2, |0.5|^2 (all exact)
-TABLE = [0.5, 0.0, 0.5 + 0.5j, 0.5]
-
-
-@pytest.mark.parametrize("u,want", [(0.0, 0), (0.25, 2), (0.2499, 0), (0.999999, 3)])
-def test_pick_outcome_strictness(engine, u, want):
-    m, seg = _measure_with(engine, TABLE, u)
+# test_statevector.cpp:210-221 restated over the two outcomes of a 1-qubit
+# measure (p_0 = |0.5|^2 = 0.25 exactly).
+@pytest.mark.parametrize("amps,u,want", [
+    ([0.5, 0.75 ** 0.5], 0.0, 0),            # u = 0 picks the first nonzero outcome
+    ([0.5, 0.75 ** 0.5], 0.25, 1),           # strict: u == cum moves on
+    ([0.5, 0.75 ** 0.5], 0.2499, 0),
+    ([0.0, 1.0], 0.0, 1),                    # zero-probability outcome unreachable
+    ([0.5 + 0.5j, 0.5 + 0.5j], 0.999999, 1),
+])
+def test_pick_outcome_strictness(engine, amps, u, want):
+    m, seg = _measure_with(engine, amps, u)
     assert m == want
     assert np.count_nonzero(seg) == 1 and abs(abs(seg[want]) - 1.0) < 1e-15
 
 
 def test_pick_outcome_slack_fallback(engine):
     """Probabilities sum below 1 and u lies above the sum: the last outcome with
-    p > 0 (pick_outcome fallback; the batch measure's slack dispatch)."""
-    amps = [0.5, 0.5, np.sqrt(0.4999999), 0.0]
-    m, seg = _measure_with(engine, amps, 0.9999999999)
-    assert m == 2
-    m, _ = _measure_with(engine, [np.sqrt(0.5), np.sqrt(0.4999999), 0.0, 0.0], 0.99999999999)
-    assert m == 1  # skips the zero tail
+    p > 0 (pick_outcome fallback; the batch measure's slack dispatch,
+    exec_batch.cpp:169-182)."""
+    m, seg = _measure_with(engine, [0.5, np.sqrt(0.4999999)], 0.9999999999)
+    assert m == 1
+    m, _ = _measure_with(engine, [np.sqrt(0.4999999), 0.0], 0.99999999999)
+    assert m == 0  # skips the zero tail
 
 
 def test_measure_degenerate(engine):
     with pytest.raises(DegenerateDistribution):
-        _measure_with(engine, [0.0, 0.0, 0.0, 0.0], 0.5)
+        _measure_with(engine, [0.0, 0.0], 0.5)
 
 
 def test_terminal_sampling_degenerate(engine):

@@ -78,3 +78,21 @@ def test_fused_states_within_bound(engine, ref, n):
     assert r.fused_blocks > 0
     errs = [rel_err(g, w) for g, w in zip(r.states, want)]
     assert max(errs) <= 1e-10, errs
+
+
+@pytest.mark.parametrize("scale", ["1", "1e5"])
+def test_fused_counts_equal_exact(engine, oracle, monkeypatch, scale):
+    """fused_matrices gives the exact executor's (= the reference's) per-shot
+    values. With the guard band widened 1e5-fold (test hook) a large share of
+    shots falls inside it and is replayed through the exact executor — the
+    replay path must give the same values."""
+    monkeypatch.setenv("SHOTSIM_B200_GUARD_SCALE", scale)
+    prog = Program.from_text(cc.quantum_volume(14, depth=8, seed=3), cc.qv_noise())
+    want = oracle.run_shots(prog, np.arange(400), 19, threads=8)
+    r = engine.run_batch(prog, RunOptions(shots=400, seed=19, fused_matrices=True, record_shot_values=True))
+    assert r.fused_blocks > 0
+    assert (np.asarray(r.shot_values) == want).all()
+    if scale != "1":
+        assert 0 < r.guard_flagged < 400
+    else:
+        assert r.guard_flagged <= 2
