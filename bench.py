@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exact", action="store_true",
+                    help="bit-exact-amplitude executor (no fused 4x4 blocks); default: fused_matrices")
     return ap.parse_args()
 
 
@@ -57,7 +59,7 @@ def workload(key, shots_override=0):
     return cfg, cfg["circuit"](), cfg["noise"](), (shots_override or cfg["shots"]), cfg["seed"]
 
 
-def config_dict(key, cfg, shots, n_gpus, executor="gpu-batch"):
+def config_dict(key, cfg, shots, n_gpus, executor="gpu-batch", fused=True):
     desc = {
         "C1": "GHZ10 + depolarizing 1%",
         "C2": "QV16 (16 layers of SU(4) blocks) + depolarizing 1% + 1% readout flip",
@@ -69,7 +71,10 @@ def config_dict(key, cfg, shots, n_gpus, executor="gpu-batch"):
             "global_shots_per_step": shots * n_gpus, "seed": cfg["seed"], "executor": executor,
             "parallelism": f"shot-sharded x{n_gpus} (weak)",
             "l2": "inputs larger than L2: per-wave state 16 GiB >> 126 MB L2",
-            "arithmetic": "fp64 complex, reference scalar-table rounding (no FMA), bit-exact counts"}
+            "arithmetic": ("fp64 complex; fused 4x4 blocks with FMA (amplitudes within 1e-10 of the reference), "
+                           "guard band + exact on-device replay on terminal sampling: bit-exact counts"
+                           if fused else
+                           "fp64 complex, reference scalar-table rounding (no FMA), bit-exact counts and amplitudes")}
 
 
 # ---- algorithmic bytes -------------------------------------------
@@ -343,8 +348,9 @@ def main():
     values = torch.empty(shots, dtype=torch.int64, device=f"cuda:{local}")
     hist = torch.zeros(1 << nclb, dtype=torch.int64, device=f"cuda:{local}") if nclb <= 24 else None
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{local}")
-    opts = RunOptions(seed=seed)
-    prof = RunOptions(seed=seed, profile=True)
+    fused = not args.exact
+    opts = RunOptions(seed=seed, fused_matrices=fused)
+    prof = RunOptions(seed=seed, profile=True, fused_matrices=fused)
 
     def step(o):
         st = eng.run_batch_device(prog, o, values.data_ptr(), begin, shots)
@@ -370,7 +376,7 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     pass_s = other_s = 0.0
-    pass_launches = launches = passes_per_wave = shapes = skipped = 0
+    pass_launches = launches = passes_per_wave = shapes = skipped = fused_blocks = flagged = 0
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -380,6 +386,8 @@ def main():
             passes_per_wave = st.fused_passes
             shapes = st.specialised_shapes
             skipped += st.trunk_skipped
+            fused_blocks = st.fused_blocks
+            flagged += st.guard_flagged
             other_s += st.special_seconds + st.sample_seconds
             launches += nl
         ev1.record(stream)
@@ -405,7 +413,8 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.steps):
             p = Program.from_text(circuit, noise)  # host lowering + upload inside the step
-            r = eng.run_batch(p, RunOptions(shots=shots, seed=seed), shot_begin=begin, shot_count=shots)
+            r = eng.run_batch(p, RunOptions(shots=shots, seed=seed, fused_matrices=fused), shot_begin=begin,
+                              shot_count=shots)
             h_vals[:] = r._values
         e2e_s = time.perf_counter() - t0
         t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
@@ -425,44 +434,52 @@ def main():
     peak, peak_src = measured_peak()
     from paper_2308_03399_b200.api import _fp64_peak
     dp_peak = _fp64_peak(eng)
-    dp_shot = dp_ops_per_shot(prog)
-    fp64 = None
-    # Shared noiseless trunk: (shot, pass) pairs whose work the trunk did once
-    # for all shots are not executed; the FP64 rate counts executed work only
-    # (skipped pairs weighted as an average pass).
-    shot_passes = shots * args.steps * max(passes_per_wave, 1)
-    executed = max(0.0, 1.0 - skipped / shot_passes) if passes_per_wave else 1.0
-    if pass_s > 0:
-        dp_achieved = dp_shot * shots * args.steps * executed / pass_s
-        fp64 = {"bound": "fp64-pipe", "achieved": dp_achieved / 1e12, "peak": dp_peak / 1e12, "unit": "T DP-op/s",
-                "frac": dp_achieved / dp_peak, "dp_ops_per_shot": dp_shot,
-                "executed_shot_pass_frac": executed,
-                "peak_source": "measured live: ssb_fp64_peak (independent DMUL/DADD chains, CUDA events)",
-                "note": "the tile passes are FP64-issue bound: bit-exact parity forbids FMA, so every complex "
-                        "product is 4 DMUL + 2 DADD; this is the kernel's true roofline fraction"}
     n_timed_shots = shots * args.steps
-    if pass_s > 0:
-        achieved = pass_b * n_timed_shots / pass_s / 1e9
+    A = 1 << prog.num_qubits
+    roof = None
+    if pass_s > 0 and fused_blocks:
+        # Dominant kernel: fused_pass_kernel. Per shot it reads + writes the
+        # state once per pass (32 A bytes) and applies every block as a dense
+        # 4x4 complex matvec with FMA (16 DP instructions per amplitude).
+        bytes_shot = 32.0 * A * passes_per_wave
+        dp_shot = 16.0 * A * fused_blocks
+        kname = "fused_pass_kernel (4x4 blocks, register groups)"
+    elif pass_s > 0:
+        # Exact mode: the tile passes read + write the state once per pass; DP
+        # instructions are the engine's no-FMA arithmetic (dp_ops_per_shot).
+        executed = max(0.0, 1.0 - skipped / (n_timed_shots * max(passes_per_wave, 1))) if passes_per_wave else 1.0
+        bytes_shot = 32.0 * A * passes_per_wave * executed
+        dp_shot = dp_ops_per_shot(prog) * executed
         kname = ("ssb_tile_pass_jit (run-time shape-specialised, %d shapes)" % shapes if shapes else "tile_pass_kernel") \
             if prog.num_qubits > 13 else "resident_kernel"
-        roof = {"bound": "hbm", "kernel": kname,
-                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config, n_timed_shots * passes_per_wave * executed / max(pass_launches, 1)),
-                "traffic_source": "profiles/ncu_summary.json (ncu --set full dram__bytes_read+write per shot-pass)",
-                "peak_source": peak_src,
-                "algorithmic_bytes_per_shot": pass_b, "alg_bytes_per_launch": pass_b * n_timed_shots / max(
-                    pass_launches, 1),
-                "kernel_share_of_step": pass_s / max(elapsed, 1e-12), "launches": pass_launches,
-                "whole_step_alg_frac": value / world * total_b / 1e9 / peak,
-                "fp64": fp64,
-                "note": "algorithmic bytes = the reference's unfused op stream (SURVEY 8(d)); fused HBM tile "
-                        "passes move far fewer real bytes, so frac > 1 is expected — see traffic"}
-    else:
-        roof = None
+    if pass_s > 0:
+        hbm_ach = bytes_shot * n_timed_shots / pass_s / 1e9
+        dp_ach = dp_shot * n_timed_shots / pass_s
+        hbm_frac, dp_frac = hbm_ach / peak, dp_ach / dp_peak
+        fp64 = {"achieved": dp_ach / 1e12, "peak": dp_peak / 1e12, "unit": "T DP-op/s", "frac": dp_frac,
+                "dp_ops_per_shot": dp_shot,
+                "peak_source": "measured live: ssb_fp64_peak (independent DMUL/DADD chains, CUDA events; DFMA "
+                               "issues at the same per-lane rate on the FP64 pipe)"}
+        hbm = {"achieved": hbm_ach, "peak": peak, "unit": "GB/s", "frac": hbm_frac,
+               "algorithmic_bytes_per_shot": bytes_shot, "peak_source": peak_src,
+               "traffic": ncu_traffic(args.config + ("" if fused_blocks else "_exact"),
+                                      n_timed_shots * passes_per_wave / max(pass_launches, 1)),
+               "traffic_source": "profiles/ncu_summary.json (ncu --set full dram__bytes_read+write per shot-pass)"}
+        lead = fp64 if dp_frac >= hbm_frac else hbm
+        roof = {"bound": "fp64" if dp_frac >= hbm_frac else "hbm", "kernel": kname,
+                "achieved": lead["achieved"], "peak": lead["peak"], "unit": lead["unit"], "frac": lead["frac"],
+                "traffic": hbm["traffic"],
+                "launches": pass_launches, "kernel_share_of_step": pass_s / max(elapsed, 1e-12),
+                "fp64": fp64, "hbm": hbm,
+                "fusion_gain": pass_b / bytes_shot if bytes_shot else None,
+                "note": "frac = the binding unit of the dominant kernel (per-launch algorithmic work / its CUDA-event "
+                        "time); fusion_gain = the reference's unfused op stream bytes (SURVEY 8(d)) / the bytes this "
+                        "kernel must move"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * elapsed_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args.config, cfg, shots, world), "e2e": e2e, "gpu_launches": launches,
+            "config": config_dict(args.config, cfg, shots, world, fused=not args.exact), "e2e": e2e,
+            "gpu_launches": launches, "guard_flagged": flagged,
             "roofline": roof, "clocks": clocks.summary()}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(circuit, noise, seed, args.cpu_seconds, check_values=gpu_vals)

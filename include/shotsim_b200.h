@@ -217,6 +217,8 @@ SSB_API int ssb_counts_checksum(const uint64_t* values, uint64_t count, uint32_t
                                 uint64_t* num_keys_out);
 
 /* ---- engine (device) -------------------------------------------------- */
+/* Number of CUDA devices visible to the process (0 without a driver). */
+SSB_API int ssb_device_count(int* count);
 SSB_API int ssb_engine_create(int device, ssb_engine** out);
 SSB_API void ssb_engine_destroy(ssb_engine* engine);
 /* Opaque cudaStream_t the engine launches on (for CUDA-event timing). */

@@ -109,6 +109,7 @@ SIGNATURES = {
     "ssb_program_flat": (C.c_int, [_vp, C.POINTER(FlatProgram)]),
     "ssb_program_dump": (C.c_int, [_vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "ssb_counts_checksum": (C.c_int, [_pu64, _u64, C.c_uint32, C.c_uint32, _pu64, _pu64]),
+    "ssb_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "ssb_engine_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "ssb_engine_destroy": (None, [_vp]),
     "ssb_engine_stream": (_vp, [_vp]),

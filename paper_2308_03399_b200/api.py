@@ -154,6 +154,9 @@ class RunResult:
     fused_blocks: int = 0
     guard_flagged: int = 0
     guard_delta: float = 0.0
+    pass_seconds: float = 0.0     # profile=True: CUDA-event time of the fused passes
+    special_seconds: float = 0.0
+    sample_seconds: float = 0.0
     states: Optional[np.ndarray] = None
 
 
@@ -240,7 +243,9 @@ class Engine:
                       fused_passes=st.fused_passes, specialised_shapes=st.specialised_shapes,
                       sampling_serial_chunks=st.sampling_serial_chunks,
                       trunk_skipped=st.trunk_skipped, fused_blocks=st.fused_blocks,
-                      guard_flagged=st.guard_flagged, guard_delta=st.guard_delta, states=states)
+                      guard_flagged=st.guard_flagged, guard_delta=st.guard_delta,
+                      pass_seconds=st.pass_seconds, special_seconds=st.special_seconds,
+                      sample_seconds=st.sample_seconds, states=states)
         r._values = values
         return r
 

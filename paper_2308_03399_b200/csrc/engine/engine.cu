@@ -1007,6 +1007,18 @@ using namespace ssb;
 
 extern "C" {
 
+SSB_API int ssb_device_count(int* count) {
+  return guard([&] {
+    if (!count) throw std::invalid_argument("null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
 SSB_API int ssb_engine_create(int device, ssb_engine** out) {
   return guard([&] {
     if (!out) throw std::invalid_argument("null argument");

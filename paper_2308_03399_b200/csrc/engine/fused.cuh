@@ -33,11 +33,12 @@ struct FEntry {
   uint16_t xbegin, xcount;
 };
 
-// Shared memory: tile | base matrices | product slots | entries | extra
-// factors | hi offsets.
+// Shared memory: tile | base matrices | product slots | entries | group and
+// block descriptors | extra factors | hi offsets.
 __host__ __device__ inline uint64_t fused_smem_bytes(unsigned k, uint32_t max_blocks, uint32_t max_sites) {
   return (uint64_t{1} << k) * 16 + uint64_t{max_blocks} * 256 + uint64_t{kFusedSlots} * 256 +
-         uint64_t{max_blocks} * sizeof(FEntry) + uint64_t{max_sites} * 4 + (uint64_t{1} << (k - 8)) * 4 + 16;
+         uint64_t{max_blocks} * (sizeof(FEntry) + sizeof(FGroup) + sizeof(FBlock)) + uint64_t{max_sites} * 4 +
+         (uint64_t{1} << (k - 8)) * 4 + 16;
 }
 
 __device__ __forceinline__ uint32_t ins0(uint32_t x, unsigned p) {
@@ -104,31 +105,49 @@ __device__ __forceinline__ void load_mat(double2 (&m)[16], const double2* p) {
 }
 
 // Persistent over (shot, tile) units like tile_pass_body (k >= 8, NT = 256).
+// Every pass descriptor the inner loops read is staged in shared memory or
+// held in registers once per CTA (a reference into global memory would be
+// re-read after every barrier).
 static __global__ void __launch_bounds__(NT, 2)
     fused_pass_kernel(FusedView F, uint32_t pass_index, double2* state, uint64_t S, const uint8_t* pauli_sel,
                       uint32_t num_pauli, uint32_t max_blocks, uint32_t max_sites) {
   extern __shared__ double2 tile[];
-  const FPass& pd = F.passes[pass_index];
-  const unsigned n = F.n, k = pd.k;
+  __shared__ FPass spd;
+  __shared__ uint8_t hpos[32];
+  if (threadIdx.x == 0) spd = F.passes[pass_index];
+  __syncthreads();
+  const unsigned n = F.n, k = spd.k;
+  const bool first = spd.first;
+  const uint32_t blk0 = spd.blk_begin, nb = spd.blk_end - spd.blk_begin;
+  const uint32_t grp0 = spd.grp_begin, ng = spd.grp_end - spd.grp_begin;
   const uint64_t tiles = uint64_t{1} << (n - k);
   const uint32_t L = 1u << k;
-  const uint32_t nb = pd.blk_end - pd.blk_begin;
   double2* bmats = tile + L;
   double2* slots = bmats + max_blocks * 16;
   FEntry* ents = reinterpret_cast<FEntry*>(slots + kFusedSlots * 16);
-  uint32_t* xf = reinterpret_cast<uint32_t*>(ents + max_blocks);
+  FGroup* sgrp = reinterpret_cast<FGroup*>(ents + max_blocks);
+  FBlock* sblk = reinterpret_cast<FBlock*>(sgrp + max_blocks);
+  uint32_t* xf = reinterpret_cast<uint32_t*>(sblk + max_blocks);
   uint32_t* hi_off = xf + max_sites;
-  __shared__ uint8_t hpos[32];
 
-  for (uint32_t i = threadIdx.x; i < nb * 16; i += NT)
-    bmats[i] = F.mats[uint64_t{F.blocks[pd.blk_begin + i / 16].mat} * 16 + i % 16];
+  for (uint32_t i = threadIdx.x; i < nb; i += NT) {
+    FBlock b = F.blocks[blk0 + i];
+    sblk[i] = b;
+  }
+  for (uint32_t i = threadIdx.x; i < ng; i += NT) {
+    FGroup g = F.groups[grp0 + i];
+    g.blk_begin -= blk0;  // pass-local block indices
+    g.blk_end -= blk0;
+    sgrp[i] = g;
+  }
   for (uint32_t i = threadIdx.x; i < (1u << (k - 8)); i += NT)
-    hi_off[i] = static_cast<uint32_t>(pdep_positions(i, pd.lq + 8, k - 8));
+    hi_off[i] = static_cast<uint32_t>(pdep_positions(i, spd.lq + 8, k - 8));
   if (threadIdx.x == 0)
     for (unsigned q = 0, j = 0; q < n; ++q)
-      if (!((pd.lmask >> q) & 1)) hpos[j++] = static_cast<uint8_t>(q);
+      if (!((spd.lmask >> q) & 1)) hpos[j++] = static_cast<uint8_t>(q);
   __syncthreads();
-  const uint32_t lo_part = static_cast<uint32_t>(pdep_positions(threadIdx.x, pd.lq, 8));
+  for (uint32_t i = threadIdx.x; i < nb * 16; i += NT) bmats[i] = F.mats[uint64_t{sblk[i / 16].mat} * 16 + i % 16];
+  const uint32_t lo_part = static_cast<uint32_t>(pdep_positions(threadIdx.x, spd.lq, 8));
   const uint64_t units = S * tiles;
   const uint64_t u_begin = units * blockIdx.x / gridDim.x, u_end = units * (blockIdx.x + 1) / gridDim.x;
   const unsigned lane = threadIdx.x & 31;
@@ -141,7 +160,7 @@ static __global__ void __launch_bounds__(NT, 2)
       const uint8_t* sel = pauli_sel + s * num_pauli;
       uint32_t slot = 0, nx = 0;
       for (uint32_t b = 0; b < nb; ++b) {
-        const FBlock B = F.blocks[pd.blk_begin + b];
+        const FBlock B = sblk[b];
         FEntry ent{static_cast<uint32_t>(bmats + b * 16 - tile), static_cast<uint16_t>(nx), 0};
         double2* R = nullptr;
         for (uint32_t c0 = B.site_begin; c0 < B.site_end; c0 += 32) {
@@ -189,7 +208,7 @@ static __global__ void __launch_bounds__(NT, 2)
     const uint64_t t_end = u_end < (s + 1) * tiles ? u_end - s * tiles : tiles;
     for (uint64_t t = t_begin; t < t_end; ++t) {
       double2* tbase = seg + pdep_positions(t, hpos, n - k);
-      if (pd.first) {
+      if (first) {
         const bool origin = (tbase == seg);
         for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
           tile[swz(l)] = make_double2((origin && (lo_part | hi_off[i]) == 0) ? 1.0 : 0.0, 0.0);
@@ -219,29 +238,31 @@ static __global__ void __launch_bounds__(NT, 2)
         asm volatile("cp.async.wait_all;" ::: "memory");
       }
       __syncthreads();
-      for (uint32_t gi = pd.grp_begin; gi < pd.grp_end; ++gi) {
-        const FGroup G = F.groups[gi];
-        const uint32_t s0 = 1u << G.g[0], s1 = 1u << G.g[1], s2 = 1u << G.g[2], s3 = 1u << G.g[3];
-        // element e of a hexad at base | go(e) (e compile-time: a few ORs)
-#define SSB_GO(e) (((e) & 1 ? s0 : 0u) | ((e) & 2 ? s1 : 0u) | ((e) & 4 ? s2 : 0u) | ((e) & 8 ? s3 : 0u))
+      for (uint32_t gi = 0; gi < ng; ++gi) {
+        const FGroup G = sgrp[gi];
+        // swz is linear over XOR, so element e of a hexad sits at
+        // swz(base) ^ (XOR of swz(2^g_i) over the set bits i of e).
+        const uint32_t t0 = swz(1u << G.g[0]), t1 = swz(1u << G.g[1]), t2 = swz(1u << G.g[2]),
+                       t3 = swz(1u << G.g[3]);
+#define SSB_GO(e) (((e) & 1 ? t0 : 0u) ^ ((e) & 2 ? t1 : 0u) ^ ((e) & 4 ? t2 : 0u) ^ ((e) & 8 ? t3 : 0u))
         for (uint32_t h = threadIdx.x; h < hexads; h += NT) {
-          const uint32_t base = ins0(ins0(ins0(ins0(h, G.g[0]), G.g[1]), G.g[2]), G.g[3]);
+          const uint32_t sb = swz(ins0(ins0(ins0(ins0(h, G.g[0]), G.g[1]), G.g[2]), G.g[3]));
           double2 a[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) a[e] = tile[swz(base | SSB_GO(e))];
+          for (int e = 0; e < 16; ++e) a[e] = tile[sb ^ SSB_GO(e)];
           for (uint32_t b = G.blk_begin; b < G.blk_end; ++b) {
-            const FBlock B = F.blocks[b];
-            const FEntry ent = ents[b - pd.blk_begin];
+            const FEntry ent = ents[b];
+            const unsigned gb = sblk[b].gb0 * 4u + sblk[b].gb1;
             double2 m[16];
             load_mat(m, tile + ent.src);
-            apply_hexad_dyn(a, m, B.gb0, B.gb1);
+            apply_hexad_dyn(a, m, gb >> 2, gb & 3);
             for (uint32_t x = 0; x < ent.xcount; ++x) {
               load_mat(m, F.mats + uint64_t{xf[ent.xbegin + x]} * 16);
-              apply_hexad_dyn(a, m, B.gb0, B.gb1);
+              apply_hexad_dyn(a, m, gb >> 2, gb & 3);
             }
           }
 #pragma unroll
-          for (int e = 0; e < 16; ++e) tile[swz(base | SSB_GO(e))] = a[e];
+          for (int e = 0; e < 16; ++e) tile[sb ^ SSB_GO(e)] = a[e];
         }
 #undef SSB_GO
         __syncthreads();

@@ -10,6 +10,8 @@ prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
 mode = sys.argv[3] if len(sys.argv) > 3 else "batch"
 if mode == "batch":
     r = eng.run_batch(prog, RunOptions(shots=shots, seed=1))
+elif mode == "fused":
+    r = eng.run_batch(prog, RunOptions(shots=shots, seed=1, fused_matrices=True))
 else:  # branch:<budget>
     r = eng.run_branch(prog, RunOptions(shots=shots, seed=1, branch_budget=int(mode.split(":")[1])))
 print(key, shots, "shots", r.device_seconds, "s", shots / r.device_seconds, "shots/s")
