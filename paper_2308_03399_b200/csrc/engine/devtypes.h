@@ -163,16 +163,28 @@ struct FPass {
 // A register group: consecutive blocks of a pass whose qubits lie in four
 // local positions; each thread holds the group's 16 amplitudes of one "hexad"
 // in registers while every block of the group is applied.
+// Tensor-core layout (fused_pass_mma_kernel): within a team of 4 lanes, the
+// lane index j holds two group bits ("lane bits") and the 16 registers the
+// other two plus the team's 4 hexads. lane0/lane1: the group bits (0..3) in
+// lane-bit 0 / 1, reg0/reg1 the register bits — at the group's load (init)
+// and after its last block (fin, the store layout).
 struct FGroup {
   uint8_t g[4];                    // local positions, ascending (group bit i <-> g[i])
   uint32_t blk_begin, blk_end;
+  uint8_t init[4];                 // lane0, lane1, reg0, reg1 at load
+  uint8_t fin[4];                  // ... at store
 };
 
+// xch: up to two lane/register bit exchanges before the block, each a
+// nibble (valid << 3 | p << 1 | q: lane bit p <-> register bit q); perm: the
+// lanes hold the block's matrix bits in swapped order (apply M with bit 0 and
+// bit 1 of its row / column indices exchanged).
 struct FBlock {
   uint8_t p0, p1;                  // local positions of matrix bit 0 / bit 1
   uint8_t gb0, gb1;                // their group bits
   uint32_t mat;                    // base matrix (16 double2, row-major 4x4)
   uint32_t site_begin, site_end;   // its Pauli sites (FSite range)
+  uint8_t xch, perm, pad[2];
 };
 
 struct FSite {

@@ -676,9 +676,21 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
   uint64_t* gids = static_cast<uint64_t*>(scratch(E, "guard_ids", count * sizeof(uint64_t)));
   CK(cudaMemsetAsync(gcount, 0, sizeof(unsigned), E->stream));
   const SampleGuard guard{f.err_bound * guard_scale(), gcount, gids, count};
-  CK(cudaFuncSetAttribute(fused_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dp.fsmem)));
+  // FMA build (default) or, with SHOTSIM_B200_FUSED_MMA=1, the experimental
+  // tensor-core (FP64 MMA) build for tiles of 9..13 qubits. The MMA build is
+  // correct (same tests) but slower on C2 today: its lane / register bit
+  // exchanges cost more issue slots than the tensor core saves.
+  const char* mma_env = std::getenv("SHOTSIM_B200_FUSED_MMA");
+  const size_t mma_smem = fused_mma_smem_bytes(f.k, std::max(1u, f.max_pass_blocks), std::max(1u, f.max_pass_sites));
+  const bool use_mma = f.k >= 9 && f.k <= kMmaMaxK && mma_smem <= E->smem_optin &&
+                       (mma_env && *mma_env && *mma_env != '0');
+  const size_t smem = use_mma ? mma_smem : dp.fsmem;
+  const void* kfn = use_mma ? reinterpret_cast<const void*>(fused_pass_mma_kernel)
+                            : reinterpret_cast<const void*>(fused_pass_kernel);
+  CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_pass_kernel, NT, dp.fsmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, smem));
+  uint32_t max_blocks = std::max(1u, f.max_pass_blocks), max_sites = std::max(1u, f.max_pass_sites);
   uint64_t waves = 0;
   for (uint64_t w0 = 0; w0 < count; w0 += wave, ++waves) {
     const uint64_t S = std::min(wave, count - w0);
@@ -693,9 +705,10 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
         static_cast<unsigned>(std::min<uint64_t>(S * tiles, uint64_t(std::max(per_sm, 1)) * E->num_sms));
     for (uint32_t p = 0; p < f.passes.size(); ++p) {
       timer.begin(0);
-      fused_pass_kernel<<<grid, NT, dp.fsmem, E->stream>>>(dp.fview, p, state, S, psel, dp.num_pauli,
-                                                          std::max(1u, f.max_pass_blocks),
-                                                          std::max(1u, f.max_pass_sites));
+      uint32_t pass = p;
+      uint32_t npauli = dp.num_pauli;
+      void* args[] = {&dp.fview, &pass, &state, const_cast<uint64_t*>(&S), &psel, &npauli, &max_blocks, &max_sites};
+      CK(cudaLaunchKernel(kfn, dim3(grid), dim3(NT), args, smem, E->stream));
       launched(E);
       timer.end(0);
     }
@@ -725,7 +738,8 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
     stats->fused_passes = f.passes.size();
     stats->fused_blocks = f.num_blocks;
     stats->guard_flagged = flagged;
-    stats->guard_delta = 2.02 * guard.err + (2.0 * double(uint64_t{1} << n) + 16.0) * 0x1p-53;
+    // largest possible half-width (m = 2^n - 1, every S'_k <= 1)
+    stats->guard_delta = 2.02 * guard.err + (16.0 + 2.0 * double(uint64_t{1} << n) * (1.0 + 1e-6)) * 0x1p-53;
   }
 }
 

@@ -277,7 +277,7 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
           }
         }
       }
-      // Pad to four local positions (any unused ones) and assign group bits.
+      // (group bits assigned below; then the lane / register bit schedule)
       uint32_t lm = 0;
       for (unsigned q = 0; q < n; ++q)
         if (gm >> q & 1) lm |= 1u << pos[q];
@@ -290,6 +290,30 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
           if (g.g[i] == f.blocks[b].p0) f.blocks[b].gb0 = i;
           if (g.g[i] == f.blocks[b].p1) f.blocks[b].gb1 = i;
         }
+      // Lane / register bit schedule for the tensor-core kernel: the lanes
+      // start on the first block's bits; before each block, a lane bit the
+      // block does not use is exchanged with the register bit it does use.
+      {
+        uint8_t lane[2] = {f.blocks[g.blk_begin].gb0, f.blocks[g.blk_begin].gb1};
+        uint8_t reg[2], nr = 0;
+        for (uint8_t i = 0; i < 4; ++i)
+          if (i != lane[0] && i != lane[1]) reg[nr++] = i;
+        g.init[0] = lane[0], g.init[1] = lane[1], g.init[2] = reg[0], g.init[3] = reg[1];
+        for (uint32_t b = g.blk_begin; b < g.blk_end; ++b) {
+          FBlock& fb = f.blocks[b];
+          const auto want = [&](uint8_t x) { return x == fb.gb0 || x == fb.gb1; };
+          uint8_t xch = 0, nx = 0;
+          for (uint8_t pbit = 0; pbit < 2; ++pbit) {
+            if (want(lane[pbit])) continue;
+            const uint8_t qbit = want(reg[0]) && reg[0] != lane[pbit ^ 1] ? 0 : 1;
+            std::swap(lane[pbit], reg[qbit]);
+            xch |= static_cast<uint8_t>((8 | pbit << 1 | qbit) << (4 * nx++));
+          }
+          fb.xch = xch;
+          fb.perm = lane[0] != fb.gb0;
+        }
+        g.fin[0] = lane[0], g.fin[1] = lane[1], g.fin[2] = reg[0], g.fin[3] = reg[1];
+      }
       f.groups.push_back(g);
     }
     pd.grp_end = static_cast<uint32_t>(f.groups.size());

@@ -1024,6 +1024,7 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
   __shared__ uint64_t outcome;
   __shared__ double Ssh;
   __shared__ double s_prev, s_at;  // boundaries of the decision (guard band)
+  __shared__ double ssum;          // guard band: sum of upper bounds of S'_0 .. S'_m
   const uint64_t s = blockIdx.x;
   if (s >= S) return;
   const unsigned n = P.n, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1033,6 +1034,7 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
   if (threadIdx.x == 0) {
     decided = 0;
     Ssh = 0.0;
+    ssum = 0.0;
   }
   long long last_nz = -1;  // per thread, reduced at the end
   __syncthreads();
@@ -1087,6 +1089,7 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
           if (!(u < Send)) {
             Ssh = Send;  // no crossing in this chunk: advance exactly
             serial = false;
+            ssum += static_cast<double>(A - c0 < SAMPLE_CHUNK ? A - c0 : SAMPLE_CHUNK) * Send;
           }
         }
       }
@@ -1097,6 +1100,7 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
         for (uint32_t j = 0; j < cnt; ++j) {
           const double Sp = Sx;
           Sx = __dadd_rn(Sx, pbuf[j]);
+          ssum += Sx;
           if (u < Sx) {
             outcome = c0 + j;
             decided = 1;
@@ -1127,11 +1131,15 @@ static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView
   if (threadIdx.x == 0) {
     cregs[s] = apply_sample_outcome(P, cregs[s], outcome);
     if (guard_err > 0.0) {
-      // Fused-matrix amplitudes: |S'_m - S_m| <= 2 err (sum of |p' - p|) + the
-      // two sequential sums' rounding ((m + 1) u each) + p's own rounding.
+      // Fused-matrix amplitudes: |S'_m - S_m| <= sum |p' - p| (<= 2.02 err + p's
+      // own rounding, 16 u) + the rounding of the two sequential sums: each
+      // step errs by at most u * |its result|, and the reference's results
+      // are within 1e-6 of ours, so both sums together err by at most
+      // 2 u (sum_k S'_k + (m + 1) 1e-6) — ssum bounds sum_k S'_k from above.
       // A draw outside [S'_{m-1} + D, S'_m - D] decides the reference's m too;
       // inside it (or on the no-crossing fallback) the shot is replayed exactly.
-      const double D = 2.02 * guard_err + (2.0 * static_cast<double>(outcome) + 16.0) * 0x1p-53;
+      const double D = 2.02 * guard_err +
+                       (16.0 + 2.0 * ssum + 2e-6 * (static_cast<double>(outcome) + 1.0)) * 0x1p-53;
       const bool flag = !decided || !(u - s_prev >= D) || !(s_at - u > D);
       if (flag) {
         const unsigned i = atomicAdd(guard_count, 1u);

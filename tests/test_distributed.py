@@ -60,3 +60,60 @@ def test_two_rank_gather_equals_single_run(wide):
     out = mp.Manager().dict()
     mp.spawn(_worker, args=(2, _free_port(), circ, noise, shots, seed, wide, out), nprocs=2, join=True)
     assert out[0] == want and out[1] == want
+
+
+def _engine_worker(rank, world, port, circ, noise, shots, seed, out):
+    """One rank: its shard on the GPU engine (device values), the dense
+    histogram built on the device (ssb_histogram_device), summed over ranks."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        from paper_2308_03399_b200 import Engine, RunOptions
+        from paper_2308_03399_b200.distributed import allreduce_histogram, counts_from_histogram
+        eng = Engine(0)
+        prog = Program.from_text(circ, noise)
+        begin, count = shard_range(rank, world, shots)
+        vals = torch.empty(count, dtype=torch.int64, device="cuda:0")
+        hist = torch.zeros(1 << prog.num_clbits, dtype=torch.int64, device="cuda:0")
+        eng.run_batch_device(prog, RunOptions(seed=seed, fused_matrices=True), vals.data_ptr(), begin, count)
+        eng.histogram_device(vals.data_ptr(), count, prog.num_clbits, hist.data_ptr())
+        torch.cuda.synchronize()
+        h = allreduce_histogram(hist.cpu())
+        out[rank] = counts_from_histogram(h, prog.num_clbits, True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_engine_histogram_equals_single_run():
+    """The multi-GPU gather on the real device path: two ranks (gloo; both on
+    the one GPU of the box) run their shot-id shards through the engine, build
+    the histogram on the device and all-reduce it; the result equals the
+    single-rank run's counts."""
+    from paper_2308_03399_b200 import Engine, RunOptions
+    circ, noise = cc.quantum_volume(14, depth=4, seed=2), cc.qv_noise()
+    shots, seed = 3001, 5
+    r = Engine(0).run_batch(Program.from_text(circ, noise), RunOptions(shots=shots, seed=seed))
+    out = mp.Manager().dict()
+    mp.spawn(_engine_worker, args=(2, _free_port(), circ, noise, shots, seed, out), nprocs=2, join=True)
+    assert out[0] == r.counts and out[1] == r.counts
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_under_torchrun():
+    """bench.py's N > 1 path (torchrun, weak shot sharding, barriers,
+    max-over-ranks timing, device histogram all-reduce, rank-0 line) with two
+    ranks sharing the box's GPU over gloo (NCCL refuses duplicate GPUs)."""
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    env = dict(os.environ, SHOTSIM_BENCH_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "1",
+           "--warmup", "1", "--shots", "2048", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["global_shots_per_step"] == 4096 and line["value"] > 0
