@@ -138,7 +138,7 @@ struct PauliTermDev {
 
 struct PauliArgs {
   unsigned n, num_terms;
-  PauliTermDev t[16];
+  const PauliTermDev* t;  // device table (any length: the reference has no cap)
 };
 
 __device__ __forceinline__ double2 pauli_phase(uint64_t idx, uint64_t z, uint32_t num_y) {
@@ -208,6 +208,9 @@ struct Evolver {
   double2* scratch = nullptr;
   double2* mats = nullptr;  // Kraus / unitary matrices of the current op
   size_t mats_cap = 0;      // in double2
+  PauliTermDev* terms = nullptr;  // Pauli terms of the current site
+  size_t terms_cap = 0;
+  std::vector<PauliTermDev> host_terms;
 
   Evolver(const ssb_flat_program& f, cudaStream_t s, uint64_t* l, int sms)
       : F(f), stream(s), launches(l), num_sms(sms), n(f.num_qubits), d(1ull << f.num_qubits) {}
@@ -274,13 +277,23 @@ struct Evolver {
     PauliArgs a{};
     a.n = n;
     a.num_terms = op.term_count;
-    if (op.term_count > 16) throw std::invalid_argument("density evolver: Pauli site with > 16 terms");
+    if (op.term_count > terms_cap) {  // sites of any length (grown on demand)
+      void* p = nullptr;
+      CKD(cudaMalloc(&p, op.term_count * sizeof(PauliTermDev)));
+      allocs.push_back(p);
+      terms = static_cast<PauliTermDev*>(p);
+      terms_cap = op.term_count;
+    }
+    host_terms.resize(op.term_count);
     double prev = 0.0;
     for (uint32_t i = 0; i < op.term_count; ++i) {
       const ssb_flat_term& T = F.terms[op.term_begin + i];
-      a.t[i] = {T.cumulative - prev, T.x_mask, T.z_mask, T.num_y};  // density.cpp:190-192
+      host_terms[i] = {T.cumulative - prev, T.x_mask, T.z_mask, T.num_y};  // density.cpp:190-192
       prev = T.cumulative;
     }
+    CKD(cudaMemcpyAsync(terms, host_terms.data(), op.term_count * sizeof(PauliTermDev), cudaMemcpyHostToDevice,
+                        stream));
+    a.t = terms;
     dm_pauli<<<grid(d * d), 256, 0, stream>>>(t.rho, scratch, a);
     launched();
     std::swap(t.rho, scratch);

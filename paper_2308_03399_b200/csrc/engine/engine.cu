@@ -682,11 +682,15 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
   // exchanges cost more issue slots than the tensor core saves.
   const char* mma_env = std::getenv("SHOTSIM_B200_FUSED_MMA");
   const size_t mma_smem = fused_mma_smem_bytes(f.k, std::max(1u, f.max_pass_blocks), std::max(1u, f.max_pass_sites));
-  const bool use_mma = f.k >= 9 && f.k <= kMmaMaxK && mma_smem <= E->smem_optin &&
-                       (mma_env && *mma_env && *mma_env != '0');
-  const size_t smem = use_mma ? mma_smem : dp.fsmem;
-  const void* kfn = use_mma ? reinterpret_cast<const void*>(fused_pass_mma_kernel)
-                            : reinterpret_cast<const void*>(fused_pass_kernel);
+  // SHOTSIM_B200_FUSED_DB=1: the FMA apply in the double-buffered one-CTA layout.
+  const char* db_env = std::getenv("SHOTSIM_B200_FUSED_DB");
+  const bool db_ok = f.k >= 9 && f.k <= kMmaMaxK && mma_smem <= E->smem_optin;
+  const bool use_mma = db_ok && (mma_env && *mma_env && *mma_env != '0');
+  const bool use_db = db_ok && !use_mma && (db_env && *db_env && *db_env != '0');
+  const size_t smem = (use_mma || use_db) ? mma_smem : dp.fsmem;
+  const void* kfn = use_mma  ? reinterpret_cast<const void*>(fused_pass_mma_kernel)
+                    : use_db ? reinterpret_cast<const void*>(fused_pass_db_kernel)
+                             : reinterpret_cast<const void*>(fused_pass_kernel);
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, smem));

@@ -147,6 +147,7 @@ static __global__ void __launch_bounds__(NT, 2)
       if (!((spd.lmask >> q) & 1)) hpos[j++] = static_cast<uint8_t>(q);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nb * 16; i += NT) bmats[i] = F.mats[uint64_t{sblk[i / 16].mat} * 16 + i % 16];
+  __syncthreads();  // warp 0 copies base matrices into the product slots below
   const uint32_t lo_part = static_cast<uint32_t>(pdep_positions(threadIdx.x, spd.lq, 8));
   const uint64_t units = S * tiles;
   const uint64_t u_begin = units * blockIdx.x / gridDim.x, u_end = units * (blockIdx.x + 1) / gridDim.x;
@@ -376,9 +377,10 @@ __host__ __device__ inline uint64_t fused_mma_smem_bytes(unsigned k, uint32_t ma
 // their temporaries need ~200 registers); the tile of the next (shot, tile)
 // unit is fetched with cp.async into the second buffer while this one is
 // computed and stored, so HBM latency overlaps the tensor-core work.
-static __global__ void __launch_bounds__(NT, 1)
-    fused_pass_mma_kernel(FusedView F, uint32_t pass_index, double2* state, uint64_t S, const uint8_t* pauli_sel,
-                          uint32_t num_pauli, uint32_t max_blocks, uint32_t max_sites) {
+template <bool MMA>
+static __device__ __forceinline__ void fused_pass_db_body(FusedView F, uint32_t pass_index, double2* state, uint64_t S,
+                                                          const uint8_t* pauli_sel, uint32_t num_pauli,
+                                                          uint32_t max_blocks, uint32_t max_sites) {
   extern __shared__ double2 tile[];
   __shared__ FPass spd;
   __shared__ uint8_t hpos[32];
@@ -521,6 +523,33 @@ static __global__ void __launch_bounds__(NT, 1)
       uint32_t tg[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) tg[i] = hsw_slow(1u << G.g[i]);
+      if (!MMA) {  // FMA build: one hexad per thread, all 16 amplitudes in registers
+        for (uint32_t h = threadIdx.x; h < hexads; h += NT) {
+          const uint32_t sb = tab[h & 15] ^ tab[16 + (h >> 4)];
+          double2 a[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            a[e] = buf[sb ^ ((e & 1) ? tg[0] : 0u) ^ ((e & 2) ? tg[1] : 0u) ^ ((e & 4) ? tg[2] : 0u) ^
+                       ((e & 8) ? tg[3] : 0u)];
+          for (uint32_t bb = G.blk_begin; bb < G.blk_end; ++bb) {
+            const FEntry ent = ents[bb];
+            const unsigned gb = sblk[bb].gb0 * 4u + sblk[bb].gb1;
+            double2 m[16];
+            load_mat(m, tile + ent.src);
+            apply_hexad_dyn(a, m, gb >> 2, gb & 3);
+            for (uint32_t x = 0; x < ent.xcount; ++x) {
+              load_mat(m, F.mats + uint64_t{xf[ent.xbegin + x]} * 16);
+              apply_hexad_dyn(a, m, gb >> 2, gb & 3);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            buf[sb ^ ((e & 1) ? tg[0] : 0u) ^ ((e & 2) ? tg[1] : 0u) ^ ((e & 4) ? tg[2] : 0u) ^
+                ((e & 8) ? tg[3] : 0u)] = a[e];
+        }
+        __syncthreads();
+        continue;
+      }
       const uint32_t lin = ((j & 1) ? tg[G.init[0]] : 0u) ^ ((j & 2) ? tg[G.init[1]] : 0u);
       const uint32_t r0i = tg[G.init[2]], r1i = tg[G.init[3]];
       const uint32_t lfn = ((j & 1) ? tg[G.fin[0]] : 0u) ^ ((j & 2) ? tg[G.fin[1]] : 0u);
@@ -551,6 +580,20 @@ static __global__ void __launch_bounds__(NT, 1)
     for (uint32_t i = 0; i < nhi; ++i) tbase[lo_part | hi_off[i]] = buf[lo_sw ^ hi_sw[i]];
     __syncthreads();  // this buffer is refilled two units later
   }
+}
+
+static __global__ void __launch_bounds__(NT, 1)
+    fused_pass_mma_kernel(FusedView F, uint32_t pass_index, double2* state, uint64_t S, const uint8_t* pauli_sel,
+                          uint32_t num_pauli, uint32_t max_blocks, uint32_t max_sites) {
+  fused_pass_db_body<true>(F, pass_index, state, S, pauli_sel, num_pauli, max_blocks, max_sites);
+}
+
+// The FMA apply in the double-buffered, one-CTA-per-SM layout (A/B of the
+// occupancy / pipelining trade against fused_pass_kernel).
+static __global__ void __launch_bounds__(NT, 1)
+    fused_pass_db_kernel(FusedView F, uint32_t pass_index, double2* state, uint64_t S, const uint8_t* pauli_sel,
+                         uint32_t num_pauli, uint32_t max_blocks, uint32_t max_sites) {
+  fused_pass_db_body<false>(F, pass_index, state, S, pauli_sel, num_pauli, max_blocks, max_sites);
 }
 
 }  // namespace ssb

@@ -137,7 +137,14 @@ __host__ __device__ inline uint64_t resident_probs_doubles(const ProgView& P) {
 // ---------------------------------------------------------------------------
 // exp (debug, may be null): receives each shot's state as terminal sampling
 // reads it (or the final state), BatchState::segment (exec_batch.hpp:31-32).
-static __global__ void __launch_bounds__(NT, 2) resident_kernel(ProgView P, uint64_t seed, const uint64_t* ids,
+// CTAs per SM the register allocation must allow (both builds). Capping the
+// one-warp build's registers to fit 12 CTAs per SM (168 registers, spills)
+// was measured slower on C1 (17.3M vs 19.8M shots/s; profiles/r02), so the
+// one-warp build keeps up to 255 registers (8 CTAs per SM).
+#ifndef SSB_RESIDENT_MINB
+#define SSB_RESIDENT_MINB 2
+#endif
+static __global__ void __launch_bounds__(NT, SSB_RESIDENT_MINB) resident_kernel(ProgView P, uint64_t seed, const uint64_t* ids,
                                                          uint64_t shot_begin, uint64_t S, uint64_t* values, int* err,
                                                          double2* exp) {
   extern __shared__ double2 smem[];

@@ -67,6 +67,19 @@ void warn(const std::string& what) {
                what.c_str());
 }
 
+// NVRTC options with the resolved tuning knobs (experiments):
+// SHOTSIM_B200_JIT_QPT / _MINB override the quads per thread and CTAs-per-SM
+// launch bound of the specialised kernel.
+std::vector<std::string> nvrtc_options() {
+  auto knob = [](const char* name, const char* dflt) {
+    const char* v = std::getenv(name);
+    return std::string(v && *v ? v : dflt);
+  };
+  return {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES",
+          "-DSSB_QPT=" + knob("SHOTSIM_B200_JIT_QPT", SSB_STR(SSB_JIT_QPT)),
+          "-DSSB_TILE_MINB=" + knob("SHOTSIM_B200_JIT_MINB", SSB_STR(SSB_JIT_MINB))};
+}
+
 // NVRTC: shape source + embedded engine headers -> sm_100a cubin. Returns an
 // empty vector (and the log) on failure. Needs no GPU.
 std::vector<char> build_cubin(const std::string& shapes, std::string* log_out) {
@@ -80,16 +93,9 @@ std::vector<char> build_cubin(const std::string& shapes, std::string* log_out) {
     *log_out = "nvrtcCreateProgram failed";
     return {};
   }
-  // Tuning knobs (experiments): SHOTSIM_B200_JIT_QPT / _MINB override the
-  // quads per thread and CTAs-per-SM launch bound of the specialised kernel.
-  auto knob = [](const char* name, const char* dflt) {
-    const char* v = std::getenv(name);
-    return std::string(v && *v ? v : dflt);
-  };
-  const std::string qpt = "-DSSB_QPT=" + knob("SHOTSIM_B200_JIT_QPT", SSB_STR(SSB_JIT_QPT));
-  const std::string minb = "-DSSB_TILE_MINB=" + knob("SHOTSIM_B200_JIT_MINB", SSB_STR(SSB_JIT_MINB));
-  std::vector<const char*> opts = {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES",
-                                   qpt.c_str(), minb.c_str()};
+  const std::vector<std::string> base = nvrtc_options();
+  std::vector<const char*> opts;
+  for (const std::string& o : base) opts.push_back(o.c_str());
   // SHOTSIM_B200_JIT_VERBOSE=1: print ptxas register / spill usage to stderr.
   const char* verbose = std::getenv("SHOTSIM_B200_JIT_VERBOSE");
   const bool loud = verbose && *verbose && *verbose != '0';
@@ -120,8 +126,10 @@ std::vector<char> build_cubin(const std::string& shapes, std::string* log_out) {
 }
 
 // On-disk cubin cache: $SHOTSIM_B200_CACHE (default ~/.cache/shotsim_b200),
-// keyed by a 64-bit FNV-1a hash of everything that determines the cubin (the
-// shape source, the embedded headers, the compile knobs).
+// keyed by a 64-bit FNV-1a hash of everything that determines the cubin: the
+// shape source, the kernel's main source, the embedded headers, the exact
+// NVRTC options (resolved knobs included), the NVRTC version and the ABI
+// version — a rebuild that changes any of them never loads a stale cubin.
 std::string cache_path(const std::string& shapes) {
   const char* dir = std::getenv("SHOTSIM_B200_CACHE");
   std::string d;
@@ -137,9 +145,13 @@ std::string cache_path(const std::string& shapes) {
     for (size_t i = 0; i < n; ++i) h = (h ^ static_cast<unsigned char>(p[i])) * 1099511628211ull;
   };
   mix(shapes.data(), shapes.size());
+  mix(kMain, std::strlen(kMain));
   for (int i = 0; i < kJitHeaderCount; ++i) mix(kJitHeaderTexts[i], std::strlen(kJitHeaderTexts[i]));
-  for (const char* k : {"SHOTSIM_B200_JIT_QPT", "SHOTSIM_B200_JIT_MINB"})
-    if (const char* v = std::getenv(k)) mix(v, std::strlen(v));
+  for (const std::string& o : nvrtc_options()) mix(o.c_str(), o.size() + 1);
+  int major = 0, minor = 0;
+  nvrtcVersion(&major, &minor);
+  const int versions[3] = {major, minor, SSB_ABI_VERSION};
+  mix(reinterpret_cast<const char*>(versions), sizeof versions);
   char name[64];
   std::snprintf(name, sizeof name, "/tile_pass_%016llx.cubin", static_cast<unsigned long long>(h));
   return d + name;

@@ -37,7 +37,7 @@ out = {
     "shots_in_launch": shots,
     "duration_ms": dur_ms * dur_scale if dur_ms is not None else None,
     "dram_bytes_per_launch": dram,
-    "dram_bytes_per_shot": dram / shots,
+    "dram_bytes_per_shot": dram / shots if shots else None,
     "fp64_pipe_active_pct": f("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
     "issue_active_pct": f("sm__inst_executed.sum.pct_of_peak_sustained_elapsed"),
     "alu_pipe_pct": f("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
@@ -46,6 +46,10 @@ out = {
     "registers_per_thread": f("launch__registers_per_thread"),
     "achieved_occupancy_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active"),
     "shared_bank_conflicts": f("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+    "smem_wavefronts_pct": f("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+    "tensor_pipe_pct": f("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+    "grid": f("launch__grid_size"),
+    "block": f("launch__block_size"),
 }
 if alg:
     out["algorithmic_bytes_per_launch"] = alg * shots

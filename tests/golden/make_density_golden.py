@@ -50,6 +50,14 @@ def cases():
     h = 0.5 ** 0.5
     rules[1]["channel"]["matrices"] = [[[h * x, h * y] for x, y in m] for m in rules[1]["channel"]["matrices"] for _ in (0, 1)]
     out.append(("rnd4_kraus18", cc.random_layers(4, 3, 5), json.dumps({"rules": rules}), [1, 2]))
+    # A 2q Pauli site longer than 16 terms: 5% depolarizing with four terms
+    # listed twice at half weight (20 terms; duplicates are legal).
+    labels = [a + b for a in "IXYZ" for b in "IXYZ"]
+    terms = [[1 - 0.05 * 15 / 16 if l == "II" else 0.05 / 16, l] for l in labels]
+    terms = [t for t in terms if t[1] not in ("XX", "YY", "ZZ", "XZ")] + \
+            [[t[0] / 2, t[1]] for t in terms if t[1] in ("XX", "YY", "ZZ", "XZ") for _ in (0, 1)]
+    pauli20 = json.dumps({"rules": [{"gates": ["cx"], "arity": 2, "channel": {"type": "pauli", "terms": terms}}]})
+    out.append(("ghz5_pauli20", cc.ghz(5), pauli20, [0, 4]))
     return out
 
 
