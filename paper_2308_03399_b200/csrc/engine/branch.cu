@@ -16,9 +16,6 @@
 // sequential scan returns because the cumulative is monotone).
 #include <cuda_runtime.h>
 
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
 #include <cstdio>
@@ -299,6 +296,16 @@ struct ChildRun {
   uint32_t pad;
 };
 
+// A node's state HBM -> shared memory with asynchronous 16-byte copies
+// (LDGSTS): every element of the thread in flight at once instead of a
+// dependent load / store loop (ncu: long-scoreboard stalls dominated).
+__device__ __forceinline__ void load_state_async(double2* st, const double2* g, uint64_t A) {
+  const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(st));
+  for (uint64_t j = threadIdx.x; j < A; j += NT)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0 + static_cast<uint32_t>(16 * j)), "l"(g + j));
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(NT) b_child_run_kernel(ProgView P, DevOp site, double2* pool, const ChildRun* nodes,
                                                          uint64_t nn, unsigned n, uint32_t g_begin, uint32_t g_end,
                                                          int has_gates) {
@@ -308,7 +315,7 @@ __global__ void __launch_bounds__(NT) b_child_run_kernel(ProgView P, DevOp site,
     const ChildRun c = nodes[x];
     if (!c.has_kid && !has_gates) continue;
     double2* g = pool + (uint64_t{c.slot} << n);
-    for (uint64_t j = threadIdx.x; j < A; j += NT) st[j] = g[j];
+    load_state_async(st, g, A);
     __syncthreads();
     if (c.has_kid) {
       if (site.kind == K_PAULI) {
@@ -419,7 +426,7 @@ __global__ void b_node_fields(DevNode* nodes, uint64_t nn, DevOp site, int set_c
   if (active) active[x] = static_cast<uint8_t>(d.cond_ok);
 }
 
-// Nonzero (node, key) groups, compacted in (node, key) order by CUB: gather
+// Nonzero (node, key) groups, compacted in (node, key) order (b_scan_*): gather
 // their counts and node-level parameters for the host planner.
 __global__ void b_gather_groups(const uint32_t* sel, const unsigned* num, const unsigned* counts, const double* vals,
                                 unsigned* out_cnt, double* out_val) {
@@ -427,6 +434,97 @@ __global__ void b_gather_groups(const uint32_t* sel, const unsigned* num, const 
   if (j >= *num) return;
   out_cnt[j] = counts[sel[j]];
   if (vals) out_val[j] = vals[sel[j]];
+}
+
+// ---- Order-preserving compaction and exclusive scan of the branch tables
+// (three small kernels; no library kernels on the branch hot path).
+// Flag = true: out[k] = i for the k-th i with in[i] != 0 (cells of nonzero
+// (node, key) groups, in (node, key) order), *sum = their number.
+// Flag = false: out[i] = in[0] + ... + in[i-1] (shot offsets), *sum = total.
+constexpr unsigned kScanPer = 4, kScanItems = NT * kScanPer;
+
+template <bool Flag>
+__device__ __forceinline__ unsigned scan_val(const unsigned* in, uint64_t i, uint64_t count) {
+  if (i >= count) return 0;
+  return Flag ? (in[i] != 0 ? 1u : 0u) : in[i];
+}
+
+// Exclusive scan of one value per thread over the CTA; returns the CTA total.
+__device__ __forceinline__ unsigned cta_exclusive_scan(unsigned v, unsigned* prefix_out) {
+  __shared__ unsigned warp_tot[NT / 32];
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= static_cast<unsigned>(off)) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  unsigned base = 0, total = 0;
+  for (unsigned w = 0; w < NT / 32; ++w) {
+    if (w < wid) base += warp_tot[w];
+    total += warp_tot[w];
+  }
+  __syncthreads();  // warp_tot is reused by the next call
+  *prefix_out = base + x - v;
+  return total;
+}
+
+template <bool Flag>
+__global__ void __launch_bounds__(NT) b_scan_totals(const unsigned* in, uint64_t count, unsigned* totals) {
+  const uint64_t first = uint64_t{blockIdx.x} * kScanItems + threadIdx.x * kScanPer;
+  unsigned v = 0;
+#pragma unroll
+  for (unsigned r = 0; r < kScanPer; ++r) v += scan_val<Flag>(in, first + r, count);
+  unsigned prefix;
+  const unsigned tot = cta_exclusive_scan(v, &prefix);
+  if (threadIdx.x == 0) totals[blockIdx.x] = tot;
+}
+
+// One CTA: totals[] -> exclusive offsets in place; *sum = grand total.
+__global__ void __launch_bounds__(NT) b_scan_top(unsigned* totals, uint32_t nblk, unsigned* sum) {
+  __shared__ unsigned carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < nblk; c0 += NT) {
+    const uint32_t i = c0 + threadIdx.x;
+    const unsigned v = i < nblk ? totals[i] : 0;
+    unsigned prefix;
+    const unsigned tot = cta_exclusive_scan(v, &prefix);
+    const unsigned base = carry;
+    if (i < nblk) totals[i] = base + prefix;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = base + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *sum = carry;
+}
+
+template <bool Flag>
+__global__ void __launch_bounds__(NT) b_scan_apply(const unsigned* in, uint64_t count, const unsigned* offs,
+                                                   unsigned* out) {
+  const uint64_t first = uint64_t{blockIdx.x} * kScanItems + threadIdx.x * kScanPer;
+  unsigned v[kScanPer], t = 0;
+#pragma unroll
+  for (unsigned r = 0; r < kScanPer; ++r) {
+    v[r] = scan_val<Flag>(in, first + r, count);
+    t += v[r];
+  }
+  unsigned prefix;
+  cta_exclusive_scan(t, &prefix);
+  unsigned pos = offs[blockIdx.x] + prefix;
+#pragma unroll
+  for (unsigned r = 0; r < kScanPer; ++r) {
+    const uint64_t i = first + r;
+    if (i >= count) break;
+    if (Flag) {
+      if (v[r]) out[pos] = static_cast<unsigned>(i);
+    } else {
+      out[i] = pos;
+    }
+    pos += v[r];
+  }
 }
 
 // Dense destination table from the planner's per-group destinations.
@@ -447,7 +545,7 @@ __global__ void __launch_bounds__(NT) b_gate_run_kernel(ProgView P, double2* poo
   const uint64_t A = uint64_t{1} << n;
   for (uint64_t x = blockIdx.x; x < nn; x += gridDim.x) {
     double2* g = pool + (uint64_t{slots[x]} << n);
-    for (uint64_t j = threadIdx.x; j < A; j += NT) st[j] = g[j];
+    load_state_async(st, g, A);
     __syncthreads();
     const uint64_t creg = cregs[x];
     for (uint32_t i = op_begin; i < op_end; ++i) {
@@ -554,7 +652,7 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
     for (uint64_t x = 0; x < nn_dev; ++x) live[x] = HostNode{staging[x].slot, staging[x].off, staging[x].len, staging[x].creg};
     live_on_host = true;
   };
-  DBuf<uint8_t> dcubtmp{&E, "branch.cubtmp"};
+  DBuf<unsigned> dscantot{&E, "branch.scantot"}, dscansum{&E, "branch.scansum"};
 
   // Size every per-site table once for the run's worst case (live nodes <=
   // max_slots, keys per node <= the largest site fan-out), so the site loop
@@ -795,11 +893,16 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
       if (ncells >= (uint64_t{1} << 32)) throw std::length_error("branch group table too large");
       uint32_t* sel = dsel.get(ncells);
       unsigned* dnum = dnumsel.get(1);
-      size_t tmp_bytes = 0;
-      cub::CountingInputIterator<uint32_t> cells(0);
-      CKB(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, cells, counts, sel, dnum, static_cast<int>(ncells), s));
-      void* tmp = dcubtmp.get(tmp_bytes);
-      CKB(cub::DeviceSelect::Flagged(tmp, tmp_bytes, cells, counts, sel, dnum, static_cast<int>(ncells), s));
+      {  // sel = the nonzero cells in order, *dnum = their number
+        const uint32_t nblk = static_cast<uint32_t>((ncells + kScanItems - 1) / kScanItems);
+        unsigned* tot = dscantot.get(nblk);
+        b_scan_totals<true><<<nblk, NT, 0, s>>>(counts, ncells, tot);
+        launched();
+        b_scan_top<<<1, NT, 0, s>>>(tot, nblk, dnum);
+        launched();
+        b_scan_apply<true><<<nblk, NT, 0, s>>>(counts, ncells, tot, sel);
+        launched();
+      }
       unsigned* gcnt = dgcnt.get(ncells);
       double* gval = vals ? dgval.get(ncells) : nullptr;
       b_gather_groups<<<gridn(ncells), NT, 0, s>>>(sel, dnum, counts, vals, gcnt, gval);
@@ -832,10 +935,16 @@ void run_branch_device(EngineView& E, const ProgView& P, const HostDevProgram& h
           CKB(cudaMemcpyAsync(dfl, hf, nfree * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
         }
         unsigned* goff = dgoff.get(ng);
-        size_t scan_bytes = 0;
-        CKB(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, gcnt, goff, static_cast<int>(ng), s));
-        void* scan_tmp = dcubtmp.get(std::max(scan_bytes, tmp_bytes));
-        CKB(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, gcnt, goff, static_cast<int>(ng), s));
+        {  // goff = exclusive prefix sums of the group counts (shot offsets)
+          const uint32_t nblk = static_cast<uint32_t>((ng + kScanItems - 1) / kScanItems);
+          unsigned* tot = dscantot.get(nblk);
+          b_scan_totals<false><<<nblk, NT, 0, s>>>(gcnt, ng, tot);
+          launched();
+          b_scan_top<<<1, NT, 0, s>>>(tot, nblk, dscansum.get(1));
+          launched();
+          b_scan_apply<false><<<nblk, NT, 0, s>>>(gcnt, ng, tot, goff);
+          launched();
+        }
         DevNode* next_tab = (dlive == dlive_a.get(1) ? dlive_b : dlive_a).get(ng);
         ChildRun* runs = dchildrun.get(ng);
         uint32_t* csrc = dcopysrc.get(ng);

@@ -422,13 +422,44 @@ void plan_passes(HostDevProgram& d, unsigned tile_k, bool fuse_kraus) {
   bool need_init = true;
   size_t staged = 0;
 
-  auto close = [&](bool force) {
+  // epi_site: the Kraus site whose decide step follows this pass; when the
+  // pass can hold its reduction's index structure (the target(s) plus the
+  // lowest 9 (1q) / 3 (2q) other qubits), the pass computes that site's
+  // matrix-0 partial sums in an epilogue (PassDesc::epi_*).
+  auto close = [&](bool force, int64_t epi_site = -1) {
     staged = 0;
     if (cur_ops.empty() && !(force && need_init)) {
       cur = low;
       return;
     }
     uint32_t mask = cur;
+    uint32_t epi_req = 0, epi_tq[2] = {0, 0}, epi_arity = 0;
+    uint32_t epi_lowq[9];
+    unsigned epi_nlow = 0;
+    if (epi_site >= 0 && k >= 10) {
+      const DevOp& ko = d.ops[static_cast<size_t>(epi_site)];
+      const DevChannel& ch = d.channels[ko.aux];
+      epi_arity = ch.arity;
+      const unsigned want = ch.arity == 1 ? 9u : 3u;
+      // 1q: pairs = 2^(n-1) >= 512 (blocks of exactly 512); 2q: groups >= 8
+      // (and at most 128 partials per tile: EpiTables in tile_pass.cuh)
+      const bool sized = (ch.arity == 1 ? n >= 10 : n >= 5) && k - ch.arity - want <= 7;
+      if (sized && (ch.arity == 1 || ch.arity == 2)) {
+        uint32_t tm = 0;
+        for (unsigned b = 0; b < ch.arity; ++b) {
+          epi_tq[b] = ko.q[b];
+          tm |= 1u << ko.q[b];
+        }
+        epi_req = tm;
+        for (unsigned q = 0; q < n && epi_nlow < want; ++q)
+          if (!(tm >> q & 1)) {
+            epi_lowq[epi_nlow++] = q;
+            epi_req |= 1u << q;
+          }
+        if (static_cast<unsigned>(std::popcount(mask | epi_req)) <= k) mask |= epi_req;
+        else epi_req = 0;
+      }
+    }
     for (unsigned q = 0; q < n && static_cast<unsigned>(std::popcount(mask)) < k; ++q) mask |= 1u << q;
     PassDesc pd{};
     pd.lmask = mask;
@@ -441,6 +472,17 @@ void plan_passes(HostDevProgram& d, unsigned tile_k, bool fuse_kraus) {
         pd.lq[j] = static_cast<uint8_t>(q);
         pos[q] = static_cast<uint8_t>(j++);
       }
+    if (epi_req) {
+      pd.epi_kind = static_cast<uint8_t>(epi_arity);
+      pd.epi_op = static_cast<uint32_t>(epi_site);
+      for (unsigned b = 0; b < epi_arity; ++b) pd.epi_t[b] = pos[epi_tq[b]];
+      pd.epi_nlow = static_cast<uint8_t>(epi_nlow);
+      for (unsigned i = 0; i < epi_nlow; ++i) pd.epi_low[i] = pos[epi_lowq[i]];
+      uint8_t nhi = 0;
+      for (unsigned q = 0; q < n; ++q)
+        if ((mask >> q & 1) && !(epi_req >> q & 1)) pd.epi_hi[nhi++] = pos[q];
+      pd.epi_nhi = nhi;
+    }
     pd.item_begin = static_cast<uint32_t>(d.items.size());
     const uint32_t po_begin = static_cast<uint32_t>(d.pass_ops.size());
     segment_ops(d, cur_ops, pos, k);
@@ -471,8 +513,9 @@ void plan_passes(HostDevProgram& d, unsigned tile_k, bool fuse_kraus) {
       add(i);
     } else if (o.kind == K_KRAUS && fuse_kraus && k >= 2) {
       // Probabilities and per-shot choice between passes; the apply becomes
-      // the first micro-op of the next pass (no separate HBM sweep).
-      close(true);
+      // the first micro-op of the next pass (no separate HBM sweep), and the
+      // pass before computes the probabilities' matrix-0 partials.
+      close(true, i);
       d.steps.push_back({S_KRAUS_DECIDE, i});
       add(i);
     } else {

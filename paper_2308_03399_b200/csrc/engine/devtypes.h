@@ -75,6 +75,21 @@ struct PassDesc {
   uint32_t po_begin;   // first pass_op of this pass (per-op fallback, k < 2)
   uint32_t kraus_mat;  // matrix-table slot (16 double2) of the per-shot Kraus
                        // matrix when the pass starts with a Kraus apply
+  // Epilogue: the next Kraus site's matrix-0 partial sums, computed from the
+  // finished tile before it is stored (saves that site's separate state read).
+  // epi_kind 1: 1q site, partials = the 512-pair block sums of
+  // expval_matrix1_scalar (kernels_scalar.cpp:103-126); 2: 2q site, partials
+  // = the 8-group leaves of expval_generic's pairwise tree
+  // (statevector.cpp:56-80). epi_t: local positions of the target(s) (matrix
+  // bit 0 / 1); epi_low: local positions of the pair / group index bits inside
+  // one partial (the lowest non-target qubits, in order); epi_hi: the other
+  // local positions (which partial of the tile), in order.
+  uint8_t epi_kind;
+  uint8_t epi_nlow, epi_nhi;
+  uint8_t epi_t[2];
+  uint8_t epi_low[9];
+  uint8_t epi_hi[12];
+  uint32_t epi_op;     // the Kraus site (op index)
 };
 
 // Micro-op codes of a streamed pass (one per gate / Pauli site).

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -427,8 +428,10 @@ int sample_force_serial() {
 // executor's S_KRAUS_DECIDE step): scaled[s] = M_sel / sqrt(p_sel) and its
 // classes for the apply micro-op at the head of the next tile pass; inactive
 // shots (failed condition) get chosen = -1 and their apply is compacted away.
+// epi: matrix 0's partial sums for this site, computed by the preceding tile
+// pass's epilogue (PassDesc::epi_*), or null.
 void kraus_decide_wave(ssb_engine* E, DevProgram& dp, uint32_t op_index, const SegCtx& c, double2* scaled,
-                       uint64_t* cls, int* chosen) {
+                       uint64_t* cls, int* chosen, const double* epi) {
   const DevOp op = dp.host.ops[op_index];
   const unsigned n = dp.host.n;
   const ProgView& P = dp.view;
@@ -442,6 +445,47 @@ void kraus_decide_wave(ssb_engine* E, DevProgram& dp, uint32_t op_index, const S
     R.nq = 1;  // matrix mi only
     R.mats += 16 * mi;
     R.cls += mi;
+    if (mi == 0 && epi) {  // partials already in HBM: only the tree above them
+      double* val = static_cast<double*>(scratch(E, "val", c.S * sizeof(double)));
+      g_finish_kernel<<<static_cast<unsigned>(std::min<uint64_t>(c.S, 1u << 20)), NT, 0, E->stream>>>(
+          c.S, 1, R.nb, ch.arity == 2, pending, const_cast<double*>(epi), val);
+      launched(E);
+      const char* dbg = std::getenv("SHOTSIM_B200_EPI_CHECK");
+      if (!(dbg && *dbg == '1')) {
+        g_kraus_step_kernel<<<grid_for(c.S), NT, 0, E->stream>>>(P, op, 0, c.S, c.seed, c.ids, c.begin, c.u, pending,
+                                                                 val, cum, scaled, cls, chosen, E->err);
+        launched(E);
+        continue;
+      }
+      // debug: compare with the reduction kernels, then continue on their values
+      std::vector<double> a(c.S), pa(c.S * R.nb);
+      CK(cudaMemcpy(a.data(), val, c.S * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(pa.data(), epi, c.S * R.nb * 8, cudaMemcpyDeviceToHost));
+      double* part = static_cast<double*>(scratch(E, "part_dbg", c.S * R.nb * sizeof(double)));
+      double* v2 = static_cast<double*>(scratch(E, "val_dbg", c.S * sizeof(double)));
+      launch_reduce(E->stream, c.state, c.S, R, pending, part);
+      g_finish_kernel<<<static_cast<unsigned>(std::min<uint64_t>(c.S, 1u << 20)), NT, 0, E->stream>>>(
+          c.S, 1, R.nb, ch.arity == 2, pending, part, v2);
+      std::vector<double> b(c.S), pb(c.S * R.nb);
+      CK(cudaMemcpy(b.data(), v2, c.S * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(pb.data(), part, c.S * R.nb * 8, cudaMemcpyDeviceToHost));
+      uint64_t bad = 0, pbad = 0, first = ~0ull;
+      for (uint64_t i = 0; i < c.S; ++i) bad += a[i] != b[i];
+      for (uint64_t i = 0; i < c.S * R.nb; ++i)
+        if (pa[i] != pb[i]) {
+          ++pbad;
+          if (first == ~0ull) first = i;
+        }
+      std::fprintf(stderr, "epi op %u arity %u q %u,%u: values differ %llu/%llu, partials differ %llu/%llu",
+                   op_index, ch.arity, op.q[0], op.q[1], (unsigned long long)bad, (unsigned long long)c.S,
+                   (unsigned long long)pbad, (unsigned long long)(c.S * R.nb));
+      if (first != ~0ull) std::fprintf(stderr, " first at %llu: %.17g vs %.17g", (unsigned long long)first, pa[first], pb[first]);
+      std::fprintf(stderr, "\n");
+      g_kraus_step_kernel<<<grid_for(c.S), NT, 0, E->stream>>>(P, op, 0, c.S, c.seed, c.ids, c.begin, c.u, pending,
+                                                               v2, cum, scaled, cls, chosen, E->err);
+      launched(E);
+      continue;
+    }
     const uint64_t chunk = chunk_for(c.S, R.nb * sizeof(double) + 16);
     for (uint64_t off = 0; off < c.S; off += chunk) {
       const SegCtx cc = c.sub(off, std::min(chunk, c.S - off), n);
@@ -625,7 +669,14 @@ bool fused_ready(ssb_engine* E, DevProgram& dp) {
   if (dp.fused_tried) return dp.fplan.ok;
   dp.fused_tried = true;
   FusedPlan& f = dp.fplan;
-  f = plan_fused(dp.host, dp.host.tile_k);
+  // Register-group size: 4 (16-amplitude hexads) or 3 (8-amplitude octads,
+  // half the registers per thread, twice the CTAs per SM);
+  // SHOTSIM_B200_FUSED_GROUP overrides the default. The tensor-core build
+  // needs 4.
+  unsigned gq = kFusedGroupDefault;
+  if (const char* v = std::getenv("SHOTSIM_B200_FUSED_GROUP"); v && (*v == '3' || *v == '4')) gq = *v - '0';
+  if (const char* v = std::getenv("SHOTSIM_B200_FUSED_MMA"); v && *v && *v != '0') gq = 4;
+  f = plan_fused(dp.host, dp.host.tile_k, gq);
   if (f.ok && f.k < 8) {
     f.ok = false;
     f.why = "tile smaller than 8 qubits";
@@ -685,15 +736,21 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
   // SHOTSIM_B200_FUSED_DB=1: the FMA apply in the double-buffered one-CTA layout.
   const char* db_env = std::getenv("SHOTSIM_B200_FUSED_DB");
   const bool db_ok = f.k >= 9 && f.k <= kMmaMaxK && mma_smem <= E->smem_optin;
-  const bool use_mma = db_ok && (mma_env && *mma_env && *mma_env != '0');
-  const bool use_db = db_ok && !use_mma && (db_env && *db_env && *db_env != '0');
+  const bool use_mma = db_ok && f.gq == 4 && (mma_env && *mma_env && *mma_env != '0');
+  const bool use_db = db_ok && f.gq == 4 && !use_mma && (db_env && *db_env && *db_env != '0');
   const size_t smem = (use_mma || use_db) ? mma_smem : dp.fsmem;
-  const void* kfn = use_mma  ? reinterpret_cast<const void*>(fused_pass_mma_kernel)
-                    : use_db ? reinterpret_cast<const void*>(fused_pass_db_kernel)
-                             : reinterpret_cast<const void*>(fused_pass_kernel);
+  // FMA build: 256 threads for 12- and 13-qubit tiles, 128 for 11-qubit ones
+  // (one hexad per thread either way).
+  // (3-qubit groups: 256 threads, 2^(k-3) octads per tile)
+  const unsigned fnt = (use_mma || use_db) ? NT : (f.gq == 4 && f.k <= 11 ? 128u : 256u);
+  const void* kfn = use_mma              ? reinterpret_cast<const void*>(fused_pass_mma_kernel)
+                    : use_db             ? reinterpret_cast<const void*>(fused_pass_db_kernel)
+                    : f.gq == 3          ? reinterpret_cast<const void*>(fused_pass_kernel<256, 3>)
+                    : fnt == 128         ? reinterpret_cast<const void*>(fused_pass_kernel<128, 4>)
+                                         : reinterpret_cast<const void*>(fused_pass_kernel<256, 4>);
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NT, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, fnt, smem));
   uint32_t max_blocks = std::max(1u, f.max_pass_blocks), max_sites = std::max(1u, f.max_pass_sites);
   uint64_t waves = 0;
   for (uint64_t w0 = 0; w0 < count; w0 += wave, ++waves) {
@@ -712,7 +769,7 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
       uint32_t pass = p;
       uint32_t npauli = dp.num_pauli;
       void* args[] = {&dp.fview, &pass, &state, const_cast<uint64_t*>(&S), &psel, &npauli, &max_blocks, &max_sites};
-      CK(cudaLaunchKernel(kfn, dim3(grid), dim3(NT), args, smem, E->stream));
+      CK(cudaLaunchKernel(kfn, dim3(grid), dim3(fnt), args, smem, E->stream));
       launched(E);
       timer.end(0);
     }
@@ -879,6 +936,17 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       }
       CK(cudaMemcpyAsync(act_dev, act, nact * sizeof(uint32_t), cudaMemcpyHostToDevice, E->stream));
     }
+    // Matrix-0 partials of the next Kraus site from a pass epilogue: per shot
+    // at most 2^(n-1)/512 (1q) or 2^(n-2)/8 (2q) doubles.
+    double* epi_part = nullptr;
+    for (const PassDesc& pd : h.passes)
+      if (pd.epi_kind) {
+        const uint64_t per = std::max<uint64_t>((uint64_t{1} << (n - 1)) / 512, (uint64_t{1} << (n - 2)) / 8);
+        epi_part = static_cast<double*>(scratch(E, "epi_part", wave * per * sizeof(double)));
+        break;
+      }
+    // Default off until it pays (C4 A/B in DESIGN.md); SHOTSIM_B200_EPILOGUE=1 enables it.
+    if (const char* v = std::getenv("SHOTSIM_B200_EPILOGUE"); !(v && *v == '1')) epi_part = nullptr;
     // Per-shot Kraus choices of the wave (S_KRAUS_DECIDE -> next pass).
     double2* kmat = nullptr;
     uint64_t* kcls = nullptr;
@@ -924,12 +992,16 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       };
       ++waves;
       fused = 0;
+      int64_t epi_op = -1;  // the Kraus site whose matrix-0 partials the last pass computed
       for (const Step& st : h.steps) {
         if (st.kind == S_KRAUS_DECIDE) {
           timer.begin(1);
-          kraus_decide_wave(E, dp, st.index, c, kmat, kcls, kchosen);
+          kraus_decide_wave(E, dp, st.index, c, kmat, kcls, kchosen,
+                            epi_op == static_cast<int64_t>(st.index) ? epi_part : nullptr);
           timer.end(1);
+          epi_op = -1;
         } else if (st.kind == S_PASS) {
+          epi_op = (epi_part && h.passes[st.index].epi_kind) ? static_cast<int64_t>(h.passes[st.index].epi_op) : -1;
           // Trunk mode: only the trunk and the shots already diverged run.
           uint64_t active = S;
           if (wtrunk) {
@@ -942,13 +1014,15 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
               static_cast<unsigned>(std::min<uint64_t>(active * tiles, uint64_t(std::max(per_sm, 1)) * E->num_sms));
           uint32_t pass_index = st.index, num_pauli = dp.num_pauli;
           uint64_t* cregs = wtrunk ? nullptr : c.cregs;  // trunk mode: no conditions
+          double* epi = epi_op >= 0 ? epi_part : nullptr;
           void* args[] = {&dp.view, &pass_index, &state, &active, &cregs, &psel, &num_pauli,
-                          &kmat, &kcls, const_cast<uint32_t**>(&wact)};
+                          &kmat, &kcls, const_cast<uint32_t**>(&wact), &epi};
           CK(cudaLaunchKernel(kfn, dim3(grid), dim3(NT), args, tsmem, E->stream));
           launched(E);
           timer.end(0);
           ++fused;
         } else if (st.kind == S_SPECIAL) {
+          epi_op = -1;
           timer.begin(1);
           apply_op(E, dp, st.index, c, false);
           timer.end(1);

@@ -139,6 +139,9 @@ __device__ __forceinline__ ExactPick warp_exact_scan(Prob prob, uint64_t count, 
   return r;
 }
 
+// +infinity without <cmath> (the header is also compiled by NVRTC).
+__device__ __forceinline__ double scan_all() { return __longlong_as_double(0x7FF0000000000000ll); }
+
 struct NoSum {
   __device__ __forceinline__ void operator()(uint64_t, double) const {}
 };

@@ -8,6 +8,7 @@
 #include <bit>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <limits>
 
 namespace ssb {
@@ -100,7 +101,7 @@ uint32_t push(FusedPlan& f, const M4& m) {
 
 }  // namespace
 
-FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
+FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
   FusedPlan f;
   const unsigned n = h.n;
   if (n < 3) {
@@ -204,6 +205,11 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
   f.k = k;
   const uint32_t low = (1u << std::min(3u, k - 2)) - 1;
   const uint32_t all = n >= 32 ? ~0u : (1u << n) - 1;
+  // Blocks per pass (shared-memory staging): kFusedMaxPassBlocks, or the
+  // SHOTSIM_B200_FUSED_CAP tuning override (8..64).
+  uint32_t cap = kFusedMaxPassBlocks;
+  if (const char* v = std::getenv("SHOTSIM_B200_FUSED_CAP"); v && *v)
+    cap = std::max<uint32_t>(8, std::min<uint32_t>(64, static_cast<uint32_t>(std::strtoul(v, nullptr, 10))));
   std::vector<uint32_t> remaining(blks.size());
   for (uint32_t i = 0; i < remaining.size(); ++i) remaining[i] = i;
   bool first = true;
@@ -213,7 +219,7 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
     for (size_t r = 0; r < remaining.size(); ++r) {
       const uint32_t b = remaining[r];
       const uint32_t qm = (1u << blks[b].q0) | (1u << blks[b].q1);
-      if (!(qm & blocked) && static_cast<unsigned>(std::popcount(L | qm)) <= k && taken.size() < kFusedMaxPassBlocks) {
+      if (!(qm & blocked) && static_cast<unsigned>(std::popcount(L | qm)) <= k && taken.size() < cap) {
         L |= qm;
         taken.push_back(b);
       } else {
@@ -259,7 +265,7 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
           if (placed[t]) continue;
           const uint32_t b = taken[t];
           const uint32_t qm = (1u << blks[b].q0) | (1u << blks[b].q1);
-          if (!(qm & pending_q) && std::popcount(gm | qm) <= 4) {
+          if (!(qm & pending_q) && std::popcount(gm | qm) <= static_cast<int>(gq)) {
             gm |= qm;
             placed[t] = 1;
             ++nplaced;
@@ -281,9 +287,10 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
       uint32_t lm = 0;
       for (unsigned q = 0; q < n; ++q)
         if (gm >> q & 1) lm |= 1u << pos[q];
-      for (unsigned j = 0; j < k && std::popcount(lm) < 4; ++j) lm |= 1u << j;
+      for (unsigned j = 0; j < k && std::popcount(lm) < static_cast<int>(gq); ++j) lm |= 1u << j;
       for (unsigned j = 0, i = 0; j < k; ++j)
         if (lm >> j & 1) g.g[i++] = static_cast<uint8_t>(j);
+      if (gq == 3) g.g[3] = static_cast<uint8_t>(k);  // unused slot (3-qubit groups)
       g.blk_end = static_cast<uint32_t>(f.blocks.size());
       for (uint32_t b = g.blk_begin; b < g.blk_end; ++b)
         for (uint8_t i = 0; i < 4; ++i) {
@@ -323,6 +330,7 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k) {
     f.passes.push_back(pd);
   }
   f.num_blocks = static_cast<uint32_t>(blks.size());
+  f.gq = gq;
   f.ok = true;
   return f;
 }

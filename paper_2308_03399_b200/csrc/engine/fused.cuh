@@ -38,7 +38,7 @@ struct FEntry {
 __host__ __device__ inline uint64_t fused_smem_bytes(unsigned k, uint32_t max_blocks, uint32_t max_sites) {
   return (uint64_t{1} << k) * 16 + uint64_t{max_blocks} * 256 + uint64_t{kFusedSlots} * 256 +
          uint64_t{max_blocks} * (sizeof(FEntry) + sizeof(FGroup) + sizeof(FBlock)) + uint64_t{max_sites} * 4 +
-         (uint64_t{1} << (k - 8)) * 4 + 16;
+         (uint64_t{1} << (k - 7)) * 4 + 16;
 }
 
 __device__ __forceinline__ uint32_t ins0(uint32_t x, unsigned p) {
@@ -88,6 +88,40 @@ __device__ __forceinline__ void apply_hexad(double2 (&a)[16], const double2 (&m)
   }
 }
 
+// 8-amplitude "octad" of a 3-qubit group: two quads.
+template <int B0, int B1>
+__device__ __forceinline__ void apply_octad(double2 (&a)[8], const double2 (&m)[16]) {
+  constexpr int R = 3 - B0 - B1;  // the group bit that enumerates the quads
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    const int rest = o << R;
+    const int e0 = rest, e1 = rest | (1 << B0), e2 = rest | (1 << B1), e3 = rest | (1 << B0) | (1 << B1);
+    const double2 x0 = a[e0], x1 = a[e1], x2 = a[e2], x3 = a[e3];
+    double2 y[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double2 acc = make_double2(0.0, 0.0);
+      acc = cfma(m[r * 4 + 0], x0, acc);
+      acc = cfma(m[r * 4 + 1], x1, acc);
+      acc = cfma(m[r * 4 + 2], x2, acc);
+      acc = cfma(m[r * 4 + 3], x3, acc);
+      y[r] = acc;
+    }
+    a[e0] = y[0];
+    a[e1] = y[1];
+    a[e2] = y[2];
+    a[e3] = y[3];
+  }
+}
+
+__device__ __forceinline__ void apply_unit_dyn(double2 (&a)[8], const double2 (&m)[16], unsigned b0, unsigned b1) {
+  switch (b0 * 4 + b1) {
+    case 1: apply_octad<0, 1>(a, m); break;
+    case 2: apply_octad<0, 2>(a, m); break;
+    default: apply_octad<1, 2>(a, m); break;
+  }
+}
+
 __device__ __forceinline__ void apply_hexad_dyn(double2 (&a)[16], const double2 (&m)[16], unsigned b0, unsigned b1) {
   switch (b0 * 4 + b1) {  // b0 < b1 (the planner orders each block's matrix bits)
     case 1: apply_hexad<0, 1>(a, m); break;
@@ -99,16 +133,23 @@ __device__ __forceinline__ void apply_hexad_dyn(double2 (&a)[16], const double2 
   }
 }
 
+__device__ __forceinline__ void apply_unit_dyn(double2 (&a)[16], const double2 (&m)[16], unsigned b0, unsigned b1) {
+  apply_hexad_dyn(a, m, b0, b1);
+}
+
 __device__ __forceinline__ void load_mat(double2 (&m)[16], const double2* p) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) m[j] = p[j];
 }
 
-// Persistent over (shot, tile) units like tile_pass_body (k >= 8, NT = 256).
+// Persistent over (shot, tile) units like tile_pass_body. FNT threads (256:
+// 12-qubit tiles, 128: 11-qubit tiles — one 16-amplitude hexad per thread);
+// the low log2(FNT) local bits come from the thread index.
 // Every pass descriptor the inner loops read is staged in shared memory or
 // held in registers once per CTA (a reference into global memory would be
 // re-read after every barrier).
-static __global__ void __launch_bounds__(NT, 2)
+template <int FNT, int G>
+static __global__ void __launch_bounds__(FNT, (G == 4 ? 512 : 1024) / FNT)
     fused_pass_kernel(FusedView F, uint32_t pass_index, double2* state, uint64_t S, const uint8_t* pauli_sel,
                       uint32_t num_pauli, uint32_t max_blocks, uint32_t max_sites) {
   extern __shared__ double2 tile[];
@@ -130,25 +171,26 @@ static __global__ void __launch_bounds__(NT, 2)
   uint32_t* xf = reinterpret_cast<uint32_t*>(sblk + max_blocks);
   uint32_t* hi_off = xf + max_sites;
 
-  for (uint32_t i = threadIdx.x; i < nb; i += NT) {
+  for (uint32_t i = threadIdx.x; i < nb; i += FNT) {
     FBlock b = F.blocks[blk0 + i];
     sblk[i] = b;
   }
-  for (uint32_t i = threadIdx.x; i < ng; i += NT) {
+  for (uint32_t i = threadIdx.x; i < ng; i += FNT) {
     FGroup g = F.groups[grp0 + i];
     g.blk_begin -= blk0;  // pass-local block indices
     g.blk_end -= blk0;
     sgrp[i] = g;
   }
-  for (uint32_t i = threadIdx.x; i < (1u << (k - 8)); i += NT)
-    hi_off[i] = static_cast<uint32_t>(pdep_positions(i, spd.lq + 8, k - 8));
+  constexpr unsigned LB = FNT == 128 ? 7 : 8;
+  for (uint32_t i = threadIdx.x; i < (1u << (k - LB)); i += FNT)
+    hi_off[i] = static_cast<uint32_t>(pdep_positions(i, spd.lq + LB, k - LB));
   if (threadIdx.x == 0)
     for (unsigned q = 0, j = 0; q < n; ++q)
       if (!((spd.lmask >> q) & 1)) hpos[j++] = static_cast<uint8_t>(q);
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nb * 16; i += NT) bmats[i] = F.mats[uint64_t{sblk[i / 16].mat} * 16 + i % 16];
+  for (uint32_t i = threadIdx.x; i < nb * 16; i += FNT) bmats[i] = F.mats[uint64_t{sblk[i / 16].mat} * 16 + i % 16];
   __syncthreads();  // warp 0 copies base matrices into the product slots below
-  const uint32_t lo_part = static_cast<uint32_t>(pdep_positions(threadIdx.x, spd.lq, 8));
+  const uint32_t lo_part = static_cast<uint32_t>(pdep_positions(threadIdx.x, spd.lq, LB));
   const uint64_t units = S * tiles;
   const uint64_t u_begin = units * blockIdx.x / gridDim.x, u_end = units * (blockIdx.x + 1) / gridDim.x;
   const unsigned lane = threadIdx.x & 31;
@@ -211,64 +253,66 @@ static __global__ void __launch_bounds__(NT, 2)
       double2* tbase = seg + pdep_positions(t, hpos, n - k);
       if (first) {
         const bool origin = (tbase == seg);
-        for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
+        for (uint32_t l = threadIdx.x, i = 0; l < L; l += FNT, ++i)
           tile[swz(l)] = make_double2((origin && (lo_part | hi_off[i]) == 0) ? 1.0 : 0.0, 0.0);
       } else {
         const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
-        for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * NT, i0 += 8) {
+        for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * FNT, i0 += 8) {
           uint32_t off[8];
 #pragma unroll
-          for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * NT < L ? hi_off[i0 + j] : 0u;
+          for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * FNT < L ? hi_off[i0 + j] : 0u;
 #pragma unroll
           for (uint32_t j = 0; j < 8; ++j)
-            if (l0 + j * NT < L)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tile_s + 16 * swz(l0 + j * NT)),
+            if (l0 + j * FNT < L)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tile_s + 16 * swz(l0 + j * FNT)),
                            "l"(tbase + (lo_part | off[j])));
         }
         if (t + 1 < t_end) {
           const double2* nbase = seg + pdep_positions(t + 1, hpos, n - k);
-          for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * NT, i0 += 8) {
+          for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * FNT, i0 += 8) {
             uint32_t off[8];
 #pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * NT < L ? hi_off[i0 + j] : 0u;
+            for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * FNT < L ? hi_off[i0 + j] : 0u;
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j)
-              if (l0 + j * NT < L) asm volatile("prefetch.global.L2 [%0];" ::"l"(nbase + (lo_part | off[j])));
+              if (l0 + j * FNT < L) asm volatile("prefetch.global.L2 [%0];" ::"l"(nbase + (lo_part | off[j])));
           }
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
       }
       __syncthreads();
       for (uint32_t gi = 0; gi < ng; ++gi) {
-        const FGroup G = sgrp[gi];
-        // swz is linear over XOR, so element e of a hexad sits at
+        const FGroup GR = sgrp[gi];
+        // swz is linear over XOR, so element e of a unit sits at
         // swz(base) ^ (XOR of swz(2^g_i) over the set bits i of e).
-        const uint32_t t0 = swz(1u << G.g[0]), t1 = swz(1u << G.g[1]), t2 = swz(1u << G.g[2]),
-                       t3 = swz(1u << G.g[3]);
+        const uint32_t t0 = swz(1u << GR.g[0]), t1 = swz(1u << GR.g[1]), t2 = swz(1u << GR.g[2]),
+                       t3 = G == 4 ? swz(1u << GR.g[3]) : 0u;
 #define SSB_GO(e) (((e) & 1 ? t0 : 0u) ^ ((e) & 2 ? t1 : 0u) ^ ((e) & 4 ? t2 : 0u) ^ ((e) & 8 ? t3 : 0u))
-        for (uint32_t h = threadIdx.x; h < hexads; h += NT) {
-          const uint32_t sb = swz(ins0(ins0(ins0(ins0(h, G.g[0]), G.g[1]), G.g[2]), G.g[3]));
-          double2 a[16];
+        for (uint32_t h = threadIdx.x; h < (L >> G); h += FNT) {
+          uint32_t base = ins0(ins0(ins0(h, GR.g[0]), GR.g[1]), GR.g[2]);
+          if (G == 4) base = ins0(base, GR.g[3]);
+          const uint32_t sb = swz(base);
+          double2 a[1 << G];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) a[e] = tile[sb ^ SSB_GO(e)];
-          for (uint32_t b = G.blk_begin; b < G.blk_end; ++b) {
+          for (int e = 0; e < (1 << G); ++e) a[e] = tile[sb ^ SSB_GO(e)];
+          for (uint32_t b = GR.blk_begin; b < GR.blk_end; ++b) {
             const FEntry ent = ents[b];
             const unsigned gb = sblk[b].gb0 * 4u + sblk[b].gb1;
             double2 m[16];
             load_mat(m, tile + ent.src);
-            apply_hexad_dyn(a, m, gb >> 2, gb & 3);
+            apply_unit_dyn(a, m, gb >> 2, gb & 3);
             for (uint32_t x = 0; x < ent.xcount; ++x) {
               load_mat(m, F.mats + uint64_t{xf[ent.xbegin + x]} * 16);
-              apply_hexad_dyn(a, m, gb >> 2, gb & 3);
+              apply_unit_dyn(a, m, gb >> 2, gb & 3);
             }
           }
 #pragma unroll
-          for (int e = 0; e < 16; ++e) tile[sb ^ SSB_GO(e)] = a[e];
+          for (int e = 0; e < (1 << G); ++e) tile[sb ^ SSB_GO(e)] = a[e];
         }
 #undef SSB_GO
         __syncthreads();
       }
-      for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) tbase[lo_part | hi_off[i]] = tile[swz(l)];
+      for (uint32_t l = threadIdx.x, i = 0; l < L; l += FNT, ++i) tbase[lo_part | hi_off[i]] = tile[swz(l)];
     }
     __syncthreads();  // the next shot's matrices rewrite slots / ents
   }

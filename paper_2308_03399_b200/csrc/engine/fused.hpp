@@ -28,6 +28,7 @@ struct FusedPlan {
   bool ok = false;
   std::string why;                 // reason when !ok (the exact path runs)
   unsigned k = 0;
+  unsigned gq = 4;                 // register-group qubits (3 or 4)
   std::vector<FPass> passes;
   std::vector<FGroup> groups;
   std::vector<FBlock> blocks;
@@ -45,7 +46,11 @@ constexpr uint32_t kFusedMaxPassBlocks = 24;
 // Per-shot product slots in shared memory (noisy blocks beyond these apply
 // their Q factors as extra 4x4 entries — same result, more work).
 constexpr uint32_t kFusedSlots = 8;
+// Default register-group size of the FMA build (A/B: SHOTSIM_B200_FUSED_GROUP).
+constexpr unsigned kFusedGroupDefault = 4;
 
-FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k);
+// gq: qubits per register group (4: 16-amplitude hexads, the tensor-core
+// layout needs 4; 3: 8-amplitude octads, half the registers per thread).
+FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq = 4);
 
 }  // namespace ssb

@@ -294,7 +294,7 @@ static __global__ void __launch_bounds__(NT, SSB_RESIDENT_MINB) resident_kernel(
 }
 
 static __global__ void __launch_bounds__(NT, SSB_TILE_MINB) tile_pass_kernel(SSB_TILE_PASS_PARAMS) {
-  tile_pass_body(P, pass_index, state, S, cregs, pauli_sel, num_pauli, kmat, kcls, act);
+  tile_pass_body(SSB_TILE_PASS_ARGS);
 }
 
 // Per-(shot, Pauli site) term choice for a wave: sel[s][site] (u8).

@@ -48,7 +48,7 @@ const char* kMain =
     "#include \"tile_pass.cuh\"\n"
     "extern \"C\" __global__ void __launch_bounds__(ssb::NT, SSB_TILE_MINB)\n"
     "ssb_tile_pass_jit(SSB_TILE_PASS_PARAMS) {\n"
-    "  ssb::tile_pass_body(P, pass_index, state, S, cregs, pauli_sel, num_pauli, kmat, kcls, act);\n"
+    "  ssb::tile_pass_body(SSB_TILE_PASS_ARGS);\n"
     "}\n";
 
 struct Entry {

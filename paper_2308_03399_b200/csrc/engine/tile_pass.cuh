@@ -3,6 +3,7 @@
 #pragma once
 
 #include "shapes.cuh"
+#include "exact_scan.cuh"
 
 namespace ssb {
 
@@ -44,6 +45,89 @@ __device__ __forceinline__ uint64_t pdep_positions(uint64_t v, const uint8_t* po
   return out;
 }
 
+// Pass epilogue (PassDesc::epi_*): the next Kraus site's matrix-0 partial
+// sums from the finished tile, in the reference's order — 1q: each 512-pair
+// block's sequential sum of |row_0|^2, |row_1|^2 per pair in pair order
+// (kernels_scalar.cpp:103-126), one warp per block with the exact
+// warp-parallel sequential sum; 2q: each 8-group leaf of expval_generic's
+// pairwise tree (per group the rows' |.|^2 summed in order, then the 8 groups
+// in order; statevector.cpp:56-80, common.cpp:12-20), one thread per leaf.
+// Index tables (built once per CTA by epi_tables): off[j] local offset of
+// pair / group j inside a partial, hv[w] local offset of partial w of the
+// tile, pidx[w] its index contribution; tile_pidx: the tile's own part.
+struct EpiTables {
+  uint16_t off[512];
+  uint16_t hv[128];
+  uint32_t pidx[128];
+};
+
+// Partial-index bit of qubit q: its position among the non-target qubits
+// (pair / group index), minus the bits inside one partial (9 or 3).
+__device__ __forceinline__ int epi_bit(const DevOp& op, unsigned kind, unsigned q) {
+  unsigned below = 0;
+  for (unsigned b = 0; b < kind; ++b) below += op.q[b] < q;
+  return static_cast<int>(q - below) - (kind == 1 ? 9 : 3);
+}
+
+static __device__ __noinline__ void epi_tables(const ProgView& P, const PassDesc& pd, EpiTables& T) {
+  const DevOp& op = P.ops[pd.epi_op];
+  const unsigned kind = pd.epi_kind, nlow = pd.epi_nlow, nhi = pd.epi_nhi;
+  for (uint32_t j = threadIdx.x; j < (1u << nlow); j += NT)
+    T.off[j] = static_cast<uint16_t>(pdep_positions(j, pd.epi_low, nlow));
+  for (uint32_t w = threadIdx.x; w < (1u << nhi); w += NT) {
+    T.hv[w] = static_cast<uint16_t>(pdep_positions(w, pd.epi_hi, nhi));
+    uint32_t x = 0;
+    for (unsigned i = 0; i < nhi; ++i)
+      if ((w >> i) & 1) x |= 1u << epi_bit(op, kind, pd.lq[pd.epi_hi[i]]);
+    T.pidx[w] = x;
+  }
+}
+
+static __device__ __noinline__ void tile_epilogue(const ProgView& P, const PassDesc& pd, const EpiTables& T,
+                                                  const double2* tile, uint64_t tile_pidx, double* part) {
+  const DevOp& op = P.ops[pd.epi_op];
+  const DevChannel ch = P.channels[op.aux];
+  const double2* mg = P.mats + 16 * ch.mat_begin;  // matrix 0
+  const uint64_t cls = P.scaled_cls[ch.mat_begin];
+  const uint32_t nparts = 1u << pd.epi_nhi;
+  if (pd.epi_kind == 1) {
+    double2 m[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m[e] = mg[e];
+    const uint32_t tb = 1u << pd.epi_t[0];
+    for (uint32_t w = threadIdx.x >> 5; w < nparts; w += NT / 32) {
+      const uint32_t hv = T.hv[w];
+      const ExactPick r = warp_exact_scan(
+          [&](uint64_t t) {
+            const uint32_t l = T.off[t >> 1] | hv;
+            const double2 in[2] = {tile[l], tile[l | tb]};
+            return c_norm(row_apply<2>(m, cls, static_cast<int>(t & 1), in));
+          },
+          1024, scan_all(), NoSum{});
+      if ((threadIdx.x & 31) == 0) part[tile_pidx | T.pidx[w]] = r.s_at;
+    }
+  } else {
+    double2 m[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) m[e] = mg[e];
+    const uint32_t b0 = 1u << pd.epi_t[0], b1 = 1u << pd.epi_t[1];
+    for (uint32_t w = threadIdx.x; w < nparts; w += NT) {
+      const uint32_t hv = T.hv[w];
+      double acc = 0.0;
+#pragma unroll
+      for (uint32_t gi = 0; gi < 8; ++gi) {
+        const uint32_t base = T.off[gi] | hv;
+        const double2 in[4] = {tile[base], tile[base | b0], tile[base | b1], tile[base | b0 | b1]};
+        double row = 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) row = __dadd_rn(row, c_norm(row_apply<4>(m, cls, r, in)));
+        acc = __dadd_rn(acc, row);
+      }
+      part[tile_pidx | T.pidx[w]] = acc;
+    }
+  }
+}
+
 // Shared-memory layout of the tile pass: tile | matrix table | uops |
 // compacted uops | kept-uop prefix (u16, nu + 1) | kept-Pauli prefix (u16,
 // nu + 1) | high-part tile offsets (u32, 2^(k - 8)).
@@ -60,7 +144,7 @@ __host__ __device__ inline uint64_t tile_smem_bytes(unsigned k, uint32_t nuops, 
 static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_t pass_index, double2* state, uint64_t S,
                                                       const uint64_t* cregs, const uint8_t* pauli_sel,
                                                       uint32_t num_pauli, const double2* kmat, const uint64_t* kcls,
-                                                      const uint32_t* act) {
+                                                      const uint32_t* act, double* epi_part) {
   extern __shared__ double2 tile[];
   const PassDesc& pd = P.passes[pass_index];
   const unsigned n = P.n, k = pd.k;
@@ -89,6 +173,14 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
   __syncthreads();
 
   const uint32_t lo_part = static_cast<uint32_t>(pdep_positions(threadIdx.x, pd.lq, kt));
+  // Epilogue index tables (once per CTA).
+  __shared__ EpiTables epi_tab;
+  const bool epi = pd.epi_kind && epi_part;
+  const uint64_t epi_nb = pd.epi_kind == 1 ? (uint64_t{1} << (n - 1)) / 512 : (uint64_t{1} << (n - 2)) / 8;
+  if (epi) {
+    epi_tables(P, pd, epi_tab);
+    __syncthreads();
+  }
   bool no_relabel = true;
   for (uint32_t it_i = pd.item_begin; it_i < pd.item_end; ++it_i) no_relabel &= P.items[it_i].sigma == 0xE4;
   // Shape-specialised straight-line executors need every register round full.
@@ -164,7 +256,7 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
     // Nothing to apply for this shot (every micro-op compacted away — e.g. a
     // pass of readout Pauli sites that all drew identity) and no relabeled
     // segment to store: its tiles are left untouched in HBM.
-    if (!pd.first && pre[nu] == 0 && no_relabel) t_end = t_begin;
+    if (!pd.first && pre[nu] == 0 && no_relabel && !epi) t_end = t_begin;
     for (uint64_t t = t_begin; t < t_end; ++t) {
       double2* tbase = seg + pdep_positions(t, hpos, n - k);
       if (pd.first) {
@@ -226,6 +318,16 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
           run_segment_staged(tile, k, it, eops, b, e, smats, P.ops, kraus_cls);
         }
       }
+      if (epi) {  // the next Kraus site's matrix-0 partials
+        __syncthreads();
+        uint64_t tile_pidx = 0;  // the tile's non-local qubits' part of the partial index
+        for (unsigned i = 0; i < n - k; ++i)
+          if ((t >> i) & 1) tile_pidx |= uint64_t{1} << epi_bit(P.ops[pd.epi_op], pd.epi_kind, hpos[i]);
+        tile_epilogue(P, pd, epi_tab, tile, tile_pidx, epi_part + s * epi_nb);
+        // the epilogue reads other threads' elements: none may be refilled by
+        // the next tile's loads before every warp is done with them
+        __syncthreads();
+      }
       for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i) tbase[lo_part | hi_off[i]] = tile[l];
     }
     __syncthreads();  // compaction of the next shot rewrites eops/pre
@@ -234,6 +336,7 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
 
 #define SSB_TILE_PASS_PARAMS                                                                            \
   ssb::ProgView P, uint32_t pass_index, double2 *state, uint64_t S, const uint64_t *cregs, const uint8_t *pauli_sel, \
-      uint32_t num_pauli, const double2 *kmat, const uint64_t *kcls, const uint32_t *act
+      uint32_t num_pauli, const double2 *kmat, const uint64_t *kcls, const uint32_t *act, double *epi_part
+#define SSB_TILE_PASS_ARGS P, pass_index, state, S, cregs, pauli_sel, num_pauli, kmat, kcls, act, epi_part
 
 }  // namespace ssb

@@ -20,6 +20,8 @@ cases = [
     ("qv14 fused fma", cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise(), "batch", 4, {"fused_matrices": True}),
     ("rnd13 kraus streamed", cc.random_layers(13, depth=2, seed=3), cc.thermal_noise(0.05, 0.1), "batch", 4,
      {"resident_max_qubits": 1, "tile_qubits": 11}),
+    ("rnd14 kraus streamed epilogue (several tiles per CTA)", cc.random_layers(14, depth=2, seed=4),
+     cc.thermal_noise(0.05, 0.1), "batch", 256, {"resident_max_qubits": 1, "tile_qubits": 10}),
     ("dyn12 streamed specials", cc.dynamic(12, rounds=1), cc.depolarizing_model(0.02), "batch", 4,
      {"resident_max_qubits": 1, "tile_qubits": 10}),
 ]
