@@ -52,10 +52,16 @@ __device__ __forceinline__ uint64_t pdep_positions(uint64_t v, const uint8_t* po
 // warp-parallel sequential sum; 2q: each 8-group leaf of expval_generic's
 // pairwise tree (per group the rows' |.|^2 summed in order, then the 8 groups
 // in order; statevector.cpp:56-80, common.cpp:12-20), one thread per leaf.
-// Index tables (built once per CTA by epi_tables): off[j] local offset of
-// pair / group j inside a partial, hv[w] local offset of partial w of the
-// tile, pidx[w] its index contribution; tile_pidx: the tile's own part.
+// Everything the epilogue reads besides the tile is staged once per CTA in
+// shared memory (EpiTables): the matrix, its classes, off[j] the local offset
+// of pair / group j inside a partial, hv[w] the local offset of the tile's
+// partial w, pidx[w] its index contribution, tbit[i] that of the tile's i-th
+// non-local qubit.
 struct EpiTables {
+  double2 m[16];
+  uint64_t cls;
+  uint32_t kind, tb0, tb1;
+  uint32_t tbit[32];
   uint16_t off[512];
   uint16_t hv[128];
   uint32_t pidx[128];
@@ -69,9 +75,19 @@ __device__ __forceinline__ int epi_bit(const DevOp& op, unsigned kind, unsigned 
   return static_cast<int>(q - below) - (kind == 1 ? 9 : 3);
 }
 
-static __device__ __noinline__ void epi_tables(const ProgView& P, const PassDesc& pd, EpiTables& T) {
+static __device__ __noinline__ void epi_tables(const ProgView& P, const PassDesc& pd, const uint8_t* hpos, unsigned n,
+                                               EpiTables& T) {
   const DevOp& op = P.ops[pd.epi_op];
   const unsigned kind = pd.epi_kind, nlow = pd.epi_nlow, nhi = pd.epi_nhi;
+  const DevChannel ch = P.channels[op.aux];
+  for (uint32_t e = threadIdx.x; e < 16; e += NT) T.m[e] = P.mats[16 * ch.mat_begin + e];  // matrix 0
+  if (threadIdx.x == 0) {
+    T.cls = P.scaled_cls[ch.mat_begin];
+    T.kind = kind;
+    T.tb0 = 1u << pd.epi_t[0];
+    T.tb1 = kind == 2 ? 1u << pd.epi_t[1] : 0u;
+  }
+  for (uint32_t i = threadIdx.x; i < n - pd.k; i += NT) T.tbit[i] = 1u << epi_bit(op, kind, hpos[i]);
   for (uint32_t j = threadIdx.x; j < (1u << nlow); j += NT)
     T.off[j] = static_cast<uint16_t>(pdep_positions(j, pd.epi_low, nlow));
   for (uint32_t w = threadIdx.x; w < (1u << nhi); w += NT) {
@@ -83,47 +99,40 @@ static __device__ __noinline__ void epi_tables(const ProgView& P, const PassDesc
   }
 }
 
-static __device__ __noinline__ void tile_epilogue(const ProgView& P, const PassDesc& pd, const EpiTables& T,
-                                                  const double2* tile, uint64_t tile_pidx, double* part) {
-  const DevOp& op = P.ops[pd.epi_op];
-  const DevChannel ch = P.channels[op.aux];
-  const double2* mg = P.mats + 16 * ch.mat_begin;  // matrix 0
-  const uint64_t cls = P.scaled_cls[ch.mat_begin];
-  const uint32_t nparts = 1u << pd.epi_nhi;
-  if (pd.epi_kind == 1) {
-    double2 m[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) m[e] = mg[e];
-    const uint32_t tb = 1u << pd.epi_t[0];
+// One tile's partials (all threads; reads the tile and T only).
+__device__ __forceinline__ void tile_epilogue(const EpiTables& T, unsigned nhi, const double2* tile,
+                                              uint32_t tile_pidx, double* part) {
+  const uint32_t nparts = 1u << nhi;
+  if (T.kind == 1) {
+    // one warp per 512-pair block: 1024 terms summed in the reference order
+    const uint32_t tb = T.tb0;
     for (uint32_t w = threadIdx.x >> 5; w < nparts; w += NT / 32) {
       const uint32_t hv = T.hv[w];
       const ExactPick r = warp_exact_scan(
           [&](uint64_t t) {
             const uint32_t l = T.off[t >> 1] | hv;
             const double2 in[2] = {tile[l], tile[l | tb]};
-            return c_norm(row_apply<2>(m, cls, static_cast<int>(t & 1), in));
+            return c_norm(row_apply<2>(T.m, T.cls, static_cast<int>(t & 1), in));
           },
           1024, scan_all(), NoSum{});
       if ((threadIdx.x & 31) == 0) part[tile_pidx | T.pidx[w]] = r.s_at;
     }
   } else {
-    double2 m[16];
+    // 8 lanes per leaf: lane g computes group g's partial (rows summed in
+    // order), lane 0 of the 8 adds the 8 partials in order
+    const uint32_t b0 = T.tb0, b1 = T.tb1;
+    const unsigned lane = threadIdx.x & 31, gi = lane & 7;
+    for (uint32_t x = threadIdx.x; x < nparts * 8; x += NT) {
+      const uint32_t w = x >> 3;
+      const uint32_t base = T.off[gi] | T.hv[w];
+      const double2 in[4] = {tile[base], tile[base | b0], tile[base | b1], tile[base | b0 | b1]};
+      double row = 0.0;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) m[e] = mg[e];
-    const uint32_t b0 = 1u << pd.epi_t[0], b1 = 1u << pd.epi_t[1];
-    for (uint32_t w = threadIdx.x; w < nparts; w += NT) {
-      const uint32_t hv = T.hv[w];
+      for (int r = 0; r < 4; ++r) row = __dadd_rn(row, c_norm(row_apply<4>(T.m, T.cls, r, in)));
       double acc = 0.0;
 #pragma unroll
-      for (uint32_t gi = 0; gi < 8; ++gi) {
-        const uint32_t base = T.off[gi] | hv;
-        const double2 in[4] = {tile[base], tile[base | b0], tile[base | b1], tile[base | b0 | b1]};
-        double row = 0.0;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) row = __dadd_rn(row, c_norm(row_apply<4>(m, cls, r, in)));
-        acc = __dadd_rn(acc, row);
-      }
-      part[tile_pidx | T.pidx[w]] = acc;
+      for (unsigned g = 0; g < 8; ++g) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, row, (lane & ~7u) | g));
+      if (gi == 0) part[tile_pidx | T.pidx[w]] = acc;
     }
   }
 }
@@ -178,7 +187,7 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
   const bool epi = pd.epi_kind && epi_part;
   const uint64_t epi_nb = pd.epi_kind == 1 ? (uint64_t{1} << (n - 1)) / 512 : (uint64_t{1} << (n - 2)) / 8;
   if (epi) {
-    epi_tables(P, pd, epi_tab);
+    epi_tables(P, pd, hpos, n, epi_tab);
     __syncthreads();
   }
   bool no_relabel = true;
@@ -320,10 +329,10 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
       }
       if (epi) {  // the next Kraus site's matrix-0 partials
         __syncthreads();
-        uint64_t tile_pidx = 0;  // the tile's non-local qubits' part of the partial index
+        uint32_t tile_pidx = 0;  // the tile's non-local qubits' part of the partial index
         for (unsigned i = 0; i < n - k; ++i)
-          if ((t >> i) & 1) tile_pidx |= uint64_t{1} << epi_bit(P.ops[pd.epi_op], pd.epi_kind, hpos[i]);
-        tile_epilogue(P, pd, epi_tab, tile, tile_pidx, epi_part + s * epi_nb);
+          if ((t >> i) & 1) tile_pidx |= epi_tab.tbit[i];
+        tile_epilogue(epi_tab, pd.epi_nhi, tile, tile_pidx, epi_part + s * epi_nb);
         // the epilogue reads other threads' elements: none may be refilled by
         // the next tile's loads before every warp is done with them
         __syncthreads();

@@ -33,6 +33,12 @@ for name, circ, noise, mode, shots, kw in cases:
     run = eng.run_branch if mode == "branch" else eng.run_batch
     r = run(prog, RunOptions(shots=shots, seed=3, **kw))
     print(name, "ok", r.dispatch_count, flush=True)
+if not only or "epilogue" in only:  # the opt-in Kraus-site epilogue, several tiles per CTA
+    os.environ["SHOTSIM_B200_EPILOGUE"] = "1"
+    prog = Program.from_text(cc.random_layers(14, depth=2, seed=4), cc.thermal_noise(0.05, 0.1))
+    r = eng.run_batch(prog, RunOptions(shots=256, seed=3, resident_max_qubits=1, tile_qubits=10))
+    os.environ["SHOTSIM_B200_EPILOGUE"] = "0"
+    print("rnd14 kraus epilogue on ok", r.dispatch_count, flush=True)
 if not only or "mma" in only:
     os.environ["SHOTSIM_B200_FUSED_MMA"] = "1"
     prog = Program.from_text(cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise())

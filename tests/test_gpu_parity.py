@@ -309,3 +309,14 @@ def test_kraus_long_channel_all_paths(engine, oracle, n, tile):
     for kw in ({}, dict(resident_max_qubits=1, tile_qubits=tile)):
         assert (values(engine.run_batch(prog, RunOptions(shots=200, seed=3, **kw))) == want).all()
     assert (values(engine.run_branch(prog, RunOptions(shots=200, seed=3, branch_budget=16))) == want).all()
+
+
+@pytest.mark.parametrize("epilogue", ["0", "1"])
+def test_kraus_epilogue_parity(engine, oracle, monkeypatch, epilogue):
+    """The opt-in tile-pass epilogue (the next Kraus site's matrix-0 partials
+    from the preceding pass, exact sequential block sums) gives the
+    reference's values for 1q and 2q channels, with several tiles per CTA."""
+    monkeypatch.setenv("SHOTSIM_B200_EPILOGUE", epilogue)
+    prog = Program.from_text(cc.random_layers(17, depth=2, seed=17), cc.thermal_noise(0.05, 0.1))
+    want = oracle.run_shots(prog, np.arange(32), 5, threads=8)
+    assert (values(engine.run_batch(prog, RunOptions(shots=32, seed=5))) == want).all()
