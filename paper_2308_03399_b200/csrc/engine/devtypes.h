@@ -207,5 +207,8 @@ struct FSite {
   uint32_t qbase;                  // qidx[qbase + term]: Q matrix, or kNoQ (identity term)
 };
 constexpr uint32_t kNoQ = 0xFFFFFFFFu;
+// Per-shot product slots in shared memory (noisy blocks beyond these apply
+// their Q factors as extra 4x4 entries — same result, more work).
+constexpr uint32_t kFusedSlots = 8;
 
 }  // namespace ssb

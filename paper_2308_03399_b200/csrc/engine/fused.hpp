@@ -43,9 +43,6 @@ struct FusedPlan {
 
 // Shared-memory block staging limit per pass (base matrices + entry list).
 constexpr uint32_t kFusedMaxPassBlocks = 24;
-// Per-shot product slots in shared memory (noisy blocks beyond these apply
-// their Q factors as extra 4x4 entries — same result, more work).
-constexpr uint32_t kFusedSlots = 8;
 // Default register-group size of the FMA build (A/B: SHOTSIM_B200_FUSED_GROUP).
 constexpr unsigned kFusedGroupDefault = 4;
 

@@ -209,7 +209,88 @@ Entry compile(const std::string& shapes) {
   return e;
 }
 
+// Generic NVRTC build of a complete source (plus the embedded engine
+// headers) for sm_100a; FMA contraction allowed (the fused-matrix kernels).
+std::vector<char> build_generic_cubin(const std::string& source, std::string* log_out) {
+  std::vector<const char*> names(kJitHeaderNames, kJitHeaderNames + kJitHeaderCount);
+  std::vector<const char*> texts(kJitHeaderTexts, kJitHeaderTexts + kJitHeaderCount);
+  nvrtcProgram prog = nullptr;
+  if (nvrtcCreateProgram(&prog, source.c_str(), "ssb_fused_jit.cu", static_cast<int>(names.size()), texts.data(),
+                         names.data()) != NVRTC_SUCCESS) {
+    *log_out = "nvrtcCreateProgram failed";
+    return {};
+  }
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo"};
+  const nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, log.data());
+    *log_out = std::string(nvrtcGetErrorString(r)) + ": " + log.substr(0, 4000);
+    nvrtcDestroyProgram(&prog);
+    return {};
+  }
+  size_t size = 0;
+  nvrtcGetCUBINSize(prog, &size);
+  std::vector<char> cubin(size);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  return cubin;
+}
+
+std::string generic_cache_path(const std::string& source) {
+  const std::string shape_like = cache_path(source);  // same directory / key ingredients
+  if (shape_like.empty()) return "";
+  return shape_like.substr(0, shape_like.rfind('/')) + "/fused_" +
+         shape_like.substr(shape_like.rfind('_') + 1);
+}
+
+struct GenericEntry {
+  cudaLibrary_t lib = nullptr;
+  std::vector<cudaKernel_t> kernels;
+};
+std::map<std::string, GenericEntry> g_generic;
+
 }  // namespace
+
+// Compiles `source` with NVRTC (cached in-process and on disk) and returns
+// the named kernels, or an empty vector (and the log) on failure.
+std::vector<const void*> jit_compile_kernels(const std::string& source, const std::vector<std::string>& names,
+                                             std::string* log) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto it = g_generic.find(source);
+  if (it == g_generic.end()) {
+    GenericEntry e;
+    const std::string cpath = generic_cache_path(source);
+    std::vector<char> cubin = read_file(cpath);
+    if (cubin.empty()) {
+      cubin = build_generic_cubin(source, log);
+      if (!cubin.empty()) write_file_atomic(cpath, cubin);
+    }
+    if (!cubin.empty() &&
+        cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess) {
+      for (const std::string& nm : names) {
+        cudaKernel_t k = nullptr;
+        if (cudaLibraryGetKernel(&k, e.lib, nm.c_str()) != cudaSuccess) {
+          cudaGetLastError();
+          e.kernels.clear();
+          if (log) *log = "kernel " + nm + " missing";
+          break;
+        }
+        e.kernels.push_back(k);
+      }
+    } else {
+      cudaGetLastError();
+    }
+    it = g_generic.emplace(source, std::move(e)).first;
+  }
+  std::vector<const void*> out;
+  for (cudaKernel_t k : it->second.kernels) out.push_back(reinterpret_cast<const void*>(k));
+  return out;
+}
+
+bool jit_compile_check(const std::string& source, std::string* log) { return !build_generic_cubin(source, log).empty(); }
 
 bool specialise_compile_check(const HostDevProgram& h, std::string* log) {
   if (h.shapes.empty()) {
