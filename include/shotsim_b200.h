@@ -180,7 +180,9 @@ typedef struct ssb_stats {
   double special_seconds;    /* Kraus / measure / reset op-at-a-time kernels  */
   double sample_seconds;     /* terminal sampling                             */
   uint64_t specialised_shapes; /* streamed: segment shapes run straight-line
-                                  (run-time specialised kernel); 0: interpreter */
+                                  (run-time specialised kernel); 0: interpreter;
+                                  fused_matrices: passes run by their
+                                  specialised kernel (SHOTSIM_B200_FUSED_JIT) */
   uint64_t sampling_serial_chunks; /* terminal-sampling chunks replayed with the
                                       reference's sequential adds (binade
                                       changes, ties, the deciding chunk) */
@@ -250,6 +252,13 @@ SSB_API int ssb_histogram_device(ssb_engine* engine, const uint64_t* values_devi
  * number of distinct segment shapes; on failure the NVRTC log is in
  * ssb_last_error(). */
 SSB_API int ssb_program_specialise_check(const ssb_program* program, uint32_t tile_qubits, uint32_t* shapes);
+
+/* Plans `program` in fused-matrix mode (ssb_run_options::fused_matrices,
+ * 12-qubit tiles) and compiles its per-pass specialised fused kernels with
+ * NVRTC for sm_100a without loading them (no GPU needed). *kernels receives
+ * the number of specialised passes; on failure the NVRTC log is in
+ * ssb_last_error(). */
+SSB_API int ssb_program_fused_specialise_check(const ssb_program* program, uint32_t* kernels);
 
 /* Diagnostics: the HBM tile pass (0-based, in execution order) each op of the
  * program runs in under the streamed plan for `tile_qubits` (0: default);

@@ -123,6 +123,7 @@ SIGNATURES = {
     "ssb_exact_distribution": (C.c_int, [_vp, _vp, C.POINTER(C.c_uint32), C.c_uint32, _pd]),
     "ssb_tvd_vs_exact": (C.c_int, [_pu64, _u64, C.c_uint32, C.c_uint32, _pu64, _pd, _u64, _pd]),
     "ssb_program_specialise_check": (C.c_int, [_vp, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "ssb_program_fused_specialise_check": (C.c_int, [_vp, C.POINTER(C.c_uint32)]),
     "ssb_program_fused_info": (C.c_int, [_vp, C.c_uint32, C.POINTER(FusedInfoC)]),
     "ssb_program_pass_map": (C.c_int, [_vp, C.c_uint32, C.POINTER(C.c_uint32), _u64, C.POINTER(C.c_uint32)]),
     "ssb_batch_create": (C.c_int, [_vp, _vp, _pu64, _u64, _u64, C.POINTER(_vp)]),

@@ -55,6 +55,13 @@ class Program:
         check(load().ssb_program_specialise_check(self._h, tile_qubits, C.byref(n)))
         return n.value
 
+    def fused_specialise_check(self) -> int:
+        """Compiles the program's per-pass specialised fused-matrix kernels
+        with NVRTC (no GPU needed); returns how many passes were specialised."""
+        n = C.c_uint32(0)
+        check(load().ssb_program_fused_specialise_check(self._h, C.byref(n)))
+        return n.value
+
     def pass_map(self, tile_qubits: int = 0) -> np.ndarray:
         """Diagnostics: the streamed plan's tile pass of every op (-1: outside
         a pass), for `tile_qubits` local qubits (0: default). Host only."""

@@ -109,6 +109,8 @@ SSB_API int ssb_tvd_vs_exact(const uint64_t* values, uint64_t shots, uint32_t nu
 
 namespace ssb {
 bool specialise_compile_check(const HostDevProgram& h, std::string* log);
+std::vector<std::pair<std::string, std::vector<uint32_t>>> fused_jit_sources(const FusedPlan& f);
+bool fused_jit_compile_check(const FusedPlan& f, std::string* log);
 }
 
 extern "C" SSB_API int ssb_program_pass_map(const ssb_program* program, uint32_t tile_qubits, uint32_t* pass_of_op,
@@ -137,6 +139,19 @@ extern "C" SSB_API int ssb_program_specialise_check(const ssb_program* program, 
     *shapes = static_cast<uint32_t>(h.shapes.size());
     std::string log;
     if (!ssb::specialise_compile_check(h, &log)) throw ssb::CudaError("shape specialisation failed: " + log);
+  });
+}
+
+extern "C" SSB_API int ssb_program_fused_specialise_check(const ssb_program* program, uint32_t* kernels) {
+  return ssb::guard([&] {
+    if (!program || !kernels) throw std::invalid_argument("null argument");
+    const ssb::FusedPlan f = ssb::plan_fused(program->dev, 12u);
+    if (!f.ok) throw std::invalid_argument("no fused-matrix plan: " + f.why);
+    uint32_t n = 0;
+    for (const auto& m : ssb::fused_jit_sources(f)) n += static_cast<uint32_t>(m.second.size());
+    *kernels = n;
+    std::string log;
+    if (!ssb::fused_jit_compile_check(f, &log)) throw ssb::CudaError("fused specialisation failed: " + log);
   });
 }
 

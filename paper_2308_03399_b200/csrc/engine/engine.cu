@@ -33,6 +33,8 @@ int launch_resident_warp(const void* view, uint64_t seed, uint64_t shot_begin, u
 
 // specialise.cpp: the shape-specialised tile-pass kernel for a plan, or null.
 const void* specialised_tile_kernel(const HostDevProgram& h);
+// fused_jit.cpp: per pass the specialised fused kernel, or null.
+std::vector<const void*> fused_jit_kernels(const FusedPlan& f, std::string* log);
 
 // Device copy of one program (+ its pass plan for one tile size).
 struct DevProgram {
@@ -52,6 +54,9 @@ struct DevProgram {
   FusedPlan fplan;
   FusedView fview{};
   size_t fsmem = 0;
+  // Per pass the run-time specialised fused kernel (fused_jit.cpp) or null.
+  bool fjit_tried = false;
+  std::vector<const void*> fjit;
   ~DevProgram() {
     for (void* p : allocs) cudaFree(p);
   }
@@ -751,6 +756,30 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, fnt, smem));
+  // SHOTSIM_B200_FUSED_JIT=1: the per-pass specialised kernels (fused_jit.cpp)
+  // for the passes that have one (same arithmetic, constant-bank products).
+  const char* jit_env = std::getenv("SHOTSIM_B200_FUSED_JIT");
+  const bool use_jit = !use_mma && !use_db && f.gq == 4 && fnt == 256 && jit_env && *jit_env && *jit_env != '0';
+  if (use_jit && !dp.fjit_tried) {
+    dp.fjit_tried = true;
+    std::string log;
+    dp.fjit = fused_jit_kernels(f, &log);
+    for (const void*& k : dp.fjit)
+      if (k && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+                   cudaSuccess) {
+        cudaGetLastError();
+        k = nullptr;
+      }
+    if (!log.empty()) std::fprintf(stderr, "shotsim_b200: fused specialisation: %s\n", log.c_str());
+  }
+  int jit_per_sm = 0;  // the smallest residency over the specialised kernels
+  if (use_jit)
+    for (const void* k : dp.fjit)
+      if (k) {
+        int v = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, fnt, smem));
+        jit_per_sm = jit_per_sm ? std::min(jit_per_sm, v) : v;
+      }
   uint32_t max_blocks = std::max(1u, f.max_pass_blocks), max_sites = std::max(1u, f.max_pass_sites);
   uint64_t waves = 0;
   for (uint64_t w0 = 0; w0 < count; w0 += wave, ++waves) {
@@ -764,12 +793,15 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
     }
     const unsigned grid =
         static_cast<unsigned>(std::min<uint64_t>(S * tiles, uint64_t(std::max(per_sm, 1)) * E->num_sms));
+    const unsigned jgrid =
+        static_cast<unsigned>(std::min<uint64_t>(S * tiles, uint64_t(std::max(jit_per_sm, 1)) * E->num_sms));
     for (uint32_t p = 0; p < f.passes.size(); ++p) {
       timer.begin(0);
       uint32_t pass = p;
       uint32_t npauli = dp.num_pauli;
       void* args[] = {&dp.fview, &pass, &state, const_cast<uint64_t*>(&S), &psel, &npauli, &max_blocks, &max_sites};
-      CK(cudaLaunchKernel(kfn, dim3(grid), dim3(fnt), args, smem, E->stream));
+      const void* pk = use_jit && p < dp.fjit.size() && dp.fjit[p] ? dp.fjit[p] : kfn;
+      CK(cudaLaunchKernel(pk, dim3(pk == kfn ? grid : jgrid), dim3(fnt), args, smem, E->stream));
       launched(E);
       timer.end(0);
     }
@@ -798,6 +830,9 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
     stats->passes = waves;
     stats->fused_passes = f.passes.size();
     stats->fused_blocks = f.num_blocks;
+    stats->specialised_shapes = 0;
+    if (use_jit)
+      for (const void* k : dp.fjit) stats->specialised_shapes += k != nullptr;
     stats->guard_flagged = flagged;
     // largest possible half-width (m = 2^n - 1, every S'_k <= 1)
     stats->guard_delta = 2.02 * guard.err + (16.0 + 2.0 * double(uint64_t{1} << n) * (1.0 + 1e-6)) * 0x1p-53;

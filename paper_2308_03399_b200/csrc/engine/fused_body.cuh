@@ -56,8 +56,9 @@ __device__ __forceinline__ double2 cfma(double2 m, double2 a, double2 acc) {
 
 // y = M x on the four register quads of a hexad whose matrix bits are group
 // bits B0 < B1 (the other two group bits enumerate the quads).
-template <int B0, int B1>
-__device__ __forceinline__ void apply_hexad(double2 (&a)[16], const double2 (&m)[16]) {
+// M: a register array double2[16] or a pointer (shared / constant memory).
+template <int B0, int B1, class M>
+__device__ __forceinline__ void apply_hexad(double2 (&a)[16], const M& m) {
 #pragma unroll
   for (int o = 0; o < 4; ++o) {
     // spread o over the two group bits that are not B0 / B1
@@ -136,6 +137,58 @@ __device__ __forceinline__ void apply_unit_dyn(double2 (&a)[16], const double2 (
 __device__ __forceinline__ void load_mat(double2 (&m)[16], const double2* p) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) m[j] = p[j];
+}
+
+// Cold path of a specialised pass (a block whose shot drew a non-identity
+// Pauli): the hexad goes back to its tile slots (the thread owns them), the
+// block's matrix and extra factors are applied there by a rolled loop, and
+// the hexad is reloaded — few live registers, so the hot path keeps its
+// allocation (an inline register version spills, an out-of-line one puts the
+// hexad in local memory).
+template <int B0, int B1>
+__device__ __forceinline__ void tile_apply_rolled(double2* tile, uint32_t sb, const uint32_t (&t)[4],
+                                                  const double2* m) {
+#pragma unroll 1
+  for (int o = 0; o < 4; ++o) {
+    uint32_t rest = 0;
+    for (int j = 0, bit = 0; j < 4; ++j)
+      if (j != B0 && j != B1) rest ^= ((o >> bit++) & 1) ? t[j] : 0u;
+    const uint32_t e0 = sb ^ rest, e1 = e0 ^ t[B0], e2 = e0 ^ t[B1], e3 = e1 ^ t[B1];
+    const double2 x0 = tile[e0], x1 = tile[e1], x2 = tile[e2], x3 = tile[e3];
+#pragma unroll 1
+    for (int r = 0; r < 4; ++r) {
+      double2 acc = make_double2(0.0, 0.0);
+      acc = cfma(m[r * 4 + 0], x0, acc);
+      acc = cfma(m[r * 4 + 1], x1, acc);
+      acc = cfma(m[r * 4 + 2], x2, acc);
+      acc = cfma(m[r * 4 + 3], x3, acc);
+      tile[r == 0 ? e0 : r == 1 ? e1 : r == 2 ? e2 : e3] = acc;  // the x are in registers
+    }
+  }
+}
+
+// One block of a specialised pass (fused_jit.cpp): the constant-bank product
+// cm when this shot's entry is the block's noiseless base matrix (shared
+// offset const_src, no extra factors), else the entry's matrix and factors
+// (cold path above). sb / t: the hexad's tile base and bit offsets.
+template <int B0, int B1>
+__device__ __forceinline__ void jit_block(double2 (&a)[16], const FEntry ent, uint32_t const_src, const double2* cm,
+                                          double2* tile, uint32_t sb, const uint32_t (&t)[4], const uint32_t* xf,
+                                          const FusedView& F) {
+  if (ent.src == const_src && ent.xcount == 0) {
+    apply_hexad<B0, B1>(a, cm);
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    tile[sb ^ ((e & 1 ? t[0] : 0u) ^ (e & 2 ? t[1] : 0u) ^ (e & 4 ? t[2] : 0u) ^ (e & 8 ? t[3] : 0u))] = a[e];
+  tile_apply_rolled<B0, B1>(tile, sb, t, tile + ent.src);
+#pragma unroll 1
+  for (uint32_t x = 0; x < ent.xcount; ++x)
+    tile_apply_rolled<B0, B1>(tile, sb, t, F.mats + uint64_t{xf[ent.xbegin + x]} * 16);
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    a[e] = tile[sb ^ ((e & 1 ? t[0] : 0u) ^ (e & 2 ? t[1] : 0u) ^ (e & 4 ? t[2] : 0u) ^ (e & 8 ? t[3] : 0u))];
 }
 
 // Persistent over (shot, tile) units like tile_pass_body. FNT threads (256:

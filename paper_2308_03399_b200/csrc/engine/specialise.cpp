@@ -20,9 +20,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <filesystem>
+#include <algorithm>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "devprog.hpp"
@@ -254,39 +257,67 @@ std::map<std::string, GenericEntry> g_generic;
 
 }  // namespace
 
-// Compiles `source` with NVRTC (cached in-process and on disk) and returns
-// the named kernels, or an empty vector (and the log) on failure.
-std::vector<const void*> jit_compile_kernels(const std::string& source, const std::vector<std::string>& names,
-                                             std::string* log) {
-  std::lock_guard<std::mutex> lock(g_mu);
-  auto it = g_generic.find(source);
-  if (it == g_generic.end()) {
-    GenericEntry e;
-    const std::string cpath = generic_cache_path(source);
-    std::vector<char> cubin = read_file(cpath);
-    if (cubin.empty()) {
-      cubin = build_generic_cubin(source, log);
-      if (!cubin.empty()) write_file_atomic(cpath, cubin);
-    }
-    if (!cubin.empty() &&
-        cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess) {
-      for (const std::string& nm : names) {
-        cudaKernel_t k = nullptr;
-        if (cudaLibraryGetKernel(&k, e.lib, nm.c_str()) != cudaSuccess) {
-          cudaGetLastError();
-          e.kernels.clear();
-          if (log) *log = "kernel " + nm + " missing";
-          break;
-        }
-        e.kernels.push_back(k);
-      }
-    } else {
-      cudaGetLastError();
-    }
-    it = g_generic.emplace(source, std::move(e)).first;
+// Compiles each source with NVRTC (cached in-process and on disk; the
+// uncached ones concurrently, one host thread each up to the core count) and
+// returns per source the named kernels, or an empty vector on failure (the
+// first log in *log).
+std::vector<std::vector<const void*>> jit_compile_batch(const std::vector<std::string>& sources,
+                                                        const std::vector<std::vector<std::string>>& names,
+                                                        std::string* log) {
+  std::vector<std::vector<char>> cubins(sources.size());
+  std::vector<std::string> logs(sources.size());
+  std::vector<size_t> todo;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (size_t i = 0; i < sources.size(); ++i)
+      if (!g_generic.count(sources[i])) todo.push_back(i);
   }
-  std::vector<const void*> out;
-  for (cudaKernel_t k : it->second.kernels) out.push_back(reinterpret_cast<const void*>(k));
+  std::vector<size_t> build;
+  for (size_t i : todo) {
+    cubins[i] = read_file(generic_cache_path(sources[i]));
+    if (cubins[i].empty()) build.push_back(i);
+  }
+  if (!build.empty()) {
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(build.size(), std::thread::hardware_concurrency()));
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> pool;
+    for (size_t t = 0; t < nt; ++t)
+      pool.emplace_back([&] {
+        for (size_t j; (j = next.fetch_add(1)) < build.size();) {
+          const size_t i = build[j];
+          cubins[i] = build_generic_cubin(sources[i], &logs[i]);
+          if (!cubins[i].empty()) write_file_atomic(generic_cache_path(sources[i]), cubins[i]);
+        }
+      });
+    for (std::thread& t : pool) t.join();
+  }
+  std::lock_guard<std::mutex> lock(g_mu);
+  std::vector<std::vector<const void*>> out(sources.size());
+  for (size_t i = 0; i < sources.size(); ++i) {
+    auto it = g_generic.find(sources[i]);
+    if (it == g_generic.end()) {
+      GenericEntry e;
+      if (!cubins[i].empty() &&
+          cudaLibraryLoadData(&e.lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0) == cudaSuccess) {
+        for (const std::string& nm : names[i]) {
+          cudaKernel_t k = nullptr;
+          if (cudaLibraryGetKernel(&k, e.lib, nm.c_str()) != cudaSuccess) {
+            cudaGetLastError();
+            e.kernels.clear();
+            logs[i] = "kernel " + nm + " missing";
+            break;
+          }
+          e.kernels.push_back(k);
+        }
+      } else {
+        cudaGetLastError();
+        if (logs[i].empty()) logs[i] = "loading the fused cubin failed";
+      }
+      it = g_generic.emplace(sources[i], std::move(e)).first;
+    }
+    for (cudaKernel_t k : it->second.kernels) out[i].push_back(reinterpret_cast<const void*>(k));
+    if (log && log->empty() && !logs[i].empty()) *log = logs[i];
+  }
   return out;
 }
 

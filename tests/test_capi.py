@@ -58,6 +58,17 @@ def test_shape_specialisation_compiles_without_gpu(key, tile):
     assert prog.specialise_check(tile) > 0
 
 
+@pytest.mark.parametrize("key", ["C2", "C5"])
+def test_fused_specialisation_compiles_without_gpu(key):
+    """The per-pass specialised fused-matrix kernels (constant-bank block
+    products, straight-line groups) compile with NVRTC for sm_100a."""
+    from paper_2308_03399_b200 import Program, circuits as cc
+    cfg = cc.CONFIGS[key]
+    prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
+    info = prog.fused_info(12)
+    assert prog.fused_specialise_check() == info["passes"]
+
+
 @pytest.mark.gpu
 def test_integration_stub_runs_verbatim():
     """INTEGRATION.md §2's ctypes stub is executed as written (scripts/stub_check.py)."""

@@ -35,8 +35,11 @@ def prog_of(key, g):
     return Program.from_text(t, nz)
 
 
-@pytest.mark.parametrize("fused", [False, True])
-def test_c2_full_run(engine, fused):
+@pytest.mark.parametrize("mode", ["exact", "fused", "fused_jit"])
+def test_c2_full_run(engine, monkeypatch, mode):
+    fused = mode != "exact"
+    if mode == "fused_jit":  # the per-pass run-time specialised fused kernels
+        monkeypatch.setenv("SHOTSIM_B200_FUSED_JIT", "1")
     g = golden("scale_c2.json")
     want = np.frombuffer(gzip.decompress((GOLDEN / g["values_file"]).read_bytes()), dtype="<u2").astype(np.uint64)
     prog = prog_of("C2", g)
@@ -49,6 +52,8 @@ def test_c2_full_run(engine, fused):
     assert hex(counts_checksum_of_values(got, 16, True)[0]) == g["checksum"]
     if fused:
         assert r.fused_blocks > 0
+    if mode == "fused_jit":
+        assert r.specialised_shapes == r.fused_passes
 
 
 def test_c3_full_branch_run(engine):

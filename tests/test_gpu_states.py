@@ -68,22 +68,32 @@ def test_states_equal_reference(engine, ref, n, path):
         assert max(rel_err(g, w) for g, w in zip(r.states, want)) <= 1e-10
 
 
-@pytest.mark.parametrize("kernel", ["fma", "mma"])
+def fused_kernel_env(monkeypatch, kernel):
+    """fma: the static FMA build (default); mma: the tensor-core build;
+    jit: the per-pass run-time specialised FMA kernels (fused_jit.cpp)."""
+    if kernel == "mma":
+        monkeypatch.setenv("SHOTSIM_B200_FUSED_MMA", "1")
+    elif kernel == "jit":
+        monkeypatch.setenv("SHOTSIM_B200_FUSED_JIT", "1")
+
+
+@pytest.mark.parametrize("kernel", ["fma", "mma", "jit"])
 @pytest.mark.parametrize("n", [14, 16])
 def test_fused_states_within_bound(engine, ref, monkeypatch, n, kernel):
     """fused_matrices: amplitudes within 1e-10 relative of the reference."""
-    if kernel == "mma":
-        monkeypatch.setenv("SHOTSIM_B200_FUSED_MMA", "1")
+    fused_kernel_env(monkeypatch, kernel)
     circ, noise = programs(n)["qv_pauli"]
     want, _, _ = ref.batch_segments(circ, noise, list(range(IDS)), 11, n)
     r = engine.run_batch(Program.from_text(circ, noise),
                          RunOptions(shots=IDS, seed=11, export_states=True, fused_matrices=True))
     assert r.fused_blocks > 0
+    if kernel == "jit":
+        assert r.specialised_shapes == r.fused_passes
     errs = [rel_err(g, w) for g, w in zip(r.states, want)]
     assert max(errs) <= 1e-10, errs
 
 
-@pytest.mark.parametrize("kernel", ["fma", "mma"])
+@pytest.mark.parametrize("kernel", ["fma", "mma", "jit"])
 @pytest.mark.parametrize("scale", ["1", "1e5"])
 def test_fused_counts_equal_exact(engine, oracle, monkeypatch, scale, kernel):
     """fused_matrices gives the exact executor's (= the reference's) per-shot
@@ -91,12 +101,13 @@ def test_fused_counts_equal_exact(engine, oracle, monkeypatch, scale, kernel):
     shots falls inside it and is replayed through the exact executor — the
     replay path must give the same values."""
     monkeypatch.setenv("SHOTSIM_B200_GUARD_SCALE", scale)
-    if kernel == "mma":  # the tensor-core build of the fused pass
-        monkeypatch.setenv("SHOTSIM_B200_FUSED_MMA", "1")
+    fused_kernel_env(monkeypatch, kernel)
     prog = Program.from_text(cc.quantum_volume(14, depth=8, seed=3), cc.qv_noise())
     want = oracle.run_shots(prog, np.arange(400), 19, threads=8)
     r = engine.run_batch(prog, RunOptions(shots=400, seed=19, fused_matrices=True, record_shot_values=True))
     assert r.fused_blocks > 0
+    if kernel == "jit":
+        assert r.specialised_shapes == r.fused_passes
     assert (np.asarray(r.shot_values) == want).all()
     if scale != "1":
         assert 0 < r.guard_flagged < 400
