@@ -34,7 +34,7 @@ struct FEntry {
 __host__ __device__ inline uint64_t fused_smem_bytes(unsigned k, uint32_t max_blocks, uint32_t max_sites) {
   return (uint64_t{1} << k) * 16 + uint64_t{max_blocks} * 256 + uint64_t{kFusedSlots} * 256 +
          uint64_t{max_blocks} * (sizeof(FEntry) + sizeof(FGroup) + sizeof(FBlock)) + uint64_t{max_sites} * 4 +
-         (uint64_t{1} << (k - 7)) * 4 + 16;
+         (uint64_t{1} << (k - 7)) * 4 + 32;
 }
 
 __device__ __forceinline__ uint32_t ins0(uint32_t x, unsigned p) {
@@ -261,7 +261,8 @@ __device__ __forceinline__ void fused_pass_body(FusedView F, uint32_t pass_index
   FGroup* sgrp = reinterpret_cast<FGroup*>(ents + max_blocks);
   FBlock* sblk = reinterpret_cast<FBlock*>(sgrp + max_blocks);
   uint32_t* xf = reinterpret_cast<uint32_t*>(sblk + max_blocks);
-  uint32_t* hi_off = xf + max_sites;
+  // 16-byte aligned: the tile loops read four offsets per LDS.128
+  uint32_t* hi_off = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(xf + max_sites) + 15) & ~uintptr_t{15});
 
   for (uint32_t i = threadIdx.x; i < nb; i += FNT) {
     FBlock b = F.blocks[blk0 + i];
@@ -286,7 +287,7 @@ __device__ __forceinline__ void fused_pass_body(FusedView F, uint32_t pass_index
   const uint64_t units = S * tiles;
   const uint64_t u_begin = units * blockIdx.x / gridDim.x, u_end = units * (blockIdx.x + 1) / gridDim.x;
   const unsigned lane = threadIdx.x & 31;
-  const uint32_t hexads = L >> 4;
+  const uint32_t per = L / FNT;  // tile elements per thread
 
   for (uint64_t s = u_begin / tiles; s * tiles < u_end; ++s) {
     // ---- this shot's matrices (warp 0): M for blocks whose draws were all
@@ -348,33 +349,47 @@ __device__ __forceinline__ void fused_pass_body(FusedView F, uint32_t pass_index
         for (uint32_t l = threadIdx.x, i = 0; l < L; l += FNT, ++i)
           tile[swz(l)] = make_double2((origin && (lo_part | hi_off[i]) == 0) ? 1.0 : 0.0, 0.0);
       } else {
-        const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
-        for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * FNT, i0 += 8) {
-          uint32_t off[8];
+        // element threadIdx.x + FNT * i sits at swz(threadIdx.x) + FNT * i
+        // (FNT >= 64: the swizzle only mixes bits 3..5 into 0..2), and its
+        // global offset is lo_part + hi_off[i] (disjoint bits)
+        const uint32_t tile_s = static_cast<uint32_t>(__cvta_generic_to_shared(tile)) + 16u * swz(threadIdx.x);
+        const double2* tb = tbase + lo_part;
+        for (uint32_t i = 0; i < per; i += 4) {
+          const uint4 h = *reinterpret_cast<const uint4*>(hi_off + i);
+          const uint32_t o[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
-          for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * FNT < L ? hi_off[i0 + j] : 0u;
-#pragma unroll
-          for (uint32_t j = 0; j < 8; ++j)
-            if (l0 + j * FNT < L)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tile_s + 16 * swz(l0 + j * FNT)),
-                           "l"(tbase + (lo_part | off[j])));
+          for (uint32_t j = 0; j < 4; ++j)
+            if (i + j < per)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tile_s + 16u * FNT * (i + j)),
+                           "l"(tb + o[j]));
         }
-        if (t + 1 < t_end) {
-          const double2* nbase = seg + pdep_positions(t + 1, hpos, n - k);
-          for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * FNT, i0 += 8) {
-            uint32_t off[8];
+#ifndef SSB_FUSED_NO_PREFETCH
+        if (t + 1 < t_end) {  // the next tile's lines on their way to L2
+          const double2* nb = seg + pdep_positions(t + 1, hpos, n - k) + lo_part;
+          for (uint32_t i = 0; i < per; i += 4) {
+            const uint4 h = *reinterpret_cast<const uint4*>(hi_off + i);
+            const uint32_t o[4] = {h.x, h.y, h.z, h.w};
 #pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * FNT < L ? hi_off[i0 + j] : 0u;
-#pragma unroll
-            for (uint32_t j = 0; j < 8; ++j)
-              if (l0 + j * FNT < L) asm volatile("prefetch.global.L2 [%0];" ::"l"(nbase + (lo_part | off[j])));
+            for (uint32_t j = 0; j < 4; ++j)
+              if (i + j < per) asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + o[j]));
           }
         }
+#endif
         asm volatile("cp.async.wait_all;" ::: "memory");
       }
       __syncthreads();
       groups(tile, ents, sgrp, sblk, xf, ng, F);  // every block of the pass, group by group
-      for (uint32_t l = threadIdx.x, i = 0; l < L; l += FNT, ++i) tbase[lo_part | hi_off[i]] = tile[swz(l)];
+      {
+        double2* tb = tbase + lo_part;
+        const double2* ts = tile + swz(threadIdx.x);
+        for (uint32_t i = 0; i < per; i += 4) {
+          const uint4 h = *reinterpret_cast<const uint4*>(hi_off + i);
+          const uint32_t o[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+          for (uint32_t j = 0; j < 4; ++j)
+            if (i + j < per) tb[o[j]] = ts[FNT * (i + j)];
+        }
+      }
     }
     __syncthreads();  // the next shot's matrices rewrite slots / ents
   }
