@@ -237,15 +237,16 @@ struct RunResult {
   uint64_t seed = 0;
   unsigned workers = 1;
   std::vector<uint64_t> shot_values;
+  std::vector<unsigned> shard_devices;  // extension: per shot shard, the device that ran it
 };
 
 // ---- executors (exec.hpp:12-38) --------------------------------------------
 struct RunOptions {
   uint64_t shots = 1;
   uint64_t seed = 0;
-  unsigned workers = 1;          // shot shards (contiguous id ranges); shard g runs on
-                                 // device g % device_count — a performance hint only:
-                                 // results never depend on it (exec.hpp:24-27)
+  unsigned workers = 1;          // shot shards (contiguous id ranges), pulled by the
+                                 // devices as they become free — a performance hint
+                                 // only: results never depend on it (exec.hpp:24-27)
   uint64_t max_batch_size = 0;
   uint64_t branch_budget = 64;
   uint64_t mem_limit_bytes = 0;

@@ -19,6 +19,7 @@
 // registry — the reference's own run_bench (bench.cpp:122-130) and CLI —
 // then reaches the GPU executors unchanged (integration/dropin_main.cpp).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <map>
 #include <memory>
@@ -161,8 +162,9 @@ RunResult run_gpu(const NoisyCircuit& program, const RunOptions& o, bool branch)
   int ndev = 0;
   if (int rc = ssb_device_count(&ndev)) rethrow(rc);
 
-  // workers = shards of contiguous shot ids, shard g on device g % ndev
-  // (a performance hint: results never depend on it, exec.hpp:24-27).
+  // workers = shards of contiguous shot ids, pulled by the devices as they
+  // become free (a performance hint: results never depend on it,
+  // exec.hpp:24-27).
   const uint64_t G = std::min<uint64_t>(o.workers, o.shots);
   const unsigned D = static_cast<unsigned>(std::min<uint64_t>(G, static_cast<uint64_t>(ndev)));
   std::vector<uint64_t> begin(G + 1, 0);
@@ -173,12 +175,13 @@ RunResult run_gpu(const NoisyCircuit& program, const RunOptions& o, bool branch)
   std::vector<int> rcs(D, 0);
   std::vector<std::string> errs(D);
   std::vector<std::thread> threads;
+  std::atomic<uint64_t> next{0};
   for (unsigned d = 0; d < D; ++d)
     threads.emplace_back([&, d] {
       Pooled& pe = pooled(static_cast<int>(d));
       std::lock_guard<std::mutex> lk(pe.mu);
       if (!pe.engine) rcs[d] = ssb_engine_create(static_cast<int>(d), &pe.engine);
-      for (uint64_t g = d; rcs[d] == 0 && g < G; g += D) {
+      for (uint64_t g; rcs[d] == 0 && (g = next.fetch_add(1)) < G;) {
         ssb_run_options ro{};
         ro.max_batch_size = o.max_batch_size;
         ro.branch_budget = o.branch_budget;

@@ -2,11 +2,15 @@
 // "gpu-batch" / "gpu-branch" run the instrumented program on sm_100a through
 // the C ABI. RunOptions::workers keeps the reference's meaning of a
 // parallelism hint (exec.hpp:24-27: results never depend on it): the shots
-// split into min(workers, shots) contiguous shot-id shards and shard g runs on
-// device g % device_count, one host thread per device running its shards in
-// order on a pooled engine (engines — and their device buffers and programs
-// cache — persist across calls). Per-shard values are concatenated and folded
-// into Counts on the host (merge_counts is commutative, result.cpp:15-21).
+// split into min(workers, shots) contiguous shot-id shards, and one host thread
+// per device pulls the next pending shard from a shared counter whenever its
+// device is free (dynamic balancing: a device whose shards branch less or run
+// faster takes over the shards still waiting), each on a pooled engine
+// (engines — and their device buffers and programs cache — persist across
+// calls). Values are keyed by shot id, so where a shard runs never changes
+// them. Per-shard values are concatenated and folded into Counts on the host
+// (merge_counts is commutative, result.cpp:15-21).
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <map>
@@ -94,13 +98,17 @@ RunResult run_sharded(const NoisyCircuit& program, const RunOptions& o, RunFn fn
   const unsigned D = static_cast<unsigned>(std::min<uint64_t>(G, static_cast<uint64_t>(ndev)));  // devices used
   std::vector<int> rcs(D, 0);
   std::vector<std::string> errs(D);
+  std::vector<unsigned> shard_dev(G, 0);
+  std::atomic<uint64_t> next_shard{0};
+  std::atomic<bool> failed{false};
   std::vector<std::thread> pool;
   for (unsigned d = 0; d < D; ++d) {
     pool.emplace_back([&, d] {
       PooledEngine& pe = pooled_engine(static_cast<int>(d));
       std::lock_guard<std::mutex> lk(pe.mu);
       if (!pe.engine) rcs[d] = ssb_engine_create(static_cast<int>(d), &pe.engine);
-      for (uint64_t g = d; rcs[d] == 0 && g < G; g += D) {
+      for (uint64_t g; rcs[d] == 0 && !failed.load() && (g = next_shard.fetch_add(1)) < G;) {
+        shard_dev[g] = d;
         ssb_run_options so = ro;
         std::vector<uint64_t>& lv = leaves[g];
         if (o.collect_leaf_stats) {
@@ -118,7 +126,10 @@ RunResult run_sharded(const NoisyCircuit& program, const RunOptions& o, RunFn fn
         }
         if (rcs[d] == 0 && o.collect_leaf_stats) lv.resize(stats[g].num_leaves);
       }
-      if (rcs[d]) errs[d] = ssb_last_error();
+      if (rcs[d]) {
+        errs[d] = ssb_last_error();
+        failed = true;
+      }
     });
   }
   for (auto& t : pool) t.join();
@@ -135,11 +146,12 @@ RunResult run_sharded(const NoisyCircuit& program, const RunOptions& o, RunFn fn
   r.workers = o.workers;
   // Shards on one device run one after another: peak = the largest shard's
   // peak per device, summed over the devices running concurrently.
+  r.shard_devices.assign(shard_dev.begin(), shard_dev.end());
   std::vector<uint64_t> dev_peak(D, 0);
   for (uint64_t g = 0; g < G; ++g) {
     const ssb_stats& s = stats[g];
     r.dispatch_count += s.dispatch_count;
-    dev_peak[g % D] = std::max(dev_peak[g % D], s.peak_states);
+    dev_peak[shard_dev[g]] = std::max(dev_peak[shard_dev[g]], s.peak_states);
     r.branch.passes = std::max(r.branch.passes, s.passes);
     r.branch.leaf_shots.insert(r.branch.leaf_shots.end(), leaves[g].begin(), leaves[g].end());
   }

@@ -12,6 +12,15 @@ collective is the gather of the result — the reference's ``merge_counts``
 
 One process per GPU, ``torch.distributed`` for the plumbing; the histogram
 itself is built on the device by ``ssb_histogram_device``.
+
+Cross-GPU load balancing ("migrate ... waiting lists
+between GPUs"): instead of one static contiguous range per rank,
+``run_balanced`` cuts the run into shot-id chunks that the ranks pull from one
+atomic counter in the job's rendezvous store (``Store.add``). A rank whose
+chunks branch less, hit fewer guard replays or simply run on a less loaded GPU
+takes over the chunks still waiting; since every shot is keyed by its id the
+values never depend on where a chunk ran. The per-shot values are then merged
+with one all-reduce (each shot is written by exactly one rank).
 """
 
 from __future__ import annotations
@@ -102,3 +111,89 @@ def gather_counts(values, num_clbits: int, has_measure: bool, group=None) -> Dic
     if not has_measure:
         return {"": int(cnt.sum())}
     return {bitstring(int(u), num_clbits): int(c) for u, c in zip(uniq, cnt)}
+
+
+class ChunkQueue:
+    """Shot-id chunks [i * chunk, min((i + 1) * chunk, total)) handed out to
+    whichever rank asks next: ``Store.add(key, 1)`` is atomic across ranks, so
+    every chunk goes to exactly one rank. `key` must be fresh per run (the
+    counter is never reset)."""
+
+    def __init__(self, store, total: int, chunk: int, key: str):
+        if chunk < 1:
+            raise ValueError("chunk must be >= 1")
+        if total < 0:
+            raise ValueError("shots must be >= 0")
+        self.store, self.total, self.chunk, self.key = store, total, chunk, key
+
+    @property
+    def num_chunks(self) -> int:
+        return -(-self.total // self.chunk)
+
+    def next(self) -> Optional[Tuple[int, int]]:
+        i = int(self.store.add(self.key, 1)) - 1
+        begin = i * self.chunk
+        if begin >= self.total:
+            return None
+        return begin, min(self.chunk, self.total - begin)
+
+
+def default_store():
+    """The default process group's rendezvous store (the one torchrun or
+    init_process_group created)."""
+    import torch.distributed as dist
+    return dist.distributed_c10d._get_default_store()
+
+
+_RUN_SEQ = [0]
+
+
+def run_balanced(run_chunk, total: int, chunk: int, store=None, key: Optional[str] = None, group=None):
+    """Runs `total` shots in chunks pulled dynamically by the ranks.
+    ``run_chunk(begin, count)`` returns the chunk's per-shot values (array-like
+    of non-negative ints). Returns ``(values, mine)``: every shot's value on
+    every rank (int64 numpy, shot-id order) and the chunks this rank ran.
+    Single process (no process group): all chunks run locally."""
+    import torch
+    import torch.distributed as dist
+    distributed = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    if key is None:  # the same sequence number on every rank: runs are collective
+        _RUN_SEQ[0] += 1
+        key = f"ssb_balanced_{_RUN_SEQ[0]}"
+    if distributed:
+        q = ChunkQueue(store if store is not None else default_store(), total, chunk, key)
+    else:
+        q = ChunkQueue(_LocalStore(), total, chunk, key)
+    vals = np.zeros(total, dtype=np.int64)
+    seen = np.zeros(total, dtype=np.int32)
+    mine = []
+    while True:
+        c = q.next()
+        if c is None:
+            break
+        b, n = c
+        v = np.asarray(run_chunk(b, n), dtype=np.int64)
+        if v.shape != (n,):
+            raise ValueError("run_chunk returned the wrong number of values")
+        vals[b:b + n] = v
+        seen[b:b + n] += 1
+        mine.append(c)
+    if distributed:
+        tv, ts = torch.from_numpy(vals), torch.from_numpy(seen)
+        dist.all_reduce(tv, group=group)
+        dist.all_reduce(ts, group=group)
+        vals, seen = tv.numpy(), ts.numpy()
+    if total and not (seen == 1).all():
+        raise RuntimeError("chunk schedule did not cover every shot exactly once")
+    return vals, mine
+
+
+class _LocalStore:
+    """Counter with Store.add semantics for the single-process case."""
+
+    def __init__(self):
+        self._v = {}
+
+    def add(self, key, n):
+        self._v[key] = self._v.get(key, 0) + n
+        return self._v[key]

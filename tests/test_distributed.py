@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 
 from paper_2308_03399_b200 import Program, circuits as cc
 from paper_2308_03399_b200.api import counts_from_values
-from paper_2308_03399_b200.distributed import gather_counts, shard_range, weak_range
+from paper_2308_03399_b200.distributed import ChunkQueue, gather_counts, run_balanced, shard_range, weak_range
 
 
 def _free_port():
@@ -117,3 +117,97 @@ def test_bench_two_ranks_under_torchrun():
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["config"]["global_shots_per_step"] == 4096 and line["value"] > 0
+
+
+def _balanced_worker(rank, world, port, circ, noise, shots, seed, chunk, slow_rank, out):
+    """One rank of a dynamically balanced run: chunks pulled from the store's
+    counter; `slow_rank` sleeps per chunk (a loaded / slower GPU), so the
+    other rank must take over the waiting chunks."""
+    import time
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        prog = Program.from_text(circ, noise)
+        orc = Oracle()
+
+        def run_chunk(b, n):
+            if rank == slow_rank:
+                time.sleep(0.3)
+            return orc.run_shots(prog, np.arange(b, b + n), seed)
+
+        vals, mine = run_balanced(run_chunk, shots, chunk)
+        out[rank] = (vals.tolist(), mine)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_chunk_queue_hands_out_each_chunk_once():
+    class S:
+        v = 0
+
+        def add(self, k, n):
+            S.v += n
+            return S.v
+    q = ChunkQueue(S(), 10, 4, "k")
+    got = []
+    while (c := q.next()) is not None:
+        got.append(c)
+    assert got == [(0, 4), (4, 4), (8, 2)] and q.num_chunks == 3
+    assert ChunkQueue(S(), 0, 4, "z").num_chunks == 0
+    with pytest.raises(ValueError):
+        ChunkQueue(S(), 10, 0, "k")
+
+
+def test_balanced_two_ranks_equal_single_run_and_shift_work():
+    """Cross-rank load balancing (run_balanced): two gloo ranks pull shot
+    chunks from one counter; the slow rank ends up with fewer chunks, and the
+    merged per-shot values equal the single run's exactly."""
+    circ, noise = cc.ghz(5), cc.depolarizing_model(0.05)
+    shots, seed, chunk = 240, 3, 20
+    from oracle.oracle import Oracle
+    want = Oracle().run_shots(Program.from_text(circ, noise), np.arange(shots), seed)
+    out = mp.Manager().dict()
+    mp.spawn(_balanced_worker, args=(2, _free_port(), circ, noise, shots, seed, chunk, 1, out), nprocs=2,
+             join=True)
+    for r in (0, 1):
+        assert out[r][0] == want.astype(np.int64).tolist()
+    c0, c1 = out[0][1], out[1][1]
+    assert sorted(c0 + c1) == [(b, chunk) for b in range(0, shots, chunk)]
+    assert len(c0) > len(c1) >= 1
+
+
+def _balanced_engine_worker(rank, world, port, circ, noise, shots, seed, chunk, budget, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2308_03399_b200 import Engine, RunOptions
+        eng = Engine(0)
+        prog = Program.from_text(circ, noise)
+
+        def run_chunk(b, n):
+            r = eng.run_branch(prog, RunOptions(shots=n, seed=seed, branch_budget=budget, record_shot_values=True),
+                               shot_begin=b)
+            return np.asarray(r.shot_values)
+
+        vals, mine = run_balanced(run_chunk, shots, chunk)
+        out[rank] = (vals.tolist(), mine)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_balanced_branch_two_ranks_equal_single_run():
+    """gpu-branch under the cross-rank chunk balancer (two ranks sharing the
+    box's GPU): the merged values equal one run_branch over all shots."""
+    from paper_2308_03399_b200 import Engine, RunOptions
+    circ, noise = cc.dynamic(10, rounds=3), cc.thermal_noise(0.02, 0.05)
+    shots, seed, chunk, budget = 6000, 9, 500, 64
+    want = Engine(0).run_branch(Program.from_text(circ, noise),
+                                RunOptions(shots=shots, seed=seed, branch_budget=budget, record_shot_values=True))
+    out = mp.Manager().dict()
+    mp.spawn(_balanced_engine_worker, args=(2, _free_port(), circ, noise, shots, seed, chunk, budget, out), nprocs=2,
+             join=True)
+    for r in (0, 1):
+        assert out[r][0] == np.asarray(want.shot_values).astype(np.int64).tolist()
+    assert sorted(out[0][1] + out[1][1]) == [(b, chunk) for b in range(0, shots, chunk)]
