@@ -75,6 +75,12 @@ __device__ __forceinline__ ExactPick warp_exact_scan(Prob prob, uint64_t count, 
         start = b + 1;
         continue;
       }
+      if (!(nz & live)) {
+        // only zeros left in this chunk: fl(S + 0) = S for every lane, and
+        // u < S was already ruled out when S was reached
+        if (m < count && lane >= start) on_sum(m, S);
+        break;
+      }
       int e = 0;
       frexp(S, &e);
       const double w = ldexp(1.0, e - 53);

@@ -262,7 +262,8 @@ __device__ __forceinline__ void fused_pass_body(FusedView F, uint32_t pass_index
   FBlock* sblk = reinterpret_cast<FBlock*>(sgrp + max_blocks);
   uint32_t* xf = reinterpret_cast<uint32_t*>(sblk + max_blocks);
   // 16-byte aligned: the tile loops read four offsets per LDS.128
-  uint32_t* hi_off = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(xf + max_sites) + 15) & ~uintptr_t{15});
+  uint32_t* hi_off =
+      reinterpret_cast<uint32_t*>((reinterpret_cast<unsigned long long>(xf + max_sites) + 15) & ~15ull);
 
   for (uint32_t i = threadIdx.x; i < nb; i += FNT) {
     FBlock b = F.blocks[blk0 + i];

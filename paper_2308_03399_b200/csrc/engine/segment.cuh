@@ -421,20 +421,33 @@ static __device__ __forceinline__ void run_segment_staged_t(double2* st, unsigne
       // Hot inner loop: consecutive 1q U micro-ops on the six register-pair
       // layouts a CX / SWAP relabeling produces (QV: 8 of 11 block ops). It
       // has a single loop-carried path, so the quad registers stay put.
+      // All-real 1q gates (H, RY, ...: the reference's real-matrix kernel
+      // class) take the same path with their own arithmetic.
       for (; i < end; ++i) {
         const Uop u = eops[i];
-        if (u.code != UC_U) break;
+        if (u.code != UC_U && u.code != UC_REAL) break;
         const double2* m = smats + u.mat;
         const double2 mm[4] = {m[0], m[1], m[2], m[3]};
         bool hit = true;
 #define SSB_P1(a0, a1, b0, b1) \
   case (a0 | (a1 << 2) | (b0 << 4) | (b1 << 6)): quad_apply1p<a0, a1, b0, b1, MK_1Q_U, FULL>(v, mm, 0, nq); break;
-        switch (u.qb) {
-          SSB_P1(0, 1, 2, 3) SSB_P1(0, 2, 1, 3) SSB_P1(0, 3, 2, 1) SSB_P1(0, 2, 3, 1) SSB_P1(0, 1, 3, 2)
-          SSB_P1(0, 3, 1, 2)
-          default: hit = false; break;
+#define SSB_P1R(a0, a1, b0, b1) \
+  case (a0 | (a1 << 2) | (b0 << 4) | (b1 << 6)): quad_apply1p<a0, a1, b0, b1, MK_1Q_REAL, FULL>(v, mm, 0, nq); break;
+        if (u.code == UC_U) {
+          switch (u.qb) {
+            SSB_P1(0, 1, 2, 3) SSB_P1(0, 2, 1, 3) SSB_P1(0, 3, 2, 1) SSB_P1(0, 2, 3, 1) SSB_P1(0, 1, 3, 2)
+            SSB_P1(0, 3, 1, 2)
+            default: hit = false; break;
+          }
+        } else {
+          switch (u.qb) {
+            SSB_P1R(0, 1, 2, 3) SSB_P1R(0, 2, 1, 3) SSB_P1R(0, 3, 2, 1) SSB_P1R(0, 2, 3, 1) SSB_P1R(0, 1, 3, 2)
+            SSB_P1R(0, 3, 1, 2)
+            default: hit = false; break;
+          }
         }
 #undef SSB_P1
+#undef SSB_P1R
         if (!hit) break;
       }
       if (i >= end) break;
@@ -480,21 +493,21 @@ static __device__ __forceinline__ void run_segment_staged_t(double2* st, unsigne
         scatter_logical(v[q], u.sigma, L);
       }
     }
+    // The segment's relabeling: logical element e sits in register slot
+    // sigma(e), so slot p is stored at the offset of e = sigma^-1(p) (the
+    // permutation goes into four uniform offsets instead of a run-time
+    // register index per element).
     const uint8_t sg = it.sigma;
+    const uint64_t offe[4] = {0, dla, dlb, dla | dlb};
+    uint64_t offp[4];
+#pragma unroll
+    for (uint32_t p = 0; p < 4; ++p)
+      offp[p] = sig(sg, 0) == p ? offe[0] : sig(sg, 1) == p ? offe[1] : sig(sg, 2) == p ? offe[2] : offe[3];
 #pragma unroll
     for (int q = 0; q < QPT; ++q) {
       if (FULL || q < nq) {
-        double2 L[4];
-        if (sg == 0xE4) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) L[e] = v[q][e];
-        } else {
-          gather_logical(v[q], sg, L);
-        }
-        st[base[q]] = L[0];
-        st[base[q] | dla] = L[1];
-        st[base[q] | dlb] = L[2];
-        st[base[q] | dla | dlb] = L[3];
+        for (int p = 0; p < 4; ++p) st[base[q] | offp[p]] = v[q][p];
       }
     }
   }
