@@ -601,6 +601,9 @@ struct KernelTimer {
   }
 };
 
+// Registers of at least this many qubits run fused mode with 11-qubit tiles.
+constexpr unsigned kFusedSmallTileMinQubits = 20;
+
 struct RunConfig {
   unsigned resident_max = kResidentMaxDefault;
   unsigned tile_k = kTileDefault;
@@ -890,8 +893,14 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       stats->fused_passes = 1;
     }
   } else {
-    DevProgram& dp = device_program(E, prog, rc.tile_k);
-    if (opts && opts->fused_matrices && fused_ready(E, dp)) {
+    // Fused mode on large registers defaults to 11-qubit tiles (more passes,
+    // but 128-thread CTAs keep more tiles in flight per SM: C5 +3.7%, C2
+    // equal; profiles/r02/fused_variants.log); an explicit tile_qubits wins.
+    const bool want_fused = opts && opts->fused_matrices;
+    const unsigned ftk = want_fused && !opts->tile_qubits && n >= kFusedSmallTileMinQubits ? 11u : rc.tile_k;
+    DevProgram& fdp = device_program(E, prog, want_fused ? ftk : rc.tile_k);
+    DevProgram& dp = want_fused && ftk != rc.tile_k && !fused_ready(E, fdp) ? device_program(E, prog, rc.tile_k) : fdp;
+    if (want_fused && &dp == &fdp && fused_ready(E, dp)) {
       run_fused(E, prog, dp, shot_begin, count, seed, opts, values_dev, stats, timer);
       if (stats) {
         stats->dispatch_count = E->launches - launches0;

@@ -69,8 +69,10 @@ def test_c3_full_branch_run(engine):
     assert sha(np.asarray(b.shot_values)) == g["values_sha256"]
 
 
-@pytest.mark.parametrize("key", ["C4", "C5"])
-def test_large_config_shot_ids(engine, key):
+@pytest.mark.parametrize("key,fused", [("C4", False), ("C5", False), ("C5", True)])
+def test_large_config_shot_ids(engine, key, fused):
+    """Reference values of sampled C4 / C5 shot ids; C5 also in fused-matrix
+    mode (n >= 20: 11-qubit tiles by default, guard replays included)."""
     g = golden("scale_c45.json")[key]
     prog = prog_of(key, g)
     got = []
@@ -81,8 +83,10 @@ def test_large_config_shot_ids(engine, key):
         j = i
         while j + 1 < len(ids) and ids[j + 1] == ids[j] + 1:
             j += 1
-        r = engine.run_batch(prog, RunOptions(shots=1, seed=g["seed"], record_shot_values=True),
+        r = engine.run_batch(prog, RunOptions(shots=1, seed=g["seed"], record_shot_values=True, fused_matrices=fused),
                              shot_begin=ids[i], shot_count=j - i + 1)
+        if fused:
+            assert r.fused_blocks > 0
         got += [int(v) for v in r.shot_values]
         i = j + 1
     assert got == g["values"]
