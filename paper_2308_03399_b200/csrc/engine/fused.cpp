@@ -248,28 +248,74 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
     // predecessors in the pass are applied, then add every ready block whose
     // qubits keep the group within four local positions (blocks sharing a
     // qubit keep their order; disjoint ones commute).
+    const char* gv = std::getenv("SHOTSIM_B200_FUSED_GREEDY");
+    const bool greedy_groups = gv && *gv && *gv != '0';
     pd.grp_begin = static_cast<uint32_t>(f.groups.size());
     pd.blk_begin = static_cast<uint32_t>(f.blocks.size());
     std::vector<char> placed(taken.size(), 0);
     size_t nplaced = 0;
     uint32_t sites_in_pass = 0;
+    auto qmask = [&](size_t t) { return (1u << blks[taken[t]].q0) | (1u << blks[taken[t]].q1); };
+    // The blocks one group starting from qubit set gm0 would take (in order):
+    // every block whose earlier unplaced blocks share none of its qubits and
+    // whose qubits keep the group within gq, rescanned until nothing grows.
+    auto closure = [&](uint32_t gm0, std::vector<char> pl, std::vector<size_t>* order) {
+      uint32_t gm = gm0;
+      size_t cnt = 0;
+      for (bool grew = true; grew;) {
+        grew = false;
+        uint32_t pending_q = 0;
+        for (size_t t = 0; t < taken.size(); ++t) {
+          if (pl[t]) continue;
+          const uint32_t qm = qmask(t);
+          if (!(qm & pending_q) && std::popcount(gm | qm) <= static_cast<int>(gq)) {
+            gm |= qm;
+            pl[t] = 1;
+            ++cnt;
+            grew = true;
+            if (order) order->push_back(t);
+          } else {
+            pending_q |= qm;
+          }
+        }
+      }
+      return cnt;
+    };
     while (nplaced < taken.size()) {
+      // Seed: the qubit set (the union of one or two ready blocks) whose
+      // closure takes the most blocks — a greedy first-fit seed often closes
+      // the group after two blocks (SHOTSIM_B200_FUSED_GREEDY=1 keeps it).
+      uint32_t seed_q = 0;
+      if (!greedy_groups) {
+        std::vector<size_t> ready;
+        uint32_t pq = 0;
+        for (size_t t = 0; t < taken.size(); ++t) {
+          if (placed[t]) continue;
+          if (!(qmask(t) & pq)) ready.push_back(t);
+          pq |= qmask(t);
+        }
+        size_t best = 0;
+        for (size_t a = 0; a < ready.size(); ++a)
+          for (size_t c = a; c < ready.size(); ++c) {
+            const uint32_t q = qmask(ready[a]) | qmask(ready[c]);
+            if (std::popcount(q) > static_cast<int>(gq)) continue;
+            const size_t got = closure(q, placed, nullptr);
+            if (got > best) best = got, seed_q = q;
+          }
+      }
+      std::vector<size_t> order;
+      closure(seed_q, placed, &order);
       uint32_t gm = 0;  // group qubit mask
       FGroup g{};
       g.blk_begin = static_cast<uint32_t>(f.blocks.size());
-      bool grew = true;
-      while (grew) {
-        grew = false;
-        uint32_t pending_q = 0;  // qubits of earlier unplaced blocks (order constraint)
-        for (size_t t = 0; t < taken.size(); ++t) {
-          if (placed[t]) continue;
+      {
+        for (size_t t : order) {
           const uint32_t b = taken[t];
-          const uint32_t qm = (1u << blks[b].q0) | (1u << blks[b].q1);
-          if (!(qm & pending_q) && std::popcount(gm | qm) <= static_cast<int>(gq)) {
+          const uint32_t qm = qmask(t);
+          {
             gm |= qm;
             placed[t] = 1;
             ++nplaced;
-            grew = true;
             FBlock fb{};
             fb.p0 = pos[blks[b].q0];
             fb.p1 = pos[blks[b].q1];
@@ -278,8 +324,6 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
             fb.site_end = site_range[b].second;
             sites_in_pass += fb.site_end - fb.site_begin;
             f.blocks.push_back(fb);
-          } else {
-            pending_q |= qm;
           }
         }
       }
