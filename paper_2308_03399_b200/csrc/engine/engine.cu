@@ -601,8 +601,10 @@ struct KernelTimer {
   }
 };
 
-// Registers of at least this many qubits run fused mode with 11-qubit tiles.
-constexpr unsigned kFusedSmallTileMinQubits = 20;
+// Registers of at least this many qubits run fused mode with 11-qubit tiles
+// (with the local-set search of plan_fused: C2 71.5k vs 68.5k shots/s at 12,
+// C5 102.7 vs 97.8; profiles/r02/fused_variants.log).
+constexpr unsigned kFusedSmallTileMinQubits = 12;
 
 struct RunConfig {
   unsigned resident_max = kResidentMaxDefault;
@@ -893,9 +895,8 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       stats->fused_passes = 1;
     }
   } else {
-    // Fused mode on large registers defaults to 11-qubit tiles (more passes,
-    // but 128-thread CTAs keep more tiles in flight per SM: C5 +3.7%, C2
-    // equal; profiles/r02/fused_variants.log); an explicit tile_qubits wins.
+    // Fused mode defaults to 11-qubit tiles (more passes, but 128-thread CTAs
+    // keep more tiles in flight per SM); an explicit tile_qubits wins.
     const bool want_fused = opts && opts->fused_matrices;
     const unsigned ftk = want_fused && !opts->tile_qubits && n >= kFusedSmallTileMinQubits ? 11u : rc.tile_k;
     DevProgram& fdp = device_program(E, prog, want_fused ? ftk : rc.tile_k);

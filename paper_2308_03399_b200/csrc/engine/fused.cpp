@@ -213,6 +213,27 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
   std::vector<uint32_t> remaining(blks.size());
   for (uint32_t i = 0; i < remaining.size(); ++i) remaining[i] = i;
   bool first = true;
+  // Blocks a pass with the fixed local set L takes from `remaining` (in
+  // order; a block is blocked once an earlier untaken block shares a qubit).
+  auto take_with = [&](uint32_t L, std::vector<uint32_t>* taken, std::vector<uint32_t>* rest) {
+    uint32_t blocked = 0;
+    size_t cnt = 0;
+    for (size_t r = 0; r < remaining.size(); ++r) {
+      const uint32_t b = remaining[r];
+      const uint32_t qm = (1u << blks[b].q0) | (1u << blks[b].q1);
+      if (!(qm & blocked) && (qm & ~L) == 0 && cnt < cap) {
+        ++cnt;
+        if (taken) taken->push_back(b);
+      } else {
+        blocked |= qm;
+        if (rest) rest->push_back(b);
+      }
+      if (blocked == all && !rest) break;
+    }
+    return cnt;
+  };
+  const char* pv = std::getenv("SHOTSIM_B200_FUSED_GREEDY_PASSES");
+  const bool greedy_passes = pv && *pv && *pv != '0';
   while (first || !remaining.empty()) {
     uint32_t L = low, blocked = 0;
     std::vector<uint32_t> taken, rest;
@@ -231,8 +252,29 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
         break;
       }
     }
-    remaining.swap(rest);
     for (unsigned q = 0; q < n && static_cast<unsigned>(std::popcount(L)) < k; ++q) L |= 1u << q;
+    // Local-set search: from the first-fit set, swap one non-forced local
+    // qubit for a non-local one while that lets the pass take more blocks
+    // (fewer passes = fewer HBM sweeps and tile IO phases).
+    if (!greedy_passes && k < n) {
+      size_t best = take_with(L, nullptr, nullptr);
+      for (bool improved = true; improved;) {
+        improved = false;
+        for (unsigned qi = 0; qi < n && !improved; ++qi) {
+          if (!(L >> qi & 1) || (low >> qi & 1)) continue;
+          for (unsigned qo = 0; qo < n && !improved; ++qo) {
+            if (L >> qo & 1) continue;
+            const uint32_t L2 = (L & ~(1u << qi)) | (1u << qo);
+            const size_t got = take_with(L2, nullptr, nullptr);
+            if (got > best) best = got, L = L2, improved = true;
+          }
+        }
+      }
+      taken.clear();
+      rest.clear();
+      take_with(L, &taken, &rest);
+    }
+    remaining.swap(rest);
     FPass pd{};
     pd.lmask = L;
     pd.k = static_cast<uint8_t>(k);
