@@ -254,7 +254,7 @@ SSB_API int ssb_histogram_device(ssb_engine* engine, const uint64_t* values_devi
 SSB_API int ssb_program_specialise_check(const ssb_program* program, uint32_t tile_qubits, uint32_t* shapes);
 
 /* Plans `program` in fused-matrix mode (ssb_run_options::fused_matrices,
- * 12-qubit tiles) and compiles its per-pass specialised fused kernels with
+ * 11-qubit tiles, its default) and compiles its per-pass specialised fused kernels with
  * NVRTC for sm_100a without loading them (no GPU needed). *kernels receives
  * the number of specialised passes; on failure the NVRTC log is in
  * ssb_last_error(). */

@@ -145,7 +145,7 @@ extern "C" SSB_API int ssb_program_specialise_check(const ssb_program* program, 
 extern "C" SSB_API int ssb_program_fused_specialise_check(const ssb_program* program, uint32_t* kernels) {
   return ssb::guard([&] {
     if (!program || !kernels) throw std::invalid_argument("null argument");
-    const ssb::FusedPlan f = ssb::plan_fused(program->dev, 12u);
+    const ssb::FusedPlan f = ssb::plan_fused(program->dev, 11u);  // the fused mode's default tile
     if (!f.ok) throw std::invalid_argument("no fused-matrix plan: " + f.why);
     uint32_t n = 0;
     for (const auto& m : ssb::fused_jit_sources(f)) n += static_cast<uint32_t>(m.second.size());

@@ -764,7 +764,8 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
   // SHOTSIM_B200_FUSED_JIT=1: the per-pass specialised kernels (fused_jit.cpp)
   // for the passes that have one (same arithmetic, constant-bank products).
   const char* jit_env = std::getenv("SHOTSIM_B200_FUSED_JIT");
-  const bool use_jit = !use_mma && !use_db && f.gq == 4 && fnt == 256 && jit_env && *jit_env && *jit_env != '0';
+  const bool use_jit = !use_mma && !use_db && f.gq == 4 && (f.k == 11 || f.k == 12) && jit_env && *jit_env &&
+                       *jit_env != '0';
   if (use_jit && !dp.fjit_tried) {
     dp.fjit_tried = true;
     std::string log;

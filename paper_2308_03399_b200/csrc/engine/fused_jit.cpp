@@ -11,8 +11,8 @@
 // (its entry points at a per-shot product slot, or carries extra factors)
 // takes the generic path, the same arithmetic as the static kernel.
 //
-// Only 12-qubit tiles with 4-qubit register groups (one hexad per thread,
-// 256 threads) are specialised; other passes keep the static kernel.
+// 11- and 12-qubit tiles with 4-qubit register groups (one hexad per thread:
+// 128 / 256 threads) are specialised; other passes keep the static kernel.
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -32,7 +32,6 @@ bool jit_compile_check(const std::string& source, std::string* log);
 
 namespace {
 
-constexpr unsigned kJitK = 12;
 // __constant__ bytes per module (the bank holds 64 KB; keep headroom).
 constexpr size_t kConstBudget = 48 * 1024;
 // Passes per NVRTC module (modules compile concurrently).
@@ -47,12 +46,12 @@ std::string hexd(double v) {
 }
 
 bool pass_ok(const FusedPlan& f, const FPass& P) {
-  if (P.k != kJitK) return false;
+  if (P.k != f.k || (f.k != 11 && f.k != 12)) return false;
   for (uint32_t b = P.blk_begin; b < P.blk_end; ++b)
     if (f.blocks[b].gb0 >= f.blocks[b].gb1 || f.blocks[b].gb1 > 3) return false;
   for (uint32_t g = P.grp_begin; g < P.grp_end; ++g)
     for (int i = 0; i < 4; ++i)
-      if (f.groups[g].g[i] >= kJitK || (i && f.groups[g].g[i] <= f.groups[g].g[i - 1])) return false;
+      if (f.groups[g].g[i] >= P.k || (i && f.groups[g].g[i] <= f.groups[g].g[i - 1])) return false;
   return true;
 }
 
@@ -94,7 +93,7 @@ void emit_pass(std::string& s, const FusedPlan& f, uint32_t p) {
       const uint32_t lb = b - P.blk_begin;
       const FBlock& B = f.blocks[b];
       s += "      jit_block<" + std::to_string(B.gb0) + ", " + std::to_string(B.gb1) + ">(a, ents[" + std::to_string(lb) +
-           "], " + std::to_string((1u << kJitK) + lb * 16) + "u, ssb_cm_" + id + " + " + std::to_string(lb * 16) +
+           "], " + std::to_string((1u << P.k) + lb * 16) + "u, ssb_cm_" + id + " + " + std::to_string(lb * 16) +
            ", tile, sb, t, xf, F);\n";
     }
     for (unsigned e = 0; e < 16; ++e) s += "      tile[sb ^ " + go[e] + "] = a[" + std::to_string(e) + "];\n";
@@ -102,18 +101,21 @@ void emit_pass(std::string& s, const FusedPlan& f, uint32_t p) {
   }
   s += "  }\n};\n";
   s += "}  // namespace ssb\n"
-       "extern \"C\" __global__ void __launch_bounds__(256, SSB_FUSED_JIT_MINB)\n"
+       "extern \"C\" __global__ void __launch_bounds__(SSB_FUSED_JIT_NT, SSB_FUSED_JIT_MINB)\n"
        "ssb_fused_" + id + "(ssb::FusedView F, uint32_t pass_index, double2* state, uint64_t S,\n"
        "    const uint8_t* pauli_sel, uint32_t num_pauli, uint32_t max_blocks, uint32_t max_sites) {\n"
-       "  ssb::fused_pass_body<256, 4>(F, pass_index, state, S, pauli_sel, num_pauli, max_blocks, max_sites,\n"
+       "  ssb::fused_pass_body<SSB_FUSED_JIT_NT, 4>(F, pass_index, state, S, pauli_sel, num_pauli, max_blocks,\n"
+       "                                         max_sites,\n"
        "                               ssb::SsbGroups" + id + "{});\n"
        "}\n"
        "namespace ssb {\n";
 }
 
-unsigned jit_minb() {
+// CTAs per SM the register allocation must allow: 128 registers per thread
+// (the static build's budget), SHOTSIM_B200_FUSED_JIT_MINB overrides.
+unsigned jit_minb(unsigned nt) {
   const char* v = std::getenv("SHOTSIM_B200_FUSED_JIT_MINB");
-  return v && *v >= '1' && *v <= '4' ? unsigned(*v - '0') : 2u;
+  return v && *v >= '1' && *v <= '8' ? unsigned(*v - '0') : 512u / nt;
 }
 
 }  // namespace
@@ -122,9 +124,11 @@ unsigned jit_minb() {
 // within kConstBudget. mods[i] = (source, pass ids).
 std::vector<std::pair<std::string, std::vector<uint32_t>>> fused_jit_sources(const FusedPlan& f) {
   std::vector<std::pair<std::string, std::vector<uint32_t>>> mods;
-  if (!f.ok || f.gq != 4 || f.k != kJitK) return mods;
-  const std::string head = "// shotsim_b200 fused-pass specialisation v2\n#define SSB_FUSED_JIT_MINB " +
-                           std::to_string(jit_minb()) + "\n#include \"fused_body.cuh\"\nnamespace ssb {\n";
+  if (!f.ok || f.gq != 4 || (f.k != 11 && f.k != 12)) return mods;
+  const unsigned nt = 1u << (f.k - 4);  // one hexad per thread
+  const std::string head = "// shotsim_b200 fused-pass specialisation v3\n#define SSB_FUSED_JIT_NT " +
+                           std::to_string(nt) + "\n#define SSB_FUSED_JIT_MINB " + std::to_string(jit_minb(nt)) +
+                           "\n#include \"fused_body.cuh\"\nnamespace ssb {\n";
   std::string cur;
   std::vector<uint32_t> ids;
   size_t bytes = 0;

@@ -65,7 +65,7 @@ def test_fused_specialisation_compiles_without_gpu(key):
     from paper_2308_03399_b200 import Program, circuits as cc
     cfg = cc.CONFIGS[key]
     prog = Program.from_text(cfg["circuit"](), cfg["noise"]())
-    info = prog.fused_info(12)
+    info = prog.fused_info(11)  # fused mode's default tile
     assert prog.fused_specialise_check() == info["passes"]
 
 
