@@ -39,6 +39,11 @@ def warp_scan(p, u, record):
                 if c0+b < count: record[c0+b] = Sn
                 if u < Sn and c0+b < count: return ('cross', c0+b)
                 S = Sn; start = b+1; continue
+            if not any(nz[l] for l in range(start,32)):
+                # only zeros left in this chunk: S stays
+                for l in range(start,32):
+                    if m[l] < count: record[m[l]] = S
+                break
             e = frexp_e(S); w = math.ldexp(1.0, e-53); a0 = int(S/w)
             k = [0]*32; bad=[False]*32
             for l in range(start,32):
@@ -121,3 +126,4 @@ def test_dyadic_ties_and_binades():
         rec = [None] * len(p)
         warp_scan(p, float("inf"), rec)
         assert rec == seq(p, 0)
+
