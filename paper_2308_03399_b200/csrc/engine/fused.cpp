@@ -270,6 +270,30 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
           }
         }
       }
+      // Small registers: the best local set outright (all subsets of the
+      // non-forced qubits, when there are at most ~20k of them).
+      const unsigned free_q = n - static_cast<unsigned>(std::popcount(low));
+      const unsigned pick = k - static_cast<unsigned>(std::popcount(low));
+      double combos = 1.0;
+      for (unsigned i = 0; i < pick; ++i) combos = combos * (free_q - i) / (i + 1);
+      if (combos <= 20000.0 && std::getenv("SHOTSIM_B200_FUSED_NO_EXHAUSTIVE") == nullptr) {
+        std::vector<unsigned> fq;
+        for (unsigned q = 0; q < n; ++q)
+          if (!(low >> q & 1)) fq.push_back(q);
+        std::vector<unsigned> idx(pick);
+        for (unsigned i = 0; i < pick; ++i) idx[i] = i;
+        while (true) {
+          uint32_t L2 = low;
+          for (unsigned i : idx) L2 |= 1u << fq[i];
+          const size_t got = take_with(L2, nullptr, nullptr);
+          if (got > best) best = got, L = L2;
+          int i = static_cast<int>(pick) - 1;  // next combination
+          while (i >= 0 && idx[i] == fq.size() - pick + i) --i;
+          if (i < 0) break;
+          ++idx[i];
+          for (unsigned j = i + 1; j < pick; ++j) idx[j] = idx[j - 1] + 1;
+        }
+      }
       taken.clear();
       rest.clear();
       take_with(L, &taken, &rest);
