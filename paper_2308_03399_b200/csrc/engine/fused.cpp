@@ -232,6 +232,10 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
     }
     return cnt;
   };
+  // One-pass lookahead in the exhaustive local-set search (default on;
+  // SHOTSIM_B200_FUSED_LOOKAHEAD=0 disables): C2 9 -> 8 passes, +0.6%.
+  const char* lv = std::getenv("SHOTSIM_B200_FUSED_LOOKAHEAD");
+  const bool lookahead = !(lv && *lv == '0');
   const char* pv = std::getenv("SHOTSIM_B200_FUSED_GREEDY_PASSES");
   const bool greedy_passes = pv && *pv && *pv != '0';
   while (first || !remaining.empty()) {
@@ -282,16 +286,37 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
           if (!(low >> q & 1)) fq.push_back(q);
         std::vector<unsigned> idx(pick);
         for (unsigned i = 0; i < pick; ++i) idx[i] = i;
+        std::vector<uint32_t> sets;
         while (true) {
           uint32_t L2 = low;
           for (unsigned i : idx) L2 |= 1u << fq[i];
-          const size_t got = take_with(L2, nullptr, nullptr);
-          if (got > best) best = got, L = L2;
+          sets.push_back(L2);
           int i = static_cast<int>(pick) - 1;  // next combination
           while (i >= 0 && idx[i] == fq.size() - pick + i) --i;
           if (i < 0) break;
           ++idx[i];
           for (unsigned j = i + 1; j < pick; ++j) idx[j] = idx[j - 1] + 1;
+        }
+        std::vector<std::pair<size_t, uint32_t>> scored;
+        for (uint32_t L2 : sets) scored.emplace_back(take_with(L2, nullptr, nullptr), L2);
+        std::stable_sort(scored.begin(), scored.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+        if (!scored.empty() && scored[0].first > best) best = scored[0].first, L = scored[0].second;
+        // One pass of lookahead: among the best first sets, the one whose
+        // remainder lets the following pass take the most blocks.
+        if (lookahead && remaining.size() > best) {
+          const std::vector<uint32_t> saved = remaining;
+          size_t best2 = 0;
+          const size_t top = std::min<size_t>(scored.size(), 24);
+          for (size_t c = 0; c < top; ++c) {
+            std::vector<uint32_t> t1, r1;
+            remaining = saved;
+            take_with(scored[c].second, &t1, &r1);
+            remaining = r1;
+            size_t next = 0;
+            for (uint32_t L3 : sets) next = std::max(next, take_with(L3, nullptr, nullptr));
+            if (scored[c].first + next > best2) best2 = scored[c].first + next, L = scored[c].second;
+          }
+          remaining = saved;
         }
       }
       taken.clear();
