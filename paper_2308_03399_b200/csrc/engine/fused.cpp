@@ -372,27 +372,59 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
       }
       return cnt;
     };
+    // Candidate seeds: qubit sets spanned by one or two ready blocks.
+    auto seeds = [&](const std::vector<char>& pl) {
+      std::vector<size_t> ready;
+      uint32_t pq = 0;
+      for (size_t t = 0; t < taken.size(); ++t) {
+        if (pl[t]) continue;
+        if (!(qmask(t) & pq)) ready.push_back(t);
+        pq |= qmask(t);
+      }
+      std::vector<uint32_t> out;
+      for (size_t a = 0; a < ready.size(); ++a)
+        for (size_t c = a; c < ready.size(); ++c) {
+          const uint32_t q = qmask(ready[a]) | qmask(ready[c]);
+          if (std::popcount(q) <= static_cast<int>(gq) && std::find(out.begin(), out.end(), q) == out.end())
+            out.push_back(q);
+        }
+      return out;
+    };
+    // Groups a greedy largest-closure seeding needs to place the rest.
+    auto rollout = [&](std::vector<char> pl) {
+      size_t groups = 0;
+      for (size_t left = std::count(pl.begin(), pl.end(), 0); left > 0; ++groups) {
+        uint32_t bq = 0;
+        size_t bc = 0;
+        for (uint32_t q : seeds(pl)) {
+          const size_t got = closure(q, pl, nullptr);
+          if (got > bc) bc = got, bq = q;
+        }
+        std::vector<size_t> ord;
+        closure(bq, pl, &ord);
+        for (size_t t : ord) pl[t] = 1;
+        left -= ord.size();
+        if (ord.empty()) break;  // cannot happen: a ready block always fits
+      }
+      return groups;
+    };
     while (nplaced < taken.size()) {
-      // Seed: the qubit set (the union of one or two ready blocks) whose
-      // closure takes the most blocks — a greedy first-fit seed often closes
-      // the group after two blocks (SHOTSIM_B200_FUSED_GREEDY=1 keeps it).
+      // Seed: the qubit set (the union of one or two ready blocks) after
+      // which a greedy largest-closure rollout needs the fewest groups for
+      // the rest of the pass — a first-fit seed often closes the group after
+      // two blocks (SHOTSIM_B200_FUSED_GREEDY=1 keeps first-fit).
       uint32_t seed_q = 0;
       if (!greedy_groups) {
-        std::vector<size_t> ready;
-        uint32_t pq = 0;
-        for (size_t t = 0; t < taken.size(); ++t) {
-          if (placed[t]) continue;
-          if (!(qmask(t) & pq)) ready.push_back(t);
-          pq |= qmask(t);
+        size_t best_total = ~size_t{0}, best_now = 0;
+        for (uint32_t q : seeds(placed)) {
+          std::vector<size_t> ord;
+          const size_t got = closure(q, placed, &ord);
+          std::vector<char> pl = placed;
+          for (size_t t : ord) pl[t] = 1;
+          const size_t total = 1 + rollout(pl);
+          if (total < best_total || (total == best_total && got > best_now))
+            best_total = total, best_now = got, seed_q = q;
         }
-        size_t best = 0;
-        for (size_t a = 0; a < ready.size(); ++a)
-          for (size_t c = a; c < ready.size(); ++c) {
-            const uint32_t q = qmask(ready[a]) | qmask(ready[c]);
-            if (std::popcount(q) > static_cast<int>(gq)) continue;
-            const size_t got = closure(q, placed, nullptr);
-            if (got > best) best = got, seed_q = q;
-          }
       }
       std::vector<size_t> order;
       closure(seed_q, placed, &order);
