@@ -130,35 +130,38 @@ std::vector<char> build_cubin(const std::string& shapes, std::string* log_out) {
 
 // On-disk cubin cache: $SHOTSIM_B200_CACHE (default ~/.cache/shotsim_b200),
 // keyed by a 64-bit FNV-1a hash of everything that determines the cubin: the
-// shape source, the kernel's main source, the embedded headers, the exact
+// generated source, the kernel's main source, the embedded headers, the exact
 // NVRTC options (resolved knobs included), the NVRTC version and the ABI
 // version — a rebuild that changes any of them never loads a stale cubin.
-std::string cache_path(const std::string& shapes) {
+std::string cache_dir() {
   const char* dir = std::getenv("SHOTSIM_B200_CACHE");
-  std::string d;
-  if (dir && *dir) {
-    d = dir;
-  } else if (const char* home = std::getenv("HOME"); home && *home) {
-    d = std::string(home) + "/.cache/shotsim_b200";
-  } else {
-    return "";
-  }
+  if (dir && *dir) return dir;
+  if (const char* home = std::getenv("HOME"); home && *home) return std::string(home) + "/.cache/shotsim_b200";
+  return "";
+}
+
+std::string keyed_path(const char* prefix, const std::string& source, const char* main,
+                       const std::vector<std::string>& options) {
+  const std::string d = cache_dir();
+  if (d.empty()) return "";
   uint64_t h = 1469598103934665603ull;
   auto mix = [&h](const char* p, size_t n) {
     for (size_t i = 0; i < n; ++i) h = (h ^ static_cast<unsigned char>(p[i])) * 1099511628211ull;
   };
-  mix(shapes.data(), shapes.size());
-  mix(kMain, std::strlen(kMain));
+  mix(source.data(), source.size());
+  mix(main, std::strlen(main));
   for (int i = 0; i < kJitHeaderCount; ++i) mix(kJitHeaderTexts[i], std::strlen(kJitHeaderTexts[i]));
-  for (const std::string& o : nvrtc_options()) mix(o.c_str(), o.size() + 1);
+  for (const std::string& o : options) mix(o.c_str(), o.size() + 1);
   int major = 0, minor = 0;
   nvrtcVersion(&major, &minor);
   const int versions[3] = {major, minor, SSB_ABI_VERSION};
   mix(reinterpret_cast<const char*>(versions), sizeof versions);
-  char name[64];
-  std::snprintf(name, sizeof name, "/tile_pass_%016llx.cubin", static_cast<unsigned long long>(h));
+  char name[96];
+  std::snprintf(name, sizeof name, "/%s_%016llx.cubin", prefix, static_cast<unsigned long long>(h));
   return d + name;
 }
+
+std::string cache_path(const std::string& shapes) { return keyed_path("tile_pass", shapes, kMain, nvrtc_options()); }
 
 std::vector<char> read_file(const std::string& path) {
   std::vector<char> out;
@@ -212,8 +215,12 @@ Entry compile(const std::string& shapes) {
   return e;
 }
 
+// Options of the generic builds (FMA contraction allowed: the fused-matrix
+// kernels).
+std::vector<std::string> generic_options() { return {"-arch=sm_100a", "-std=c++17", "-lineinfo"}; }
+
 // Generic NVRTC build of a complete source (plus the embedded engine
-// headers) for sm_100a; FMA contraction allowed (the fused-matrix kernels).
+// headers) for sm_100a.
 std::vector<char> build_generic_cubin(const std::string& source, std::string* log_out) {
   std::vector<const char*> names(kJitHeaderNames, kJitHeaderNames + kJitHeaderCount);
   std::vector<const char*> texts(kJitHeaderTexts, kJitHeaderTexts + kJitHeaderCount);
@@ -223,8 +230,10 @@ std::vector<char> build_generic_cubin(const std::string& source, std::string* lo
     *log_out = "nvrtcCreateProgram failed";
     return {};
   }
-  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo"};
-  const nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+  const std::vector<std::string> base = generic_options();
+  std::vector<const char*> opts;
+  for (const std::string& o : base) opts.push_back(o.c_str());
+  const nvrtcResult r = nvrtcCompileProgram(prog, static_cast<int>(opts.size()), opts.data());
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
@@ -243,10 +252,7 @@ std::vector<char> build_generic_cubin(const std::string& source, std::string* lo
 }
 
 std::string generic_cache_path(const std::string& source) {
-  const std::string shape_like = cache_path(source);  // same directory / key ingredients
-  if (shape_like.empty()) return "";
-  return shape_like.substr(0, shape_like.rfind('/')) + "/fused_" +
-         shape_like.substr(shape_like.rfind('_') + 1);
+  return keyed_path("fused", source, "", generic_options());
 }
 
 struct GenericEntry {
