@@ -78,9 +78,12 @@ std::vector<std::string> nvrtc_options() {
     const char* v = std::getenv(name);
     return std::string(v && *v ? v : dflt);
   };
-  return {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES",
-          "-DSSB_QPT=" + knob("SHOTSIM_B200_JIT_QPT", SSB_STR(SSB_JIT_QPT)),
-          "-DSSB_TILE_MINB=" + knob("SHOTSIM_B200_JIT_MINB", SSB_STR(SSB_JIT_MINB))};
+  std::vector<std::string> o = {"-arch=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo", "-DSSB_SHAPES",
+                                "-DSSB_QPT=" + knob("SHOTSIM_B200_JIT_QPT", SSB_STR(SSB_JIT_QPT)),
+                                "-DSSB_TILE_MINB=" + knob("SHOTSIM_B200_JIT_MINB", SSB_STR(SSB_JIT_MINB))};
+  // SHOTSIM_B200_TILE_PREFETCH=1: L2 prefetch of the next tile (A/B; off).
+  if (knob("SHOTSIM_B200_TILE_PREFETCH", "0") == "1") o.push_back("-DSSB_TILE_PREFETCH");
+  return o;
 }
 
 // NVRTC: shape source + embedded engine headers -> sm_100a cubin. Returns an

@@ -290,8 +290,11 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tile_s + 16 * (l0 + j * NT)),
                            "l"(tbase + (lo_part | off[j])));
         }
-        // Warm L2 with the next tile of this shot while this one is computed,
-        // so its loads return at L2 latency (no registers, no shared memory).
+        // Optional (SSB_TILE_PREFETCH): warm L2 with the next tile of this
+        // shot while this one is computed. Off by default: on B200 it costs
+        // more DRAM reads than it saves latency (C4 +2.5%, C5 exact +1.2%
+        // without it; ncu: 26% DRAM reads above the algorithmic bytes with it).
+#ifdef SSB_TILE_PREFETCH
         if (t + 1 < t_end) {
           const double2* nb = seg + pdep_positions(t + 1, hpos, n - k);
           for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * NT, i0 += 8) {
@@ -303,6 +306,7 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
               if (l0 + j * NT < L) asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + (lo_part | off[j])));
           }
         }
+#endif
         asm volatile("cp.async.wait_all;" ::: "memory");
       }
       __syncthreads();
