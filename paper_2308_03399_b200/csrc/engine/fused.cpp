@@ -280,7 +280,9 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
       const unsigned pick = k - static_cast<unsigned>(std::popcount(low));
       double combos = 1.0;
       for (unsigned i = 0; i < pick; ++i) combos = combos * (free_q - i) / (i + 1);
-      if (combos <= 20000.0 && std::getenv("SHOTSIM_B200_FUSED_NO_EXHAUSTIVE") == nullptr) {
+      // (bounded work: sets x remaining blocks per pass)
+      const double scan = combos * static_cast<double>(remaining.size());
+      if (combos <= 20000.0 && scan <= 3e7 && std::getenv("SHOTSIM_B200_FUSED_NO_EXHAUSTIVE") == nullptr) {
         std::vector<unsigned> fq;
         for (unsigned q = 0; q < n; ++q)
           if (!(low >> q & 1)) fq.push_back(q);
@@ -303,7 +305,7 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
         if (!scored.empty() && scored[0].first > best) best = scored[0].first, L = scored[0].second;
         // One pass of lookahead: among the best first sets, the one whose
         // remainder lets the following pass take the most blocks.
-        if (lookahead && remaining.size() > best) {
+        if (lookahead && remaining.size() > best && 24.0 * scan <= 3e8) {
           const std::vector<uint32_t> saved = remaining;
           size_t best2 = 0;
           const size_t top = std::min<size_t>(scored.size(), 24);
