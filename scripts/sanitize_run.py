@@ -18,6 +18,8 @@ cases = [
     ("qv14 exact jit", cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise(), "batch", 4, {}),
     ("qv14 exact interp", cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise(), "batch", 4, {"interpret_only": True}),
     ("qv14 fused fma", cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise(), "batch", 4, {"fused_matrices": True}),
+    ("qv14 fused fma 12-qubit tiles", cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise(), "batch", 4,
+     {"fused_matrices": True, "tile_qubits": 12}),
     ("rnd13 kraus streamed", cc.random_layers(13, depth=2, seed=3), cc.thermal_noise(0.05, 0.1), "batch", 4,
      {"resident_max_qubits": 1, "tile_qubits": 11}),
     ("rnd14 kraus streamed epilogue (several tiles per CTA)", cc.random_layers(14, depth=2, seed=4),
@@ -39,6 +41,14 @@ if not only or "epilogue" in only:  # the opt-in Kraus-site epilogue, several ti
     r = eng.run_batch(prog, RunOptions(shots=256, seed=3, resident_max_qubits=1, tile_qubits=10))
     os.environ["SHOTSIM_B200_EPILOGUE"] = "0"
     print("rnd14 kraus epilogue on ok", r.dispatch_count, flush=True)
+if not only or "jit" in only:  # the per-pass NVRTC-specialised fused kernels (11- and 12-qubit tiles)
+    os.environ["SHOTSIM_B200_FUSED_JIT"] = "1"
+    for tile in (11, 12):
+        prog = Program.from_text(cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise())
+        r = eng.run_batch(prog, RunOptions(shots=4, seed=3, fused_matrices=True, tile_qubits=tile))
+        assert r.specialised_shapes == r.fused_passes
+        print("qv14 fused jit tile", tile, "ok", r.dispatch_count, flush=True)
+    os.environ["SHOTSIM_B200_FUSED_JIT"] = "0"
 if not only or "mma" in only:
     os.environ["SHOTSIM_B200_FUSED_MMA"] = "1"
     prog = Program.from_text(cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise())
