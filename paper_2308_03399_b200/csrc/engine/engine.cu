@@ -752,10 +752,11 @@ void run_fused(ssb_engine* E, const ssb_program* prog, DevProgram& dp, uint64_t 
   // FMA build: 256 threads for 12- and 13-qubit tiles, 128 for 11-qubit ones
   // (one hexad per thread either way).
   // (3-qubit groups: 256 threads, 2^(k-3) octads per tile)
-  const unsigned fnt = (use_mma || use_db) ? NT : (f.gq == 4 && f.k <= 11 ? 128u : 256u);
+  const unsigned fnt = (use_mma || use_db) ? NT : (f.gq == 4 && f.k <= 10 ? 64u : f.gq == 4 && f.k <= 11 ? 128u : 256u);
   const void* kfn = use_mma              ? reinterpret_cast<const void*>(fused_pass_mma_kernel)
                     : use_db             ? reinterpret_cast<const void*>(fused_pass_db_kernel)
                     : f.gq == 3          ? reinterpret_cast<const void*>(fused_pass_kernel<256, 3>)
+                    : fnt == 64          ? reinterpret_cast<const void*>(fused_pass_kernel<64, 4>)
                     : fnt == 128         ? reinterpret_cast<const void*>(fused_pass_kernel<128, 4>)
                                          : reinterpret_cast<const void*>(fused_pass_kernel<256, 4>);
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

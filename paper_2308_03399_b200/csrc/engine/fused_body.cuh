@@ -34,7 +34,7 @@ struct FEntry {
 __host__ __device__ inline uint64_t fused_smem_bytes(unsigned k, uint32_t max_blocks, uint32_t max_sites) {
   return (uint64_t{1} << k) * 16 + uint64_t{max_blocks} * 256 + uint64_t{kFusedSlots} * 256 +
          uint64_t{max_blocks} * (sizeof(FEntry) + sizeof(FGroup) + sizeof(FBlock)) + uint64_t{max_sites} * 4 +
-         (uint64_t{1} << (k - 7)) * 4 + 32;
+         (uint64_t{1} << (k - 6)) * 4 + 32;
 }
 
 __device__ __forceinline__ uint32_t ins0(uint32_t x, unsigned p) {
@@ -275,7 +275,7 @@ __device__ __forceinline__ void fused_pass_body(FusedView F, uint32_t pass_index
     g.blk_end -= blk0;
     sgrp[i] = g;
   }
-  constexpr unsigned LB = FNT == 128 ? 7 : 8;
+  constexpr unsigned LB = FNT == 64 ? 6 : FNT == 128 ? 7 : 8;  // log2(FNT)
   for (uint32_t i = threadIdx.x; i < (1u << (k - LB)); i += FNT)
     hi_off[i] = static_cast<uint32_t>(pdep_positions(i, spd.lq + LB, k - LB));
   if (threadIdx.x == 0)

@@ -1,5 +1,5 @@
 bash scripts/lib_ab.sh base tree base tree 2>&1 | tail -8
-for t in 11 12; do
+for t in 10 11 12; do
 python - <<PY
 import os,sys
 sys.path.insert(0,'.')

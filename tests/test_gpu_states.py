@@ -113,3 +113,15 @@ def test_fused_counts_equal_exact(engine, oracle, monkeypatch, scale, kernel):
         assert 0 < r.guard_flagged < 400
     else:
         assert r.guard_flagged <= 2
+
+
+@pytest.mark.parametrize("tile", [10, 11, 12])
+def test_fused_tile_sizes_equal_exact(engine, oracle, tile):
+    """Every fused tile size (64 / 128 / 256-thread CTAs, one hexad per
+    thread) gives the reference's per-shot values."""
+    prog = Program.from_text(cc.quantum_volume(14, depth=8, seed=3), cc.qv_noise())
+    want = oracle.run_shots(prog, np.arange(300), 23, threads=8)
+    r = engine.run_batch(prog, RunOptions(shots=300, seed=23, fused_matrices=True, tile_qubits=tile,
+                                          record_shot_values=True))
+    assert r.fused_blocks > 0
+    assert (np.asarray(r.shot_values) == want).all()
