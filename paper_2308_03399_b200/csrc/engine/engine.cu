@@ -686,7 +686,7 @@ bool fused_ready(ssb_engine* E, DevProgram& dp) {
   unsigned gq = kFusedGroupDefault;
   if (const char* v = std::getenv("SHOTSIM_B200_FUSED_GROUP"); v && (*v == '3' || *v == '4')) gq = *v - '0';
   if (const char* v = std::getenv("SHOTSIM_B200_FUSED_MMA"); v && *v && *v != '0') gq = 4;
-  f = plan_fused(dp.host, dp.host.tile_k, gq);
+  f = plan_fused_cached(dp.host, dp.host.tile_k, gq);
   if (f.ok && f.k < 8) {
     f.ok = false;
     f.why = "tile smaller than 8 qubits";

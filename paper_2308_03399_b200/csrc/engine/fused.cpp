@@ -10,6 +10,9 @@
 #include <complex>
 #include <cstdlib>
 #include <limits>
+#include <map>
+#include <mutex>
+#include <string>
 
 namespace ssb {
 
@@ -501,6 +504,46 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
   f.num_blocks = static_cast<uint32_t>(blks.size());
   f.gq = gq;
   f.ok = true;
+  return f;
+}
+
+// Plans are pure functions of the program's ops / terms / channels /
+// matrices, the tile size, the group size and the planner knobs; a caller
+// that lowers the same circuit again (the drop-in plugin flattens the
+// program on every run) gets the cached plan instead of re-running the
+// products and the local-set search (C2: ~50 ms).
+FusedPlan plan_fused_cached(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
+  uint64_t h1 = 1469598103934665603ull, h2 = 0x9E3779B97F4A7C15ull;
+  auto mix = [&](const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) {
+      h1 = (h1 ^ b[i]) * 1099511628211ull;
+      h2 = (h2 ^ b[i]) * 0x100000001B3ull + 0x632BE59BD9B4E019ull;
+    }
+  };
+  const uint32_t scal[4] = {h.n, h.end, tile_k, gq};
+  mix(scal, sizeof scal);
+  mix(h.ops.data(), h.ops.size() * sizeof(DevOp));
+  mix(h.terms.data(), h.terms.size() * sizeof(DevTerm));
+  mix(h.channels.data(), h.channels.size() * sizeof(DevChannel));
+  mix(h.mats.data(), h.mats.size() * sizeof(double));
+  for (const char* k : {"SHOTSIM_B200_FUSED_CAP", "SHOTSIM_B200_FUSED_GREEDY", "SHOTSIM_B200_FUSED_GREEDY_PASSES",
+                        "SHOTSIM_B200_FUSED_LOOKAHEAD", "SHOTSIM_B200_FUSED_NO_EXHAUSTIVE"}) {
+    const char* v = std::getenv(k);
+    const std::string kv = std::string(k) + "=" + (v ? v : "");
+    mix(kv.data(), kv.size() + 1);
+  }
+  static std::mutex mu;
+  static std::map<std::pair<uint64_t, uint64_t>, FusedPlan> cache;
+  const auto key = std::make_pair(h1, h2);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (auto it = cache.find(key); it != cache.end()) return it->second;
+  }
+  FusedPlan f = plan_fused(h, tile_k, gq);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 32) cache.erase(cache.begin());  // bounded (plans of up to ~MBs each)
+  cache.emplace(key, f);
   return f;
 }
 

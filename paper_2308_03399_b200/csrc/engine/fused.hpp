@@ -49,5 +49,7 @@ constexpr unsigned kFusedGroupDefault = 4;
 // gq: qubits per register group (4: 16-amplitude hexads, the tensor-core
 // layout needs 4; 3: 8-amplitude octads, half the registers per thread).
 FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq = 4);
+// plan_fused through a process-wide cache keyed by the program's content.
+FusedPlan plan_fused_cached(const HostDevProgram& h, unsigned tile_k, unsigned gq = 4);
 
 }  // namespace ssb
