@@ -18,8 +18,13 @@
 namespace ssb {
 
 // The static (interpreter) FMA build of the fused pass.
+// Threads per SM the register allocation must allow (4-qubit groups: 512,
+// i.e. 128 registers per thread; A/B knob SSB_FUSED_G4_THREADS).
+#ifndef SSB_FUSED_G4_THREADS
+#define SSB_FUSED_G4_THREADS 512
+#endif
 template <int FNT, int G>
-static __global__ void __launch_bounds__(FNT, (G == 4 ? 512 : 1024) / FNT)
+static __global__ void __launch_bounds__(FNT, (G == 4 ? SSB_FUSED_G4_THREADS : 1024) / FNT)
     fused_pass_kernel(FusedView F, uint32_t pass_index, double2* state, uint64_t S, const uint8_t* pauli_sel,
                       uint32_t num_pauli, uint32_t max_blocks, uint32_t max_sites) {
   fused_pass_body<FNT, G>(F, pass_index, state, S, pauli_sel, num_pauli, max_blocks, max_sites,
