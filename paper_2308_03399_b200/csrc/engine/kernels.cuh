@@ -1013,7 +1013,10 @@ static __global__ void g_sample_scan_kernel(ProgView P, const double2* st, uint6
 // thread 0 replays the chunk with the reference's sequential adds. Binade
 // changes (~n per shot) and ties are the only serial chunks besides the
 // crossing one. Fallback when no crossing: the last outcome with p > 0.
-constexpr uint32_t SAMPLE_CHUNK = 2048;
+#ifndef SSB_SAMPLE_CHUNK
+#define SSB_SAMPLE_CHUNK 2048
+#endif
+constexpr uint32_t SAMPLE_CHUNK = SSB_SAMPLE_CHUNK;
 constexpr uint32_t SAMPLE_NT = 256;
 
 static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView P, const double2* st, uint64_t S,
