@@ -125,3 +125,20 @@ def test_fused_tile_sizes_equal_exact(engine, oracle, tile):
                                           record_shot_values=True))
     assert r.fused_blocks > 0
     assert (np.asarray(r.shot_values) == want).all()
+
+
+def test_fused_plan_cache_across_program_objects(engine, oracle, monkeypatch):
+    """Fused plans are cached by program content: lowering the same circuit
+    again (the plugin path) reuses the plan, a changed circuit does not, and
+    both give the reference's values."""
+    circ, noise = cc.quantum_volume(14, depth=6, seed=8), cc.qv_noise()
+    want = oracle.run_shots(Program.from_text(circ, noise), np.arange(200), 29, threads=8)
+    for _ in range(2):
+        r = engine.run_batch(Program.from_text(circ, noise),
+                             RunOptions(shots=200, seed=29, fused_matrices=True, record_shot_values=True))
+        assert (np.asarray(r.shot_values) == want).all()
+    other = cc.quantum_volume(14, depth=6, seed=9)
+    want2 = oracle.run_shots(Program.from_text(other, noise), np.arange(200), 29, threads=8)
+    r = engine.run_batch(Program.from_text(other, noise),
+                         RunOptions(shots=200, seed=29, fused_matrices=True, record_shot_values=True))
+    assert (np.asarray(r.shot_values) == want2).all()
