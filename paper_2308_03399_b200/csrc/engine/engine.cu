@@ -33,6 +33,8 @@ int launch_resident_warp(const void* view, uint64_t seed, uint64_t shot_begin, u
 
 // specialise.cpp: the shape-specialised tile-pass kernel for a plan, or null.
 const void* specialised_tile_kernel(const HostDevProgram& h);
+// specialise.cpp: whether that kernel double-buffers its tiles (SSB_TILE_DB).
+bool specialised_tile_double_buffered();
 // fused_jit.cpp: per pass the specialised fused kernel, or null.
 std::vector<const void*> fused_jit_kernels(const FusedPlan& f, std::string* log);
 
@@ -1003,13 +1005,14 @@ void run_batch_device(ssb_engine* E, const ssb_program* prog, uint64_t shot_begi
       kcls = static_cast<uint64_t*>(scratch(E, "wave_kcls", wave * sizeof(uint64_t)));
       kchosen = static_cast<int*>(scratch(E, "wave_kchosen", wave * sizeof(int)));
     }
-    size_t tsmem = 0;
-    for (const PassDesc& pd : h.passes)
-      tsmem = std::max<size_t>(tsmem, tile_smem_bytes(pd.k, pd.uop_end - pd.uop_begin, pd.mat_count));
     // The shape-specialised build of the same kernel (specialise.cpp) when
     // available, else the static interpreter build.
     const void* kfn = (opts && opts->interpret_only) ? nullptr : specialised_tile_kernel(h);
     const bool specialised = kfn != nullptr;
+    const bool tile_db = specialised && specialised_tile_double_buffered();
+    size_t tsmem = 0;
+    for (const PassDesc& pd : h.passes)
+      tsmem = std::max<size_t>(tsmem, tile_smem_bytes(pd.k, pd.uop_end - pd.uop_begin, pd.mat_count, tile_db));
     if (!kfn) kfn = reinterpret_cast<const void*>(tile_pass_kernel);
     CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsmem)));
     int per_sm = 0;

@@ -83,6 +83,8 @@ std::vector<std::string> nvrtc_options() {
                                 "-DSSB_TILE_MINB=" + knob("SHOTSIM_B200_JIT_MINB", SSB_STR(SSB_JIT_MINB))};
   // SHOTSIM_B200_TILE_PREFETCH=1: L2 prefetch of the next tile (A/B; off).
   if (knob("SHOTSIM_B200_TILE_PREFETCH", "0") == "1") o.push_back("-DSSB_TILE_PREFETCH");
+  // SHOTSIM_B200_TILE_DB=1: double-buffered tiles (A/B).
+  if (knob("SHOTSIM_B200_TILE_DB", "0") == "1") o.push_back("-DSSB_TILE_DB");
   return o;
 }
 
@@ -331,6 +333,12 @@ std::vector<std::vector<const void*>> jit_compile_batch(const std::vector<std::s
 }
 
 bool jit_compile_check(const std::string& source, std::string* log) { return !build_generic_cubin(source, log).empty(); }
+
+bool specialised_tile_double_buffered() {
+  for (const std::string& o : nvrtc_options())
+    if (o == "-DSSB_TILE_DB") return true;
+  return false;
+}
 
 bool specialise_compile_check(const HostDevProgram& h, std::string* log) {
   if (h.shapes.empty()) {

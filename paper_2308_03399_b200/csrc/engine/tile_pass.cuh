@@ -140,9 +140,10 @@ __device__ __forceinline__ void tile_epilogue(const EpiTables& T, unsigned nhi, 
 // Shared-memory layout of the tile pass: tile | matrix table | uops |
 // compacted uops | kept-uop prefix (u16, nu + 1) | kept-Pauli prefix (u16,
 // nu + 1) | high-part tile offsets (u32, 2^(k - 8)).
-__host__ __device__ inline uint64_t tile_smem_bytes(unsigned k, uint32_t nuops, uint32_t nmats) {
+__host__ __device__ inline uint64_t tile_smem_bytes(unsigned k, uint32_t nuops, uint32_t nmats, bool db = false) {
   const unsigned kt = k < 8 ? k : 8;
-  return (uint64_t{1} << k) * 16 + uint64_t{nmats} * 16 + uint64_t{nuops} * 32 + (uint64_t{nuops} + 1) * 4 + 16 +
+  return (uint64_t{1} << k) * 16 * (db ? 2 : 1) + uint64_t{nmats} * 16 + uint64_t{nuops} * 32 +
+         (uint64_t{nuops} + 1) * 4 + 16 +
          (uint64_t{1} << (k - kt)) * 4 + uint64_t{nuops} + 16;
 }
 
@@ -154,14 +155,22 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
                                                       const uint64_t* cregs, const uint8_t* pauli_sel,
                                                       uint32_t num_pauli, const double2* kmat, const uint64_t* kcls,
                                                       const uint32_t* act, double* epi_part) {
-  extern __shared__ double2 tile[];
+  extern __shared__ double2 tile0[];
   const PassDesc& pd = P.passes[pass_index];
   const unsigned n = P.n, k = pd.k;
   const unsigned kt = k < 8 ? k : 8;
   const uint64_t tiles = uint64_t{1} << (n - k);
   const uint32_t L = 1u << k;
   const uint32_t nu = pd.uop_end - pd.uop_begin;
-  double2* smats = tile + L;
+  // SSB_TILE_DB: two tile buffers; the next tile of the shot is loaded while
+  // this one is computed and stored (tile_smem_bytes(..., db = true)).
+#ifdef SSB_TILE_DB
+  constexpr uint32_t NBUF = 2;
+#else
+  constexpr uint32_t NBUF = 1;
+#endif
+  double2* tile = tile0;
+  double2* smats = tile0 + NBUF * L;
   Uop* uops = reinterpret_cast<Uop*>(smats + pd.mat_count);
   Uop* eops = uops + nu;
   uint16_t* pre = reinterpret_cast<uint16_t*>(eops + nu);
@@ -266,12 +275,41 @@ static __device__ __forceinline__ void tile_pass_body(const ProgView& P, uint32_
     // pass of readout Pauli sites that all drew identity) and no relabeled
     // segment to store: its tiles are left untouched in HBM.
     if (!pd.first && pre[nu] == 0 && no_relabel && !epi) t_end = t_begin;
+    // LDGSTS of tile tt of this shot into buffer dst (one commit group).
+    auto load_tile = [&](uint64_t tt, double2* dst) {
+      const double2* tb = seg + pdep_positions(tt, hpos, n - k);
+      const uint32_t dst_s = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+      for (uint32_t l0 = threadIdx.x, i0 = 0; l0 < L; l0 += 8 * NT, i0 += 8) {
+        uint32_t off[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) off[j] = l0 + j * NT < L ? hi_off[i0 + j] : 0u;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j)
+          if (l0 + j * NT < L)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_s + 16 * (l0 + j * NT)),
+                         "l"(tb + (lo_part | off[j])));
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     for (uint64_t t = t_begin; t < t_end; ++t) {
       double2* tbase = seg + pdep_positions(t, hpos, n - k);
+      tile = tile0 + (NBUF == 2 ? ((t - t_begin) & 1) * L : 0);
       if (pd.first) {
         const bool origin = (tbase == seg);
         for (uint32_t l = threadIdx.x, i = 0; l < L; l += NT, ++i)
           tile[l] = make_double2((origin && (lo_part | hi_off[i]) == 0) ? 1.0 : 0.0, 0.0);
+      } else if (NBUF == 2) {
+        // This tile was requested one iteration ago (or now, for the shot's
+        // first); request the next one into the other buffer before waiting.
+        // Each thread's copies land in the slots only it reads at the store,
+        // so refilling the other buffer needs no barrier.
+        if (t == t_begin) load_tile(t, tile);
+        if (t + 1 < t_end) {
+          load_tile(t + 1, tile0 + ((t + 1 - t_begin) & 1) * L);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
       } else {
         // Asynchronous global -> shared copies (LDGSTS): every 16-byte element
         // of the thread is in flight at once, with no register round trip
