@@ -386,10 +386,13 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
         if (!(qmask(t) & pq)) ready.push_back(t);
         pq |= qmask(t);
       }
+      // (the second block may be any unplaced one: it can become ready
+      // inside the group once its predecessors there are applied)
       std::vector<uint32_t> out;
       for (size_t a = 0; a < ready.size(); ++a)
-        for (size_t c = a; c < ready.size(); ++c) {
-          const uint32_t q = qmask(ready[a]) | qmask(ready[c]);
+        for (size_t c = 0; c < taken.size(); ++c) {
+          if (pl[c]) continue;
+          const uint32_t q = qmask(ready[a]) | qmask(c);
           if (std::popcount(q) <= static_cast<int>(gq) && std::find(out.begin(), out.end(), q) == out.end())
             out.push_back(q);
         }
