@@ -211,3 +211,16 @@ def test_balanced_branch_two_ranks_equal_single_run():
     for r in (0, 1):
         assert out[r][0] == np.asarray(want.shot_values).astype(np.int64).tolist()
     assert sorted(out[0][1] + out[1][1]) == [(b, chunk) for b in range(0, shots, chunk)]
+
+
+def test_run_balanced_single_process_edges():
+    """Without a process group every chunk runs locally; empty runs, chunks
+    larger than the run and a wrong chunk length are handled."""
+    vals, mine = run_balanced(lambda b, n: np.arange(b, b + n) * 3, 10, 4)
+    assert vals.tolist() == [3 * i for i in range(10)] and mine == [(0, 4), (4, 4), (8, 2)]
+    vals, mine = run_balanced(lambda b, n: np.zeros(n), 0, 4)
+    assert vals.size == 0 and mine == []
+    vals, mine = run_balanced(lambda b, n: np.ones(n), 3, 100)
+    assert vals.tolist() == [1, 1, 1] and mine == [(0, 3)]
+    with pytest.raises(ValueError):
+        run_balanced(lambda b, n: np.ones(n + 1), 5, 2)
