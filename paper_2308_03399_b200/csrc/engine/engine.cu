@@ -59,8 +59,14 @@ struct DevProgram {
   // Per pass the run-time specialised fused kernel (fused_jit.cpp) or null.
   bool fjit_tried = false;
   std::vector<const void*> fjit;
+  // The arrays come from the device's stream-ordered pool on the engine's
+  // stream: freeing them (a program destroyed while the engine lives) returns
+  // them to the pool without a device-wide synchronisation — plain cudaFree
+  // here took up to ~200 ms now and then on the plugin path, which lowers
+  // and destroys a program on every run.
+  cudaStream_t stream = nullptr;
   ~DevProgram() {
-    for (void* p : allocs) cudaFree(p);
+    for (void* p : allocs) cudaFreeAsync(p, stream);
   }
 };
 
@@ -150,9 +156,10 @@ template <class T>
 T* upload(DevProgram& d, const std::vector<T>& v) {
   if (v.empty()) return nullptr;
   void* p = nullptr;
-  CK(cudaMalloc(&p, v.size() * sizeof(T)));
+  CK(cudaMallocAsync(&p, v.size() * sizeof(T), d.stream));
   d.allocs.push_back(p);
-  CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  // (pageable source: the copy has completed when the call returns)
+  CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, d.stream));
   return static_cast<T*>(p);
 }
 
@@ -167,6 +174,7 @@ DevProgram& device_program(ssb_engine* E, const ssb_program* prog, unsigned tile
   auto it = E->programs.find(key);
   if (it != E->programs.end()) return *it->second;
   auto d = std::make_unique<DevProgram>();
+  d->stream = E->stream;
   d->host = prog->dev;
   if (tile_k == 0) plan_resident(d->host);
   else plan_passes(d->host, tile_k);
@@ -1179,6 +1187,14 @@ SSB_API int ssb_engine_create(int device, ssb_engine** out) {
     E->num_sms = prop.multiProcessorCount;
     E->smem_optin = prop.sharedMemPerBlockOptin;
     CK(cudaStreamCreateWithFlags(&E->stream, cudaStreamNonBlocking));
+    {  // keep freed program arrays in the device's pool for reuse (DevProgram)
+      cudaMemPool_t pool = nullptr;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = uint64_t{1} << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaGetLastError();
+    }
     CK(cudaEventCreate(&E->ev0));
     CK(cudaEventCreate(&E->ev1));
     CK(cudaMalloc(&E->err, sizeof(int)));
@@ -1201,7 +1217,8 @@ SSB_API void ssb_engine_destroy(ssb_engine* E) {
   }
   cudaSetDevice(E->device);
   cudaStreamSynchronize(E->stream);
-  E->programs.clear();
+  E->programs.clear();  // (stream-ordered frees)
+  cudaStreamSynchronize(E->stream);
   for (auto& [name, slot] : E->scratch) cudaFree(slot.first);
   for (auto& [name, slot] : E->host_scratch) cudaFreeHost(slot.first);
   cudaFree(E->err);
