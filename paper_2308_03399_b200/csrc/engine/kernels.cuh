@@ -681,7 +681,10 @@ static __global__ void __launch_bounds__(kE2Block) g_expval2_split_kernel(const 
 // consecutive 512-pair blocks of one (shot, matrix); each round copies 16
 // pairs of every block in (16 lanes read 256 contiguous bytes), then each
 // thread continues its block's sequential sum over those 16 pairs.
-constexpr unsigned kE1Threads = 128, kE1Pairs = 16;
+#ifndef SSB_E1_PAIRS
+#define SSB_E1_PAIRS 16
+#endif
+constexpr unsigned kE1Threads = 128, kE1Pairs = SSB_E1_PAIRS;  // pairs per thread per staged round
 __device__ __forceinline__ uint32_t e1_slot(uint32_t j, uint32_t h, uint32_t p) {
   return j * (2 * kE1Pairs + 1) + h * kE1Pairs + p;  // one pad slot per block: conflict-free
 }
