@@ -353,9 +353,11 @@ const void* specialised_tile_kernel(const HostDevProgram& h) {
   // a multiple of NT * QPT (= 256 at one quad per thread), i.e. k >= 10.
   if (h.shapes.empty() || h.tile_k < 10) return nullptr;
   if (const char* off = std::getenv("SHOTSIM_B200_NO_SPECIALISE"); off && *off && *off != '0') return nullptr;
-  const std::string src = shape_source(h) + "// " + std::to_string(std::getenv("SHOTSIM_B200_JIT_QPT") != nullptr) +
-                          (std::getenv("SHOTSIM_B200_JIT_QPT") ? std::getenv("SHOTSIM_B200_JIT_QPT") : "") +
-                          (std::getenv("SHOTSIM_B200_JIT_MINB") ? std::getenv("SHOTSIM_B200_JIT_MINB") : "") + "\n";
+  // In-process key: the shapes plus the resolved NVRTC options (the knobs
+  // change the kernel, e.g. SSB_TILE_DB its shared-memory layout).
+  std::string src = shape_source(h) + "//";
+  for (const std::string& o : nvrtc_options()) src += " " + o;
+  src += "\n";
   std::lock_guard<std::mutex> lock(g_mu);
   auto it = g_cache.find(src);
   if (it == g_cache.end()) it = g_cache.emplace(src, compile(src)).first;

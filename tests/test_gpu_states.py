@@ -45,14 +45,17 @@ PATHS = {
     "tile_jit": (lambda n: True, dict(resident_max_qubits=1, tile_qubits=10)),
     "tile_interp": (lambda n: True, dict(resident_max_qubits=1, tile_qubits=10, interpret_only=True)),
     "tile_default": (lambda n: n > 13, dict()),
+    "tile_db": (lambda n: n == 14, dict(resident_max_qubits=1, tile_qubits=11)),  # SHOTSIM_B200_TILE_DB=1
     "branch": (lambda n: True, None),
 }
 
 
 @pytest.mark.parametrize("n", [12, 14, 16])
 @pytest.mark.parametrize("path", list(PATHS))
-def test_states_equal_reference(engine, ref, n, path):
+def test_states_equal_reference(engine, ref, monkeypatch, n, path):
     ok, kw = PATHS[path]
+    if path == "tile_db":  # the double-buffered specialised tile pass (A/B knob)
+        monkeypatch.setenv("SHOTSIM_B200_TILE_DB", "1")
     if not ok(n):
         pytest.skip("path not used at this size")
     for name, (circ, noise) in programs(n).items():
