@@ -216,13 +216,14 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
   std::vector<uint32_t> remaining(blks.size());
   for (uint32_t i = 0; i < remaining.size(); ++i) remaining[i] = i;
   bool first = true;
-  // Blocks a pass with the fixed local set L takes from `remaining` (in
-  // order; a block is blocked once an earlier untaken block shares a qubit).
-  auto take_with = [&](uint32_t L, std::vector<uint32_t>* taken, std::vector<uint32_t>* rest) {
+  // Blocks a pass with the fixed local set L takes from `rem` (in order; a
+  // block is blocked once an earlier untaken block shares a qubit).
+  auto take_from = [&](const std::vector<uint32_t>& rem, uint32_t L, std::vector<uint32_t>* taken,
+                       std::vector<uint32_t>* rest) {
     uint32_t blocked = 0;
     size_t cnt = 0;
-    for (size_t r = 0; r < remaining.size(); ++r) {
-      const uint32_t b = remaining[r];
+    for (size_t r = 0; r < rem.size(); ++r) {
+      const uint32_t b = rem[r];
       const uint32_t qm = (1u << blks[b].q0) | (1u << blks[b].q1);
       if (!(qm & blocked) && (qm & ~L) == 0 && cnt < cap) {
         ++cnt;
@@ -241,93 +242,165 @@ FusedPlan plan_fused(const HostDevProgram& h, unsigned tile_k, unsigned gq) {
   const bool lookahead = !(lv && *lv == '0');
   const char* pv = std::getenv("SHOTSIM_B200_FUSED_GREEDY_PASSES");
   const bool greedy_passes = pv && *pv && *pv != '0';
-  while (first || !remaining.empty()) {
+  // The local set of the next pass over `rem`: first-fit, then hill-climbing
+  // one-qubit swaps, then (small registers) every subset with one pass of
+  // lookahead. `top` (optional) receives the best-scoring sets, best first.
+  auto choose_local = [&](const std::vector<uint32_t>& rem, std::vector<uint32_t>* top) {
     uint32_t L = low, blocked = 0;
-    std::vector<uint32_t> taken, rest;
-    for (size_t r = 0; r < remaining.size(); ++r) {
-      const uint32_t b = remaining[r];
+    size_t nt = 0;
+    for (size_t r = 0; r < rem.size(); ++r) {
+      const uint32_t b = rem[r];
       const uint32_t qm = (1u << blks[b].q0) | (1u << blks[b].q1);
-      if (!(qm & blocked) && static_cast<unsigned>(std::popcount(L | qm)) <= k && taken.size() < cap) {
+      if (!(qm & blocked) && static_cast<unsigned>(std::popcount(L | qm)) <= k && nt < cap) {
         L |= qm;
-        taken.push_back(b);
+        ++nt;
       } else {
         blocked |= qm;
-        rest.push_back(b);
       }
-      if (blocked == all) {
-        rest.insert(rest.end(), remaining.begin() + static_cast<long>(r) + 1, remaining.end());
-        break;
-      }
+      if (blocked == all) break;
     }
     for (unsigned q = 0; q < n && static_cast<unsigned>(std::popcount(L)) < k; ++q) L |= 1u << q;
-    // Local-set search: from the first-fit set, swap one non-forced local
-    // qubit for a non-local one while that lets the pass take more blocks
-    // (fewer passes = fewer HBM sweeps and tile IO phases).
-    if (!greedy_passes && k < n) {
-      size_t best = take_with(L, nullptr, nullptr);
-      for (bool improved = true; improved;) {
-        improved = false;
-        for (unsigned qi = 0; qi < n && !improved; ++qi) {
-          if (!(L >> qi & 1) || (low >> qi & 1)) continue;
-          for (unsigned qo = 0; qo < n && !improved; ++qo) {
-            if (L >> qo & 1) continue;
-            const uint32_t L2 = (L & ~(1u << qi)) | (1u << qo);
-            const size_t got = take_with(L2, nullptr, nullptr);
-            if (got > best) best = got, L = L2, improved = true;
-          }
+    if (greedy_passes || k >= n) return L;
+    size_t best = take_from(rem, L, nullptr, nullptr);
+    for (bool improved = true; improved;) {
+      improved = false;
+      for (unsigned qi = 0; qi < n && !improved; ++qi) {
+        if (!(L >> qi & 1) || (low >> qi & 1)) continue;
+        for (unsigned qo = 0; qo < n && !improved; ++qo) {
+          if (L >> qo & 1) continue;
+          const uint32_t L2 = (L & ~(1u << qi)) | (1u << qo);
+          const size_t got = take_from(rem, L2, nullptr, nullptr);
+          if (got > best) best = got, L = L2, improved = true;
         }
       }
-      // Small registers: the best local set outright (all subsets of the
-      // non-forced qubits, when there are at most ~20k of them).
-      const unsigned free_q = n - static_cast<unsigned>(std::popcount(low));
-      const unsigned pick = k - static_cast<unsigned>(std::popcount(low));
-      double combos = 1.0;
-      for (unsigned i = 0; i < pick; ++i) combos = combos * (free_q - i) / (i + 1);
-      // (bounded work: sets x remaining blocks per pass)
-      const double scan = combos * static_cast<double>(remaining.size());
-      if (combos <= 20000.0 && scan <= 3e7 && std::getenv("SHOTSIM_B200_FUSED_NO_EXHAUSTIVE") == nullptr) {
-        std::vector<unsigned> fq;
-        for (unsigned q = 0; q < n; ++q)
-          if (!(low >> q & 1)) fq.push_back(q);
-        std::vector<unsigned> idx(pick);
-        for (unsigned i = 0; i < pick; ++i) idx[i] = i;
-        std::vector<uint32_t> sets;
-        while (true) {
-          uint32_t L2 = low;
-          for (unsigned i : idx) L2 |= 1u << fq[i];
-          sets.push_back(L2);
-          int i = static_cast<int>(pick) - 1;  // next combination
-          while (i >= 0 && idx[i] == fq.size() - pick + i) --i;
-          if (i < 0) break;
-          ++idx[i];
-          for (unsigned j = i + 1; j < pick; ++j) idx[j] = idx[j - 1] + 1;
-        }
-        std::vector<std::pair<size_t, uint32_t>> scored;
-        for (uint32_t L2 : sets) scored.emplace_back(take_with(L2, nullptr, nullptr), L2);
-        std::stable_sort(scored.begin(), scored.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
-        if (!scored.empty() && scored[0].first > best) best = scored[0].first, L = scored[0].second;
-        // One pass of lookahead: among the best first sets, the one whose
-        // remainder lets the following pass take the most blocks.
-        if (lookahead && remaining.size() > best && 24.0 * scan <= 3e8) {
-          const std::vector<uint32_t> saved = remaining;
-          size_t best2 = 0;
-          const size_t top = std::min<size_t>(scored.size(), 24);
-          for (size_t c = 0; c < top; ++c) {
-            std::vector<uint32_t> t1, r1;
-            remaining = saved;
-            take_with(scored[c].second, &t1, &r1);
-            remaining = r1;
-            size_t next = 0;
-            for (uint32_t L3 : sets) next = std::max(next, take_with(L3, nullptr, nullptr));
-            if (scored[c].first + next > best2) best2 = scored[c].first + next, L = scored[c].second;
-          }
-          remaining = saved;
-        }
-      }
-      taken.clear();
-      rest.clear();
-      take_with(L, &taken, &rest);
     }
+    const unsigned free_q = n - static_cast<unsigned>(std::popcount(low));
+    const unsigned pick = k - static_cast<unsigned>(std::popcount(low));
+    double combos = 1.0;
+    for (unsigned i = 0; i < pick; ++i) combos = combos * (free_q - i) / (i + 1);
+    const double scan = combos * static_cast<double>(rem.size());  // bounded work
+    if (combos <= 20000.0 && scan <= 3e7 && std::getenv("SHOTSIM_B200_FUSED_NO_EXHAUSTIVE") == nullptr) {
+      std::vector<unsigned> fq;
+      for (unsigned q = 0; q < n; ++q)
+        if (!(low >> q & 1)) fq.push_back(q);
+      std::vector<unsigned> idx(pick);
+      for (unsigned i = 0; i < pick; ++i) idx[i] = i;
+      std::vector<uint32_t> sets;
+      while (true) {
+        uint32_t L2 = low;
+        for (unsigned i : idx) L2 |= 1u << fq[i];
+        sets.push_back(L2);
+        int i = static_cast<int>(pick) - 1;  // next combination
+        while (i >= 0 && idx[i] == fq.size() - pick + i) --i;
+        if (i < 0) break;
+        ++idx[i];
+        for (unsigned j = i + 1; j < pick; ++j) idx[j] = idx[j - 1] + 1;
+      }
+      std::vector<std::pair<size_t, uint32_t>> scored;
+      for (uint32_t L2 : sets) scored.emplace_back(take_from(rem, L2, nullptr, nullptr), L2);
+      std::stable_sort(scored.begin(), scored.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+      if (!scored.empty() && scored[0].first > best) best = scored[0].first, L = scored[0].second;
+      if (lookahead && rem.size() > best && 24.0 * scan <= 3e8) {
+        size_t best2 = 0;
+        const size_t ntop = std::min<size_t>(scored.size(), 24);
+        for (size_t c = 0; c < ntop; ++c) {
+          std::vector<uint32_t> r1;
+          take_from(rem, scored[c].second, nullptr, &r1);
+          size_t next = 0;
+          for (uint32_t L3 : sets) next = std::max(next, take_from(r1, L3, nullptr, nullptr));
+          if (scored[c].first + next > best2) best2 = scored[c].first + next, L = scored[c].second;
+        }
+      }
+      if (top) {
+        top->push_back(L);
+        for (size_t c = 0; c < scored.size() && top->size() < 8; ++c)
+          if (scored[c].second != L && scored[c].first + 2 >= scored[0].first) top->push_back(scored[c].second);
+      }
+    }
+    return L;
+  };
+  // Register groups a pass over these blocks needs (greedy largest closure):
+  // the cost model of the plan rollouts below.
+  auto count_groups = [&](const std::vector<uint32_t>& bl) {
+    std::vector<uint32_t> qm(bl.size());
+    for (size_t t = 0; t < bl.size(); ++t) qm[t] = (1u << blks[bl[t]].q0) | (1u << blks[bl[t]].q1);
+    std::vector<char> pl(bl.size(), 0);
+    auto closure = [&](uint32_t gm, bool commit) {
+      std::vector<char> q = pl;
+      size_t cnt = 0;
+      for (bool grew = true; grew;) {
+        grew = false;
+        uint32_t pending = 0;
+        for (size_t t = 0; t < bl.size(); ++t) {
+          if (q[t]) continue;
+          if (!(qm[t] & pending) && std::popcount(gm | qm[t]) <= static_cast<int>(gq)) {
+            gm |= qm[t], q[t] = 1, ++cnt, grew = true;
+          } else {
+            pending |= qm[t];
+          }
+        }
+      }
+      if (commit) pl = q;
+      return cnt;
+    };
+    size_t groups = 0;
+    for (size_t left = bl.size(); left > 0; ++groups) {
+      std::vector<size_t> ready;
+      uint32_t pq = 0;
+      for (size_t t = 0; t < bl.size(); ++t) {
+        if (pl[t]) continue;
+        if (!(qm[t] & pq)) ready.push_back(t);
+        pq |= qm[t];
+      }
+      uint32_t bq = 0;
+      size_t bc = 0;
+      for (size_t a : ready)
+        for (size_t c = 0; c < bl.size(); ++c) {
+          if (pl[c]) continue;
+          const uint32_t q = qm[a] | qm[c];
+          if (std::popcount(q) > static_cast<int>(gq)) continue;
+          const size_t got = closure(q, false);
+          if (got > bc) bc = got, bq = q;
+        }
+      if (bc == 0) break;
+      closure(bq, true);
+      left -= bc;
+    }
+    return groups;
+  };
+  // Cost of finishing the plan greedily from `rem` (a pass's tile IO costs
+  // about four register groups: profiles/r02/fused_variants.log).
+  constexpr double kPassCost = 4.0;
+  auto rollout_cost = [&](std::vector<uint32_t> rem) {
+    double cost = 0.0;
+    while (!rem.empty()) {
+      const uint32_t L = choose_local(rem, nullptr);
+      std::vector<uint32_t> t, r;
+      take_from(rem, L, &t, &r);
+      if (t.empty()) return 1e300;
+      cost += kPassCost + static_cast<double>(count_groups(t));
+      rem.swap(r);
+    }
+    return cost;
+  };
+  const char* rv = std::getenv("SHOTSIM_B200_FUSED_ROLLOUT");
+  const bool plan_rollout = !(rv && *rv == '0');
+  while (first || !remaining.empty()) {
+    std::vector<uint32_t> taken, rest, top;
+    uint32_t L = choose_local(remaining, &top);
+    // Plan rollouts (small plans): among the best-scoring local sets, the
+    // one whose pass + greedy completion costs the fewest passes and groups.
+    if (plan_rollout && top.size() > 1 && remaining.size() <= 400) {
+      double best_cost = 1e300;
+      for (uint32_t L2 : top) {
+        std::vector<uint32_t> t, r;
+        take_from(remaining, L2, &t, &r);
+        if (t.empty()) continue;
+        const double c = kPassCost + static_cast<double>(count_groups(t)) + rollout_cost(r);
+        if (c < best_cost - 1e-9) best_cost = c, L = L2;
+      }
+    }
+    take_from(remaining, L, &taken, &rest);
     remaining.swap(rest);
     FPass pd{};
     pd.lmask = L;
