@@ -523,6 +523,9 @@ struct SampleGuard {
   uint64_t cap = 0;
 };
 
+// Waves with at least this many shots per SM use 128-thread sampler CTAs.
+constexpr unsigned kSampleSmallCtaShotsPerSm = 8;
+
 void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c, const SampleGuard& g = SampleGuard{}) {
   const unsigned n = dp.host.n;
   const ProgView& P = dp.view;
@@ -530,9 +533,15 @@ void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c, const Sampl
     // Chunked exact parallel sampler (sample_exact_kernel), one CTA per shot.
     for (uint64_t off = 0; off < c.S; off += (1u << 30)) {
       const SegCtx cc = c.sub(off, std::min<uint64_t>(1u << 30, c.S - off), n);
-      sample_exact_kernel<<<static_cast<unsigned>(cc.S), SAMPLE_NT, 0, E->stream>>>(
-          P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs, E->serial_chunks, E->err, sample_force_serial(),
-          g.err, g.count, g.ids, g.cap);
+      // many shots: 128-thread CTAs (more shots in flight per SM); few: 256
+      if (cc.S >= uint64_t{kSampleSmallCtaShotsPerSm} * E->num_sms)
+        sample_exact_kernel<128><<<static_cast<unsigned>(cc.S), 128, 0, E->stream>>>(
+            P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs, E->serial_chunks, E->err, sample_force_serial(),
+            g.err, g.count, g.ids, g.cap);
+      else
+        sample_exact_kernel<256><<<static_cast<unsigned>(cc.S), 256, 0, E->stream>>>(
+            P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs, E->serial_chunks, E->err, sample_force_serial(),
+            g.err, g.count, g.ids, g.cap);
       launched(E);
     }
     return;
