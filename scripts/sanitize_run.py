@@ -20,6 +20,8 @@ cases = [
     ("qv14 fused fma", cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise(), "batch", 4, {"fused_matrices": True}),
     ("qv14 fused fma 12-qubit tiles", cc.quantum_volume(14, depth=2, seed=1), cc.qv_noise(), "batch", 4,
      {"fused_matrices": True, "tile_qubits": 12}),
+    ("qv12 fused many shots (128-thread sampler CTAs)", cc.quantum_volume(12, depth=2, seed=1), cc.qv_noise(),
+     "batch", 1200, {"fused_matrices": True, "resident_max_qubits": 1}),
     ("rnd13 kraus streamed", cc.random_layers(13, depth=2, seed=3), cc.thermal_noise(0.05, 0.1), "batch", 4,
      {"resident_max_qubits": 1, "tile_qubits": 11}),
     ("rnd14 kraus streamed epilogue (several tiles per CTA)", cc.random_layers(14, depth=2, seed=4),
