@@ -56,6 +56,9 @@ __device__ __forceinline__ double2 cfma(double2 m, double2 a, double2 acc) {
 
 // y = M x on the four register quads of a hexad whose matrix bits are group
 // bits B0 < B1 (the other two group bits enumerate the quads).
+// Largest register for which the fused pass prefetches the next tile into L2.
+constexpr unsigned kFusedPrefetchMaxQubits = 20;
+
 // M: a register array double2[16] or a pointer (shared / constant memory).
 template <int B0, int B1, class M>
 __device__ __forceinline__ void apply_hexad(double2 (&a)[16], const M& m) {
@@ -365,7 +368,10 @@ __device__ __forceinline__ void fused_pass_body(FusedView F, uint32_t pass_index
                            "l"(tb + o[j]));
         }
 #ifndef SSB_FUSED_NO_PREFETCH
-        if (t + 1 < t_end) {  // the next tile's lines on their way to L2
+        // the next tile's lines on their way to L2 — on registers of up to 20
+        // qubits (C2 +1%; C5's 24 qubits run 2% faster without it,
+        // profiles/r02/fused_variants.log)
+        if (t + 1 < t_end && n <= kFusedPrefetchMaxQubits) {
           const double2* nb = seg + pdep_positions(t + 1, hpos, n - k) + lo_part;
           for (uint32_t i = 0; i < per; i += 4) {
             const uint4 h = *reinterpret_cast<const uint4*>(hi_off + i);
