@@ -533,15 +533,23 @@ void sample_terminal(ssb_engine* E, DevProgram& dp, const SegCtx& c, const Sampl
     // Chunked exact parallel sampler (sample_exact_kernel), one CTA per shot.
     for (uint64_t off = 0; off < c.S; off += (1u << 30)) {
       const SegCtx cc = c.sub(off, std::min<uint64_t>(1u << 30, c.S - off), n);
-      // many shots: 128-thread CTAs (more shots in flight per SM); few: 256
-      if (cc.S >= uint64_t{kSampleSmallCtaShotsPerSm} * E->num_sms)
-        sample_exact_kernel<128><<<static_cast<unsigned>(cc.S), 128, 0, E->stream>>>(
-            P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs, E->serial_chunks, E->err, sample_force_serial(),
-            g.err, g.count, g.ids, g.cap);
-      else
-        sample_exact_kernel<256><<<static_cast<unsigned>(cc.S), 256, 0, E->stream>>>(
-            P, cc.state, cc.S, cc.seed, cc.ids, cc.begin, cc.cregs, E->serial_chunks, E->err, sample_force_serial(),
-            g.err, g.count, g.ids, g.cap);
+      // many shots: 128-thread CTAs (more shots in flight per SM); fewer: 256;
+      // fewer shots than SMs: 512 (each shot's chunk loop gets the threads:
+      // C5 107 -> 114 shots/s; SHOTSIM_B200_SAMPLE_FEW_NT=256/1024 for A/B)
+      const char* fe = std::getenv("SHOTSIM_B200_SAMPLE_FEW_NT");
+      const unsigned few = fe && std::string(fe) == "256" ? 256u : fe && std::string(fe) == "1024" ? 1024u : 512u;
+      const unsigned snt = cc.S >= uint64_t{kSampleSmallCtaShotsPerSm} * E->num_sms ? 128u
+                           : cc.S >= uint64_t(E->num_sms)                             ? 256u
+                                                                                      : few;
+      auto launch = [&](auto kern, unsigned nt) {
+        kern<<<static_cast<unsigned>(cc.S), nt, 0, E->stream>>>(P, cc.state, cc.S, cc.seed, cc.ids, cc.begin,
+                                                               cc.cregs, E->serial_chunks, E->err,
+                                                               sample_force_serial(), g.err, g.count, g.ids, g.cap);
+      };
+      if (snt == 128) launch(sample_exact_kernel<128>, 128);
+      else if (snt == 512) launch(sample_exact_kernel<512>, 512);
+      else if (snt == 1024) launch(sample_exact_kernel<1024>, 1024);
+      else launch(sample_exact_kernel<256>, 256);
       launched(E);
     }
     return;

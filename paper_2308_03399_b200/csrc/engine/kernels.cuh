@@ -1021,9 +1021,10 @@ static __global__ void g_sample_scan_kernel(ProgView P, const double2* st, uint6
 #endif
 constexpr uint32_t SAMPLE_CHUNK = SSB_SAMPLE_CHUNK;
 // Threads per shot (one CTA per shot): 128 when a wave has many shots (more
-// shots in flight per SM hide the chunk loop's latency: C2 +4.8%), 256 when
-// it has few (each shot's chunks need the threads: C5 -10% at 128);
-// sample_terminal picks (profiles/r02/fused_variants.log).
+// shots in flight per SM hide the chunk loop's latency: C2 +4.8%), 256 for
+// fewer, 512 when there are fewer shots than SMs (each shot's chunks need
+// the threads: C5 +6%); sample_terminal picks
+// (profiles/r02/fused_variants.log).
 template <uint32_t SAMPLE_NT>
 static __global__ void __launch_bounds__(SAMPLE_NT) sample_exact_kernel(ProgView P, const double2* st, uint64_t S,
                                                                         uint64_t seed, const uint64_t* ids,
